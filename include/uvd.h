@@ -1,0 +1,251 @@
+/*
+ * uvd.h — C-ABI of the B200-native irradiance-matrix engine (libuvd.so).
+ *
+ * The hot path of arXiv 2103.14137 "Optimized Coverage Planning for UV Surface
+ * Disinfection" (SURVEY §8(a) rows a1–a8): assemble the occlusion-tested
+ * irradiance matrix A[patch i, vantage configuration j] (§IV-C, PAPER.md
+ * P:223–254), then the fluence products A·t and Aᵀ·y (Eq. 5; the
+ * LP of Eq. 8/9) and the area coverage (P:9).
+ *
+ * Conventions: lengths in metres, power in W, time in s,
+ * irradiance in W/m², fluence in J/m².  Citations: P:n = PAPER.md line n,
+ * S:n = SPEC.md line n, Q# = reading n in DESIGN.md §Readings.
+ *
+ * Ownership: the caller owns every input; the library copies what it needs
+ * during the call and retains no caller pointer.  A scene owns its device
+ * buffers (allocated through the uvd_allocator, default cudaMallocAsync) and
+ * releases them in uvd_scene_destroy.  Outputs are caller-allocated DEVICE
+ * buffers unless a parameter says "host".
+ *
+ * Streams: every call enqueues on `stream` (a cudaStream_t, NULL = legacy
+ * default stream).  Calls that return host scalars synchronise that stream:
+ * uvd_scene_create, uvd_vantage_sample, uvd_sync_status, uvd_coverage.
+ * A scene is immutable after creation; concurrent const calls are safe.
+ *
+ * Errors: no exception crosses the ABI.  Calls return UVD_OK (0) or a
+ * negative uvd_status and set a thread-local message (uvd_last_error).  On
+ * error, outputs are unspecified.  In-kernel domain errors (lamp–centroid
+ * distance < 1e-9 m) set a per-scene device flag reported by
+ * uvd_sync_status.
+ */
+#ifndef UVD_H_
+#define UVD_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define UVD_API __attribute__((visibility("default")))
+#else
+#define UVD_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  UVD_OK = 0,
+  UVD_ERR_INVALID = -1,   /* bad argument / non-finite input / zero-area triangle */
+  UVD_ERR_DOMAIN = -2,    /* lamp–centroid distance < 1e-9 m                    */
+  UVD_ERR_EMPTY = -3,     /* zero feasible vantage configurations               */
+  UVD_ERR_CAPACITY = -4,  /* caller buffer too small; required size returned            */
+  UVD_ERR_NOMEM = -5,     /* device allocation failed                                    */
+  UVD_ERR_CUDA = -6       /* CUDA runtime failure (message = cudaGetErrorString)          */
+} uvd_status;
+
+/* Optional device allocator (e.g. bound to PyTorch's caching allocator).
+ * alloc returns a device pointer (NULL on failure); free releases it.
+ * Both are called on the creating thread, stream-ordered on `stream`. */
+typedef struct {
+  void* (*alloc)(size_t bytes, int device, void* stream, void* ctx);
+  void (*free)(void* ptr, int device, void* stream, void* ctx);
+  void* ctx;
+} uvd_allocator;
+
+/* ------------------------------------------------------------------ a1/a2 */
+typedef struct uvd_scene uvd_scene;     /* opaque, immutable after create */
+
+enum { UVD_SCENE_TRIMESH = 0, UVD_SCENE_EXTRUDED = 1 };
+
+/* A simple polygon, CCW, n >= 3 vertices xy[2n] (host memory). */
+typedef struct {
+  const float* xy;
+  int32_t n;
+} uvd_polygon;
+
+/* Scene description (pointers are HOST memory unless device_input != 0).
+ *  TRIMESH  ("simplicial complex with N triangles"): vertices[n_vertices*3]
+ *           fp32, tris[n_tris*3] int32 (0-based, right-hand winding gives the
+ *           outward normal n(s), Q14).  Patch i = triangle.
+ *  EXTRUDED (2.5D world): room bounds {x0,y0,x1,y1}, wall height
+ *           h, obstacle polygons strictly inside the bounds, patch resolution
+ *           res.  Walls = the bounds' 4 edges (CCW) then each polygon's edges in
+ *           order; each wall of length len is split into ceil(len/res) equal
+ *           patches, patch = vertical rectangle (2 triangles). */
+typedef struct {
+  int32_t kind;
+  const float* vertices;
+  int64_t n_vertices;
+  const int32_t* tris;
+  int64_t n_tris;
+  float bounds[4];
+  float wall_height;
+  const uvd_polygon* obstacles;
+  int32_t n_obstacles;
+  float patch_res;
+  int32_t device_input;   /* TRIMESH: 1 = vertices/tris are DEVICE pointers on `device` */
+} uvd_scene_desc;
+
+/* Build a scene on `device`: copy the input, compute the canonical patch
+ * attributes (a1), build the LBVH over all triangles (a2: Morton codes, radix
+ * sort, Karras hierarchy, bottom-up refit).  Synchronises `stream`.
+ * Canonical patch attributes (fp64 arithmetic, rounded once to fp32):
+ *   3D : c = fl32((a+b+c)/3), n = fl32(cross(b-a,c-a)/|.|), area = |cross|/2;
+ *   2.5D: q_s = fl32(e0 + ((e1-e0)*s)/n_seg) (q_nseg = e1), c = fl32((q_s+q_{s+1})/2, h/2),
+ *         n = (-dy,dx)/len for boundary walls (into the room), (dy,-dx)/len for
+ *         obstacle walls (out of the obstacle), area = len*h.
+ * Patch (row) order: 2.5D = wall order; 3D = LBVH leaf (Morton) order, with
+ * orig_id mapping back to the input triangle index.
+ * Errors: INVALID (non-finite vertex, index out of range, zero-area triangle,
+ * polygon outside bounds / n<3, res<=0, h<=0), NOMEM, CUDA. */
+UVD_API int uvd_scene_create(const uvd_scene_desc* desc, int device, void* stream,
+                     const uvd_allocator* allocator, uvd_scene** out);
+
+/* Host scalars: number of patches N (rows of A), number of triangles M,
+ * bbox {xmin,ymin,zmin,xmax,ymax,zmax} of all vertices, total patch area. */
+UVD_API int uvd_scene_query(const uvd_scene* scene, int64_t* n_patches, int64_t* n_tris, float bbox[6],
+                    double* total_area);
+
+/* Copy the canonical patch attributes into caller DEVICE buffers (any may be
+ * NULL): centroid[N*3], normal[N*3] fp32, area[N] fp64, orig_id[N] int64. */
+UVD_API int uvd_scene_patches(const uvd_scene* scene, float* centroid, float* normal, double* area,
+                      int64_t* orig_id, void* stream);
+
+UVD_API void uvd_scene_destroy(uvd_scene* scene);
+
+/* ---------------------------------------------------------------------- a3 */
+enum { UVD_ROBOT_DISC2D = 0, UVD_ROBOT_TOWER = 1, UVD_ROBOT_FLOAT3D = 2, UVD_ROBOT_ARM = 3 };
+
+/* Vantage sampling.  Cell-centred grid of spacing ρ:
+ * x = lo + (a + 1/2)ρ, a = 0..floor((hi-lo)/ρ)-1 (Q9), candidates ordered x
+ * fastest, then y, then z.
+ *  DISC2D  (EXTRUDED scenes; planar disc robot): grid over the bounds at
+ *          z = lamp_z; feasible iff inside the bounds, 2D distance to every wall
+ *          >= clearance and outside every obstacle polygon.
+ *  FLOAT3D (TRIMESH; Floatbot): grid over the mesh bbox; feasible iff the
+ *          point is >= clearance from every triangle and in free space (Q20).
+ *  TOWER   (TRIMESH; Towerbot): floor grid over the bbox xy; lamp_samples
+ *          points z_l = lamp_z0 + (l+1/2)(lamp_z1-lamp_z0)/L (Q11); feasible
+ *          iff every sample is >= clearance from every triangle and sample 0 is free.
+ *  ARM     (TRIMESH; Armbot proxy, Q12): grid over bbox xy × [zmin,zmax]; feasible
+ *          iff >= clearance, free, and within `reach` (3D) of a feasible base: floor
+ *          grid point at z = base_z that is >= base_clearance and free.
+ * Free space (Q20): the nearest triangle hit along p + t(0.0123, 0.0371, 1), t>0,
+ * exists and is front-facing.
+ * Output: lamp_xyz[cap * L * 3] fp32 DEVICE (L = lamp_samples for TOWER, else 1),
+ * raw_index[cap] int64 DEVICE (optional), *out_k HOST = number of feasible
+ * configurations.  If K > cap: returns UVD_ERR_CAPACITY with *out_k = K and
+ * nothing written (call with cap = 0 to size).  K == 0: UVD_ERR_EMPTY.
+ * Synchronises `stream`. */
+typedef struct {
+  int32_t robot;
+  float spacing, clearance;
+  float lamp_z, lamp_z0, lamp_z1;
+  float reach, zmin, zmax;
+  int32_t lamp_samples;
+  float base_clearance, base_z;
+} uvd_vantage_opts;
+
+UVD_API int uvd_vantage_sample(const uvd_scene* scene, const uvd_vantage_opts* opts, float* lamp_xyz,
+                       int64_t* raw_index, int64_t cap, int64_t* out_k, void* stream);
+
+/* ------------------------------------------------------------------ a4–a6 */
+/* Lamp model: total radiant flux P split over L = samples_per_config
+ * isotropic point samples of power P/L each. */
+typedef struct {
+  double power_w;
+  int32_t samples_per_config;
+} uvd_lamp;
+
+enum { UVD_DENSE_COLMAJOR = 0, UVD_CSC = 1 };
+
+/* Matrix output (all DEVICE pointers).
+ *  DENSE_COLMAJOR: values[n_cols * ld] fp32; local column c occupies
+ *                  values[c*ld .. c*ld + N); rows N..ld-1 are written as 0.
+ *                  ld >= N and ld % 32 == 0 (torch shape (n_cols, ld)).
+ *  CSC:            colptr[n_cols+1] int64, rowidx[nnz_cap] int32, values[nnz_cap]
+ *                  fp32, rows ascending within a column; entries are the nonzero
+ *                  A[i,j].  Two-phase: if nnz > nnz_cap the call returns
+ *                  UVD_ERR_CAPACITY after writing colptr (colptr[n_cols] = nnz).
+ *  vis_bits  (optional): [n_cols][L][ceil(N/32)] uint32, bit (i%32) of word i/32 =
+ *            patch i front-facing and unoccluded from lamp sample l.
+ *  col_sumsq (optional): [n_cols] fp64 Σ_i A[i,c]² (for ‖A‖_F).
+ *  counters  (optional): 4 uint64 accumulated by the call (instrumented,
+ *            slower path, for the roofline accounting): [0] front-facing rays
+ *            that entered traversal, [1] per-ray child-box tests, [2] per-ray
+ *            triangle tests, [3] warp node fetches. */
+typedef struct {
+  int32_t format;
+  int64_t ld;
+  float* values;
+  int64_t* colptr;
+  int32_t* rowidx;
+  int64_t nnz_cap;
+  uint32_t* vis_bits;
+  double* col_sumsq;
+  unsigned long long* counters;
+} uvd_matrix_out;
+
+/* Assemble columns of A (a4 cull, a5 occlusion, a6 Eq. 7):
+ *   A[i,j] = Σ_l vis_ijl · (P/L) · <p_jl - c_i, n_i> / (4π |p_jl - c_i|³)
+ * (fp64, rounded once to fp32), vis_ijl = [<p_jl - c_i, n_i> > 0] and no scene
+ * triangle other than patch i's own meets the open segment p_jl -> c_i at
+ * t ∈ (1e-4/d, 1 - 1e-4/d) (inclusive triangle edges; Q5–Q8, Q15).
+ * lamp_xyz: DEVICE [k_total * L * 3] (configuration j -> samples j*L .. j*L+L-1).
+ * cols: HOST [n_cols] global configuration ids of this call's columns (local
+ * column c <-> cols[c]); NULL means all, n_cols = k_total.  Asynchronous;
+ * call uvd_sync_status to collect in-kernel DOMAIN errors. */
+UVD_API int uvd_irradiance_matrix(const uvd_scene* scene, const float* lamp_xyz, int64_t k_total,
+                          const int64_t* cols, int64_t n_cols, const uvd_lamp* lamp,
+                          uvd_matrix_out* out, void* stream);
+
+/* Synchronise `stream` and report (then clear) the scene's in-kernel error flag:
+ * UVD_OK or UVD_ERR_DOMAIN. */
+UVD_API int uvd_sync_status(const uvd_scene* scene, void* stream);
+
+/* ---------------------------------------------------------------------- a7 */
+/* Fluence products on a local column shard (Eq. 5), fp64 accumulation:
+ *  transpose = 0:  out[n] = A · x      (x = dwell times t[k], s; out = μ, J/m²)
+ *  transpose = 1:  out[k] = Aᵀ · x     (x = y[n]; out = g)
+ * A is a uvd_matrix_out previously filled by uvd_irradiance_matrix (dense or CSC),
+ * n = number of patches, k = number of local columns.  x, out DEVICE fp64.
+ * For A·t, columns with t_k == 0 are skipped.  Summation order is fixed
+ * (deterministic).  Asynchronous. */
+UVD_API int uvd_fluence(const uvd_matrix_out* A, int64_t n, int64_t k, int transpose, const double* x,
+                double* out, void* stream);
+
+/* ---------------------------------------------------------------------- a8 */
+/* Coverage (P:9 "fraction of the surface area"):
+ *   out[0] = Σ_i |s_i| [μ_i >= μ_min]      (covered area, inclusive, Q16)
+ *   out[1] = Σ_i |s_i|                     (total area)
+ *   out[2] = Σ_i |s_i| [a_rowsum_i > 0]    (ever-visible area; = out[1] if NULL)
+ * mu, a_rowsum: DEVICE fp64 [N] in canonical patch order.  out: HOST.
+ * Deterministic reduction order.  Synchronises `stream`. */
+UVD_API int uvd_coverage(const uvd_scene* scene, const double* mu, double mu_min, const double* a_rowsum,
+                 double out[3], void* stream);
+
+/* Thread-local message of the last failing call on this thread ("" if none). */
+UVD_API const char* uvd_last_error(void);
+
+/* Library version (major*10000 + minor*100 + patch). */
+UVD_API int uvd_version(void);
+
+/* Number of CUDA kernels this library has launched in this process (all
+ * devices, all threads) — for launch accounting in benchmarks. */
+UVD_API unsigned long long uvd_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* UVD_H_ */

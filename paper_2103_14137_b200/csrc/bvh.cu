@@ -1,0 +1,384 @@
+// bvh.cu — GPU LBVH build (BASELINE north_star "GPU LBVH
+// build (Morton codes, radix sort, Karras hierarchy)").
+//
+//   k_morton    63-bit Morton code of each triangle centroid in the scene bbox
+//   radix sort  hand-written LSD sort of (u64 key, u32 value), 8-bit digits,
+//               stable block-local ranking with warp match/ballot
+//   k_karras    internal-node topology from longest common prefixes
+//               (Karras 2012; equal keys broken by index)
+//   k_refit     bottom-up AABBs with atomic arrival counters
+//   k_emit      BVH2 nodes holding both child boxes (64 B), subtrees of
+//               <= kLeafMax triangles collapsed into leaf ranges, boxes padded
+//               outward so fp32 slab tests are conservative for the fp64 ray.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "uvd_internal.cuh"
+
+namespace uvd {
+
+// ----------------------------------------------------------------- morton --
+__device__ __forceinline__ uint64_t spread21(uint32_t v) {
+  uint64_t x = v & 0x1fffffu;
+  x = (x | x << 32) & 0x1f00000000ffffull;
+  x = (x | x << 16) & 0x1f0000ff0000ffull;
+  x = (x | x << 8) & 0x100f00f00f00f00full;
+  x = (x | x << 4) & 0x10c30c30c30c30c3ull;
+  x = (x | x << 2) & 0x1249249249249249ull;
+  return x;
+}
+
+__global__ void k_morton(const float4* __restrict__ tri_in, int64_t M, float3 lo, float3 inv_ext,
+                         uint64_t* __restrict__ keys, uint32_t* __restrict__ vals) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= M) return;
+  float4 a = tri_in[3 * t], b = tri_in[3 * t + 1], c = tri_in[3 * t + 2];
+  float cx = (a.x + b.x + c.x) * (1.0f / 3.0f);
+  float cy = (a.y + b.y + c.y) * (1.0f / 3.0f);
+  float cz = (a.z + b.z + c.z) * (1.0f / 3.0f);
+  const float scale = 2097151.0f;  // 2^21 - 1
+  uint32_t ix = (uint32_t)fminf(fmaxf((cx - lo.x) * inv_ext.x * scale, 0.f), scale);
+  uint32_t iy = (uint32_t)fminf(fmaxf((cy - lo.y) * inv_ext.y * scale, 0.f), scale);
+  uint32_t iz = (uint32_t)fminf(fmaxf((cz - lo.z) * inv_ext.z * scale, 0.f), scale);
+  keys[t] = (spread21(ix) << 2) | (spread21(iy) << 1) | spread21(iz);
+  vals[t] = (uint32_t)t;
+}
+
+// ------------------------------------------------------------- radix sort --
+constexpr int kSortThreads = 256;
+constexpr int kSortItems = 16;
+constexpr int kSortTile = kSortThreads * kSortItems;
+constexpr int kSortWarps = kSortThreads / 32;
+
+__global__ void __launch_bounds__(kSortThreads) k_hist(const uint64_t* __restrict__ keys, int64_t n,
+                                                       int shift, uint32_t* __restrict__ counts,
+                                                       int nblocks) {
+  __shared__ uint32_t h[256];
+  h[threadIdx.x] = 0;
+  __syncthreads();
+  int64_t base = (int64_t)blockIdx.x * kSortTile;
+  for (int r = 0; r < kSortItems; ++r) {
+    int64_t i = base + r * kSortThreads + threadIdx.x;
+    if (i < n) atomicAdd(&h[(keys[i] >> shift) & 255u], 1u);
+  }
+  __syncthreads();
+  counts[(int64_t)threadIdx.x * nblocks + blockIdx.x] = h[threadIdx.x];
+}
+
+// exclusive scan of `n` uint32 in place, one block of 1024 threads
+__global__ void __launch_bounds__(1024) k_scan_excl(uint32_t* __restrict__ a, int64_t n) {
+  __shared__ uint32_t part[1024];
+  int64_t per = (n + 1023) / 1024;
+  int64_t s = threadIdx.x * per, e = s + per < n ? s + per : n;
+  uint32_t sum = 0;
+  for (int64_t i = s; i < e; ++i) sum += a[i];
+  part[threadIdx.x] = sum;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {
+    uint32_t v = threadIdx.x >= off ? part[threadIdx.x - off] : 0;
+    __syncthreads();
+    part[threadIdx.x] += v;
+    __syncthreads();
+  }
+  uint32_t run = threadIdx.x ? part[threadIdx.x - 1] : 0;
+  for (int64_t i = s; i < e; ++i) {
+    uint32_t v = a[i];
+    a[i] = run;
+    run += v;
+  }
+}
+
+__global__ void __launch_bounds__(kSortThreads) k_scatter(const uint64_t* __restrict__ kin,
+                                                          const uint32_t* __restrict__ vin,
+                                                          uint64_t* __restrict__ kout,
+                                                          uint32_t* __restrict__ vout, int64_t n,
+                                                          int shift,
+                                                          const uint32_t* __restrict__ offsets,
+                                                          int nblocks) {
+  __shared__ uint32_t base[256];
+  __shared__ uint32_t wcnt[kSortWarps][256];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  base[threadIdx.x] = offsets[(int64_t)threadIdx.x * nblocks + blockIdx.x];
+  for (int w = 0; w < kSortWarps; ++w) wcnt[w][threadIdx.x] = 0;
+  __syncthreads();
+  const uint32_t lt_mask = (1u << lane) - 1u;
+  int64_t tile = (int64_t)blockIdx.x * kSortTile;
+  for (int r = 0; r < kSortItems; ++r) {
+    int64_t i = tile + r * kSortThreads + threadIdx.x;
+    bool valid = i < n;
+    uint64_t k = valid ? kin[i] : 0;
+    uint32_t v = valid ? vin[i] : 0;
+    uint32_t dg = valid ? (uint32_t)((k >> shift) & 255u) : 256u + lane;
+    uint32_t peers = __match_any_sync(0xffffffffu, dg);
+    uint32_t rank = __popc(peers & lt_mask);
+    if (valid && rank == 0) wcnt[warp][dg] = __popc(peers);
+    __syncthreads();
+    {  // per-digit prefix over warps (thread = digit)
+      uint32_t run = base[threadIdx.x];
+      for (int w = 0; w < kSortWarps; ++w) {
+        uint32_t c = wcnt[w][threadIdx.x];
+        wcnt[w][threadIdx.x] = run;
+        run += c;
+      }
+      base[threadIdx.x] = run;
+    }
+    __syncthreads();
+    if (valid) {
+      uint32_t pos = wcnt[warp][dg] + rank;
+      kout[pos] = k;
+      vout[pos] = v;
+    }
+    __syncthreads();
+    for (int w = 0; w < kSortWarps; ++w) wcnt[w][threadIdx.x] = 0;
+    __syncthreads();
+  }
+}
+
+int sort_pairs_u64(uint64_t* keys, uint32_t* vals, int64_t n, Alloc& al, cudaStream_t st) {
+  if (n <= 1) return UVD_OK;
+  int nblocks = (int)((n + kSortTile - 1) / kSortTile);
+  uint64_t* k2 = (uint64_t*)al.get(n * sizeof(uint64_t));
+  uint32_t* v2 = (uint32_t*)al.get(n * sizeof(uint32_t));
+  uint32_t* cnt = (uint32_t*)al.get((size_t)256 * nblocks * sizeof(uint32_t));
+  if (!k2 || !v2 || !cnt) {
+    set_error("sort: out of device memory (n=%lld)", (long long)n);
+    return UVD_ERR_NOMEM;
+  }
+  uint64_t *ka = keys, *kb = k2;
+  uint32_t *va = vals, *vb = v2;
+  for (int pass = 0; pass < 8; ++pass) {   // 8 x 8 bits covers the 63-bit codes
+    int shift = pass * 8;
+    k_hist<<<nblocks, kSortThreads, 0, st>>>(ka, n, shift, cnt, nblocks);
+    note_launch();
+    k_scan_excl<<<1, 1024, 0, st>>>(cnt, (int64_t)256 * nblocks);
+    note_launch();
+    k_scatter<<<nblocks, kSortThreads, 0, st>>>(ka, va, kb, vb, n, shift, cnt, nblocks);
+    note_launch();
+    uint64_t* tk = ka; ka = kb; kb = tk;
+    uint32_t* tv = va; va = vb; vb = tv;
+  }
+  // 8 passes: the result is back in (keys, vals)
+  UVD_CUDA_TRY(cudaGetLastError());
+  al.put(k2);
+  al.put(v2);
+  al.put(cnt);
+  return UVD_OK;
+}
+
+// ----------------------------------------------------------------- karras --
+__device__ __forceinline__ int delta(const uint64_t* __restrict__ k, int64_t n, int64_t i, int64_t j) {
+  if (j < 0 || j >= n) return -1;
+  uint64_t a = k[i], b = k[j];
+  if (a == b) return 64 + __clzll((unsigned long long)(i ^ j));
+  return __clzll((unsigned long long)(a ^ b));
+}
+
+// internal node i in [0, n-2]: range [first,last], children as refs into
+// (internal: idx, leaf: 0x80000000|idx) -> int32 arrays
+__global__ void k_karras(const uint64_t* __restrict__ keys, int64_t n, int32_t* __restrict__ left,
+                         int32_t* __restrict__ right, int32_t* __restrict__ rfirst,
+                         int32_t* __restrict__ rlast, int32_t* __restrict__ parent_int,
+                         int32_t* __restrict__ parent_leaf) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n - 1) return;
+  int d = delta(keys, n, i, i + 1) - delta(keys, n, i, i - 1) >= 0 ? 1 : -1;
+  int dmin = delta(keys, n, i, i - d);
+  int64_t lmax = 2;
+  while (delta(keys, n, i, i + lmax * d) > dmin) lmax <<= 1;
+  int64_t l = 0;
+  for (int64_t t = lmax >> 1; t >= 1; t >>= 1)
+    if (delta(keys, n, i, i + (l + t) * d) > dmin) l += t;
+  int64_t j = i + l * d;
+  int dnode = delta(keys, n, i, j);
+  int64_t s = 0;
+  int64_t len = l;
+  // binary search for the split: largest s with delta(i, i+s*d) > dnode
+  int64_t t = len;
+  do {
+    t = (t + 1) >> 1;
+    if (s + t < len + 1 && delta(keys, n, i, i + (s + t) * d) > dnode) s += t;
+  } while (t > 1);
+  int64_t gamma = i + s * d + (d < 0 ? -1 : 0);
+  int64_t first = d > 0 ? i : j, last = d > 0 ? j : i;
+  int32_t lc, rc;
+  if (first == gamma) { lc = (int32_t)(0x80000000u | (uint32_t)gamma); parent_leaf[gamma] = (int32_t)i; }
+  else { lc = (int32_t)gamma; parent_int[gamma] = (int32_t)i; }
+  if (last == gamma + 1) { rc = (int32_t)(0x80000000u | (uint32_t)(gamma + 1)); parent_leaf[gamma + 1] = (int32_t)i; }
+  else { rc = (int32_t)(gamma + 1); parent_int[gamma + 1] = (int32_t)i; }
+  left[i] = lc;
+  right[i] = rc;
+  rfirst[i] = (int32_t)first;
+  rlast[i] = (int32_t)last;
+}
+
+struct Box { float lx, ly, lz, hx, hy, hz; };
+
+__device__ __forceinline__ Box tri_box(const float4* __restrict__ tri, int64_t r) {
+  float4 a = tri[3 * r], b = tri[3 * r + 1], c = tri[3 * r + 2];
+  Box x;
+  x.lx = fminf(a.x, fminf(b.x, c.x)); x.hx = fmaxf(a.x, fmaxf(b.x, c.x));
+  x.ly = fminf(a.y, fminf(b.y, c.y)); x.hy = fmaxf(a.y, fmaxf(b.y, c.y));
+  x.lz = fminf(a.z, fminf(b.z, c.z)); x.hz = fmaxf(a.z, fmaxf(b.z, c.z));
+  return x;
+}
+__device__ __forceinline__ Box join(Box a, Box b) {
+  Box x;
+  x.lx = fminf(a.lx, b.lx); x.ly = fminf(a.ly, b.ly); x.lz = fminf(a.lz, b.lz);
+  x.hx = fmaxf(a.hx, b.hx); x.hy = fmaxf(a.hy, b.hy); x.hz = fmaxf(a.hz, b.hz);
+  return x;
+}
+
+__device__ __forceinline__ Box load_box(const float* __restrict__ bx, int64_t i) {
+  const volatile float* p = bx + 6 * i;
+  Box x;
+  x.lx = p[0]; x.ly = p[1]; x.lz = p[2]; x.hx = p[3]; x.hy = p[4]; x.hz = p[5];
+  return x;
+}
+__device__ __forceinline__ void store_box(float* bx, int64_t i, Box x) {
+  volatile float* p = bx + 6 * i;
+  p[0] = x.lx; p[1] = x.ly; p[2] = x.lz; p[3] = x.hx; p[4] = x.hy; p[5] = x.hz;
+}
+
+__global__ void k_refit(const float4* __restrict__ tri, int64_t n, const int32_t* __restrict__ left,
+                        const int32_t* __restrict__ right, const int32_t* __restrict__ parent_int,
+                        const int32_t* __restrict__ parent_leaf, float* __restrict__ ibox,
+                        int* __restrict__ arrive) {
+  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  int64_t p = parent_leaf[r];
+  while (p >= 0) {
+    __threadfence();
+    if (atomicAdd(&arrive[p], 1) == 0) return;  // first child to arrive stops
+    __threadfence();
+    int32_t lc = left[p], rc = right[p];
+    Box bl = lc < 0 ? tri_box(tri, (int64_t)(lc & 0x7fffffff)) : load_box(ibox, lc);
+    Box br = rc < 0 ? tri_box(tri, (int64_t)(rc & 0x7fffffff)) : load_box(ibox, rc);
+    store_box(ibox, p, join(bl, br));
+    p = p == 0 ? -1 : parent_int[p];
+  }
+}
+
+__device__ __forceinline__ float pad_lo(float x) { return x - (1e-5f + 1e-6f * fabsf(x)); }
+__device__ __forceinline__ float pad_hi(float x) { return x + (1e-5f + 1e-6f * fabsf(x)); }
+
+__device__ __forceinline__ void child_info(const float4* __restrict__ tri, const float* __restrict__ ibox,
+                                           const int32_t* __restrict__ rfirst,
+                                           const int32_t* __restrict__ rlast, int32_t c, Box* b,
+                                           uint32_t* ref) {
+  if (c < 0) {
+    int64_t r = c & 0x7fffffff;
+    *b = tri_box(tri, r);
+    *ref = make_leaf((uint32_t)r, 1u);
+  } else {
+    *b = load_box(ibox, c);
+    int32_t f = rfirst[c], l = rlast[c];
+    int32_t cnt = l - f + 1;
+    *ref = cnt <= kLeafMax ? make_leaf((uint32_t)f, (uint32_t)cnt) : (uint32_t)c;
+  }
+}
+
+__global__ void k_emit(const float4* __restrict__ tri, int64_t n, const int32_t* __restrict__ left,
+                       const int32_t* __restrict__ right, const int32_t* __restrict__ rfirst,
+                       const int32_t* __restrict__ rlast, const float* __restrict__ ibox,
+                       Node* __restrict__ nodes) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n - 1) return;
+  Box b0, b1;
+  uint32_t r0, r1;
+  child_info(tri, ibox, rfirst, rlast, left[i], &b0, &r0);
+  child_info(tri, ibox, rfirst, rlast, right[i], &b1, &r1);
+  Node nd;
+  nd.a = make_float4(pad_lo(b0.lx), pad_hi(b0.hx), pad_lo(b0.ly), pad_hi(b0.hy));
+  nd.b = make_float4(pad_lo(b1.lx), pad_hi(b1.hx), pad_lo(b1.ly), pad_hi(b1.hy));
+  nd.c = make_float4(pad_lo(b0.lz), pad_hi(b0.hz), pad_lo(b1.lz), pad_hi(b1.hz));
+  nd.d = make_uint4(r0, r1, 0u, 0u);
+  nodes[i] = nd;
+}
+
+// single-leaf scene (M <= kLeafMax): a root node with one leaf child and an
+// empty second child
+__global__ void k_emit_small(const float4* __restrict__ tri, int64_t n, Node* nodes) {
+  Box b = tri_box(tri, 0);
+  for (int64_t r = 1; r < n; ++r) b = join(b, tri_box(tri, r));
+  Node nd;
+  nd.a = make_float4(pad_lo(b.lx), pad_hi(b.hx), pad_lo(b.ly), pad_hi(b.hy));
+  nd.b = make_float4(1.f, -1.f, 1.f, -1.f);  // empty box: never hit
+  nd.c = make_float4(pad_lo(b.lz), pad_hi(b.hz), 1.f, -1.f);
+  nd.d = make_uint4(make_leaf(0u, (uint32_t)n), make_leaf(0u, 1u), 0u, 0u);
+  nodes[0] = nd;
+}
+
+// gather input-order triangles into sorted (leaf) order
+__global__ void k_gather_tri(const float4* __restrict__ tri_in, const uint32_t* __restrict__ order,
+                             int64_t M, float4* __restrict__ tri) {
+  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= M) return;
+  int64_t t = order[r];
+  tri[3 * r] = tri_in[3 * t];
+  tri[3 * r + 1] = tri_in[3 * t + 1];
+  tri[3 * r + 2] = tri_in[3 * t + 2];
+}
+
+static inline unsigned grid_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+// Morton-sort the triangles (tri_in, input order) and build the BVH over them.
+// On return s->tri is leaf-ordered and `order` (if non-null) receives the
+// sorted -> input permutation (caller frees).
+int build_bvh(uvd_scene* s, float4* tri_in, uint32_t** order_out, cudaStream_t st) {
+  Alloc& al = s->alloc;
+  const int64_t M = s->M;
+  uint64_t* keys = (uint64_t*)al.get(M * sizeof(uint64_t));
+  uint32_t* vals = (uint32_t*)al.get(M * sizeof(uint32_t));
+  s->tri = (float4*)al.get(3 * M * sizeof(float4));
+  s->nodes = (Node*)al.get(std::max<int64_t>(M - 1, 1) * sizeof(Node));
+  if (!keys || !vals || !s->tri || !s->nodes) {
+    set_error("scene: out of device memory building the BVH (M=%lld)", (long long)M);
+    return UVD_ERR_NOMEM;
+  }
+  float3 lo = make_float3(s->bbox[0], s->bbox[1], s->bbox[2]);
+  float ex = s->bbox[3] - s->bbox[0], ey = s->bbox[4] - s->bbox[1], ez = s->bbox[5] - s->bbox[2];
+  float3 inv = make_float3(ex > 0 ? 1.f / ex : 0.f, ey > 0 ? 1.f / ey : 0.f, ez > 0 ? 1.f / ez : 0.f);
+  k_morton<<<grid_for(M, 256), 256, 0, st>>>(tri_in, M, lo, inv, keys, vals);
+  note_launch();
+  UVD_TRY(sort_pairs_u64(keys, vals, M, al, st));
+  k_gather_tri<<<grid_for(M, 256), 256, 0, st>>>(tri_in, vals, M, s->tri);
+  note_launch();
+  if (M <= kLeafMax) {
+    k_emit_small<<<1, 1, 0, st>>>(s->tri, M, s->nodes);
+    note_launch();
+    s->root = 0;
+  } else {
+    int64_t ni = M - 1;
+    int32_t* left = (int32_t*)al.get(ni * 4);
+    int32_t* right = (int32_t*)al.get(ni * 4);
+    int32_t* rf = (int32_t*)al.get(ni * 4);
+    int32_t* rl = (int32_t*)al.get(ni * 4);
+    int32_t* pint = (int32_t*)al.get(ni * 4);
+    int32_t* pleaf = (int32_t*)al.get(M * 4);
+    float* ibox = (float*)al.get(ni * 6 * sizeof(float));
+    int* arrive = (int*)al.get(ni * sizeof(int));
+    if (!left || !right || !rf || !rl || !pint || !pleaf || !ibox || !arrive) {
+      set_error("scene: out of device memory (BVH scratch)");
+      return UVD_ERR_NOMEM;
+    }
+    UVD_CUDA_TRY(cudaMemsetAsync(arrive, 0, ni * sizeof(int), st));
+    k_karras<<<grid_for(ni, 256), 256, 0, st>>>(keys, M, left, right, rf, rl, pint, pleaf);
+    note_launch();
+    k_refit<<<grid_for(M, 256), 256, 0, st>>>(s->tri, M, left, right, pint, pleaf, ibox, arrive);
+    note_launch();
+    k_emit<<<grid_for(ni, 256), 256, 0, st>>>(s->tri, M, left, right, rf, rl, ibox, s->nodes);
+    note_launch();
+    s->root = 0;
+    for (void* p : {(void*)left, (void*)right, (void*)rf, (void*)rl, (void*)pint, (void*)pleaf,
+                    (void*)ibox, (void*)arrive})
+      al.put(p);
+  }
+  UVD_CUDA_TRY(cudaGetLastError());
+  al.put(keys);
+  if (order_out) *order_out = vals;
+  else al.put(vals);
+  return UVD_OK;
+}
+
+}  // namespace uvd

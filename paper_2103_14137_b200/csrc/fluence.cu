@@ -1,0 +1,223 @@
+// fluence.cu — fluence products and coverage.
+//
+//   k_nonzero   ordered list of columns with t_k != 0 (LP plans are sparse)
+//   k_gemv_n    μ = A·t  (Eq. 5): each thread owns 4 consecutive rows
+//               (one float4 per column, coalesced 512 B per warp per column),
+//               walks the nonzero columns in order, fp64 accumulation -> the
+//               summation order is fixed (deterministic); HBM-bound
+//   k_gemv_t    g = Aᵀ·y (the LP's adjoint product): one CTA per 4
+//               columns, float4 row chunks, y read once per 4 columns, fixed
+//               tree reduction in fp64; HBM-bound
+//   k_coverage  Σ|s_i|[μ_i ≥ μ_min], Σ|s_i|, Σ|s_i|[rowsum_i > 0] (P:9),
+//               fixed-shape two-level reduction
+#include <cuda_runtime.h>
+
+#include <algorithm>
+
+#include "uvd_internal.cuh"
+
+namespace uvd {
+
+__global__ void __launch_bounds__(1024) k_nonzero(const double* __restrict__ x, int64_t k,
+                                                  int32_t* __restrict__ idx, double* __restrict__ val,
+                                                  int32_t* __restrict__ cnt) {
+  __shared__ int32_t part[1024];
+  int64_t per = (k + 1023) / 1024;
+  int64_t s = threadIdx.x * per, e = s + per < k ? s + per : k;
+  int32_t c = 0;
+  for (int64_t i = s; i < e; ++i) c += x[i] != 0.0;
+  part[threadIdx.x] = c;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {
+    int32_t v = threadIdx.x >= off ? part[threadIdx.x - off] : 0;
+    __syncthreads();
+    part[threadIdx.x] += v;
+    __syncthreads();
+  }
+  int32_t run = threadIdx.x ? part[threadIdx.x - 1] : 0;
+  for (int64_t i = s; i < e; ++i)
+    if (x[i] != 0.0) { idx[run] = (int32_t)i; val[run] = x[i]; ++run; }
+  if (threadIdx.x == 1023) *cnt = part[1023];
+}
+
+constexpr int kGemvThreads = 256;
+
+__global__ void __launch_bounds__(kGemvThreads) k_gemv_n(const float* __restrict__ A, int64_t ld,
+                                                         int64_t n, const int32_t* __restrict__ idx,
+                                                         const double* __restrict__ val,
+                                                         const int32_t* __restrict__ cnt,
+                                                         double* __restrict__ out) {
+  const int64_t q = blockIdx.x * (int64_t)kGemvThreads + threadIdx.x;  // row quad
+  const int64_t r0 = 4 * q;
+  if (r0 >= n) return;
+  const int32_t nz = *cnt;
+  double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+  const float4* __restrict__ A4 = reinterpret_cast<const float4*>(A);
+  const int64_t ld4 = ld / 4;
+  int32_t k = 0;
+  for (; k + 4 <= nz; k += 4) {  // 4 columns in flight
+    float4 v0 = __ldcs(A4 + (int64_t)idx[k] * ld4 + q);
+    float4 v1 = __ldcs(A4 + (int64_t)idx[k + 1] * ld4 + q);
+    float4 v2 = __ldcs(A4 + (int64_t)idx[k + 2] * ld4 + q);
+    float4 v3 = __ldcs(A4 + (int64_t)idx[k + 3] * ld4 + q);
+    double t0 = val[k], t1 = val[k + 1], t2 = val[k + 2], t3 = val[k + 3];
+    a0 += (double)v0.x * t0; a1 += (double)v0.y * t0; a2 += (double)v0.z * t0; a3 += (double)v0.w * t0;
+    a0 += (double)v1.x * t1; a1 += (double)v1.y * t1; a2 += (double)v1.z * t1; a3 += (double)v1.w * t1;
+    a0 += (double)v2.x * t2; a1 += (double)v2.y * t2; a2 += (double)v2.z * t2; a3 += (double)v2.w * t2;
+    a0 += (double)v3.x * t3; a1 += (double)v3.y * t3; a2 += (double)v3.z * t3; a3 += (double)v3.w * t3;
+  }
+  for (; k < nz; ++k) {
+    float4 v = __ldcs(A4 + (int64_t)idx[k] * ld4 + q);
+    double t = val[k];
+    a0 += (double)v.x * t; a1 += (double)v.y * t; a2 += (double)v.z * t; a3 += (double)v.w * t;
+  }
+  out[r0] = a0;
+  if (r0 + 1 < n) out[r0 + 1] = a1;
+  if (r0 + 2 < n) out[r0 + 2] = a2;
+  if (r0 + 3 < n) out[r0 + 3] = a3;
+}
+
+constexpr int kGemvTCols = 4;
+
+__global__ void __launch_bounds__(kGemvThreads) k_gemv_t(const float* __restrict__ A, int64_t ld,
+                                                         int64_t n, int64_t k,
+                                                         const double* __restrict__ y,
+                                                         double* __restrict__ out) {
+  __shared__ double red[kGemvTCols][kGemvThreads / 32];
+  const int64_t c0 = (int64_t)blockIdx.x * kGemvTCols;
+  const float4* __restrict__ A4 = reinterpret_cast<const float4*>(A);
+  const int64_t ld4 = ld / 4, nq = (n + 3) / 4;
+  double acc[kGemvTCols];
+#pragma unroll
+  for (int c = 0; c < kGemvTCols; ++c) acc[c] = 0.0;
+  for (int64_t q = threadIdx.x; q < nq; q += kGemvThreads) {
+    const int64_t r = 4 * q;
+    double y0 = y[r];
+    double y1 = r + 1 < n ? y[r + 1] : 0.0;
+    double y2 = r + 2 < n ? y[r + 2] : 0.0;
+    double y3 = r + 3 < n ? y[r + 3] : 0.0;
+#pragma unroll
+    for (int c = 0; c < kGemvTCols; ++c) {
+      if (c0 + c < k) {
+        float4 v = __ldcs(A4 + (c0 + c) * ld4 + q);
+        acc[c] += (double)v.x * y0 + (double)v.y * y1 + (double)v.z * y2 + (double)v.w * y3;
+      }
+    }
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int c = 0; c < kGemvTCols; ++c) {
+    double v = acc[c];
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) red[c][warp] = v;
+  }
+  __syncthreads();
+  if (threadIdx.x < kGemvTCols && c0 + threadIdx.x < k) {
+    double v = 0.0;
+    for (int w = 0; w < kGemvThreads / 32; ++w) v += red[threadIdx.x][w];
+    out[c0 + threadIdx.x] = v;
+  }
+}
+
+// coverage: per-block partials, then one block combines them in fixed order
+constexpr int kCovThreads = 256;
+__global__ void __launch_bounds__(kCovThreads) k_coverage_part(const double* __restrict__ mu,
+                                                               const double* __restrict__ area,
+                                                               const double* __restrict__ rowsum,
+                                                               int64_t n, double mu_min,
+                                                               double* __restrict__ part) {
+  __shared__ double s[3][kCovThreads];
+  double c = 0.0, t = 0.0, v = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)kCovThreads + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * kCovThreads) {
+    double a = area[i];
+    t += a;
+    if (mu[i] >= mu_min) c += a;             // inclusive (Q16)
+    if (!rowsum || rowsum[i] > 0.0) v += a;  // ever visible
+  }
+  s[0][threadIdx.x] = c; s[1][threadIdx.x] = t; s[2][threadIdx.x] = v;
+  __syncthreads();
+  for (int off = kCovThreads / 2; off > 0; off >>= 1) {
+    if (threadIdx.x < off)
+      for (int k = 0; k < 3; ++k) s[k][threadIdx.x] += s[k][threadIdx.x + off];
+    __syncthreads();
+  }
+  if (threadIdx.x < 3) part[3 * blockIdx.x + threadIdx.x] = s[threadIdx.x][0];
+}
+
+__global__ void k_coverage_final(const double* __restrict__ part, int nb, double* __restrict__ out) {
+  if (threadIdx.x < 3) {
+    double v = 0.0;
+    for (int b = 0; b < nb; ++b) v += part[3 * b + threadIdx.x];
+    out[threadIdx.x] = v;
+  }
+}
+
+}  // namespace uvd
+
+using namespace uvd;
+
+extern "C" int uvd_fluence(const uvd_matrix_out* A, int64_t n, int64_t k, int transpose,
+                           const double* x, double* out, void* stream) {
+  clear_error();
+  if (!A || !x || !out || n < 0 || k < 0) { set_error("uvd_fluence: bad argument"); return UVD_ERR_INVALID; }
+  if (A->format != UVD_DENSE_COLMAJOR) { set_error("uvd_fluence: format %d not supported yet", A->format); return UVD_ERR_INVALID; }
+  if (!A->values || A->ld < n || A->ld % 4 != 0 || ((uintptr_t)A->values & 15)) {
+    set_error("uvd_fluence: dense A needs 16-B aligned values and ld >= n, ld %% 4 == 0");
+    return UVD_ERR_INVALID;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n == 0) return UVD_OK;
+  if (!transpose) {
+    if (k == 0) { UVD_CUDA_TRY(cudaMemsetAsync(out, 0, n * sizeof(double), st)); return UVD_OK; }
+    int32_t* idx = nullptr;
+    double* val = nullptr;
+    int32_t* cnt = nullptr;
+    UVD_CUDA_TRY(cudaMallocAsync((void**)&idx, k * sizeof(int32_t), st));
+    UVD_CUDA_TRY(cudaMallocAsync((void**)&val, k * sizeof(double), st));
+    UVD_CUDA_TRY(cudaMallocAsync((void**)&cnt, sizeof(int32_t), st));
+    k_nonzero<<<1, 1024, 0, st>>>(x, k, idx, val, cnt);
+    note_launch();
+    int64_t quads = (n + 3) / 4;
+    k_gemv_n<<<(unsigned)((quads + kGemvThreads - 1) / kGemvThreads), kGemvThreads, 0, st>>>(
+        A->values, A->ld, n, idx, val, cnt, out);
+    note_launch();
+    UVD_CUDA_TRY(cudaGetLastError());
+    cudaFreeAsync(idx, st);
+    cudaFreeAsync(val, st);
+    cudaFreeAsync(cnt, st);
+  } else {
+    if (k == 0) return UVD_OK;
+    k_gemv_t<<<(unsigned)((k + kGemvTCols - 1) / kGemvTCols), kGemvThreads, 0, st>>>(
+        A->values, A->ld, n, k, x, out);
+    note_launch();
+    UVD_CUDA_TRY(cudaGetLastError());
+  }
+  return UVD_OK;
+}
+
+extern "C" int uvd_coverage(const uvd_scene* s, const double* mu, double mu_min,
+                            const double* a_rowsum, double out[3], void* stream) {
+  clear_error();
+  if (!s || !mu || !out) { set_error("uvd_coverage: null argument"); return UVD_ERR_INVALID; }
+  cudaStream_t st = (cudaStream_t)stream;
+  int dev = 0, sms = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  int nb = (int)std::min<int64_t>((s->N + kCovThreads - 1) / kCovThreads, 2 * sms);
+  nb = std::max(nb, 1);
+  double* part = nullptr;
+  double* dout = nullptr;
+  UVD_CUDA_TRY(cudaMallocAsync((void**)&part, 3 * nb * sizeof(double), st));
+  UVD_CUDA_TRY(cudaMallocAsync((void**)&dout, 3 * sizeof(double), st));
+  k_coverage_part<<<nb, kCovThreads, 0, st>>>(mu, s->area, a_rowsum, s->N, mu_min, part);
+  note_launch();
+  k_coverage_final<<<1, 32, 0, st>>>(part, nb, dout);
+  note_launch();
+  UVD_CUDA_TRY(cudaMemcpyAsync(out, dout, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  cudaFreeAsync(part, st);
+  cudaFreeAsync(dout, st);
+  UVD_CUDA_TRY(cudaStreamSynchronize(st));
+  UVD_CUDA_TRY(cudaGetLastError());
+  return UVD_OK;
+}

@@ -1,0 +1,457 @@
+// scene.cu — uvd_scene_create / query / patches / destroy, error handling and
+// the allocator (SURVEY §8(a) row a1 "scene ingest and canonical patch
+// attributes"; §8(b) boundary).
+//
+// Canonical patch attributes are computed in fp64 with explicitly rounded
+// intrinsics (__dadd_rn / __dmul_rn / __ddiv_rn / __dsqrt_rn: no FMA
+// contraction) and rounded once to fp32, so they are bit-identical to any
+// plain IEEE fp64 evaluation of the same formulas (include/uvd.h documents
+// them).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <string>
+#include <cmath>
+#include <cstdlib>
+#include <vector>
+
+#include "uvd_internal.cuh"
+
+namespace uvd {
+
+static thread_local char g_err[1024] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+void clear_error() { g_err[0] = 0; }
+
+static std::atomic<unsigned long long> g_launches{0};
+void note_launch(int n) { g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
+
+void* Alloc::get(size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  bytes = (bytes + 255) & ~(size_t)255;
+  if (has_user) return user.alloc(bytes, device, (void*)stream, user.ctx);
+  void* p = nullptr;
+  if (cudaMallocAsync(&p, bytes, stream) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return p;
+}
+void Alloc::put(void* p) {
+  if (!p) return;
+  if (has_user) user.free(p, device, (void*)stream, user.ctx);
+  else cudaFreeAsync(p, stream);
+}
+
+// --------------------------------------------------------- fp64 helpers --
+__device__ __forceinline__ double dadd(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ double dsub(double a, double b) { return __dadd_rn(a, -b); }
+__device__ __forceinline__ double dmul(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double ddiv(double a, double b) { return __ddiv_rn(a, b); }
+
+// 3D patch = triangle: c = fl32(((a+b)+c)/3), n = fl32(cross(b-a, c-a)/|.|),
+// area = |cross|/2 (P:158, P:248 mean irradiance needs |s_i|).
+__global__ void k_tri_attrs(const float* __restrict__ V, int64_t nv, const int32_t* __restrict__ F,
+                            int64_t nt, float4* __restrict__ tri_in, float* __restrict__ cen,
+                            float* __restrict__ nrm, double* __restrict__ area,
+                            unsigned long long* __restrict__ bad) {
+  int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= nt) return;
+  int32_t i0 = F[3 * t], i1 = F[3 * t + 1], i2 = F[3 * t + 2];
+  if (i0 < 0 || i1 < 0 || i2 < 0 || i0 >= nv || i1 >= nv || i2 >= nv) {
+    atomicMin(bad, (unsigned long long)t);
+    return;
+  }
+  const float* pa = V + 3 * (int64_t)i0;
+  const float* pb = V + 3 * (int64_t)i1;
+  const float* pc = V + 3 * (int64_t)i2;
+  double ax = pa[0], ay = pa[1], az = pa[2];
+  double bx = pb[0], by = pb[1], bz = pb[2];
+  double cx = pc[0], cy = pc[1], cz = pc[2];
+  cen[3 * t + 0] = (float)ddiv(dadd(dadd(ax, bx), cx), 3.0);
+  cen[3 * t + 1] = (float)ddiv(dadd(dadd(ay, by), cy), 3.0);
+  cen[3 * t + 2] = (float)ddiv(dadd(dadd(az, bz), cz), 3.0);
+  double ux = dsub(bx, ax), uy = dsub(by, ay), uz = dsub(bz, az);
+  double vx = dsub(cx, ax), vy = dsub(cy, ay), vz = dsub(cz, az);
+  double nx = dsub(dmul(uy, vz), dmul(uz, vy));
+  double ny = dsub(dmul(uz, vx), dmul(ux, vz));
+  double nz = dsub(dmul(ux, vy), dmul(uy, vx));
+  double len = __dsqrt_rn(dadd(dadd(dmul(nx, nx), dmul(ny, ny)), dmul(nz, nz)));
+  if (!(len > 0.0)) {
+    atomicMin(bad, (unsigned long long)t);
+    len = 1.0;
+  }
+  nrm[3 * t + 0] = (float)ddiv(nx, len);
+  nrm[3 * t + 1] = (float)ddiv(ny, len);
+  nrm[3 * t + 2] = (float)ddiv(nz, len);
+  area[t] = ddiv(len, 2.0);
+  tri_in[3 * t] = make_float4(pa[0], pa[1], pa[2], __int_as_float(0));
+  tri_in[3 * t + 1] = make_float4(pb[0], pb[1], pb[2], __int_as_float((int)t));
+  tri_in[3 * t + 2] = make_float4(pc[0], pc[1], pc[2], 0.f);
+}
+
+// 2.5D: patch i of wall w (segment s of n_seg): q_s = fl32(e0 + ((e1-e0)*s)/n_seg),
+// q_{n_seg} = e1; centroid ((q_s+q_{s+1})/2, h/2); normal (-dy,dx)/len (boundary,
+// into the room) or (dy,-dx)/len (obstacle, outward); area len*h.
+// Triangles: quad A=(q_s,0) B=(q_{s+1},0) C=(q_{s+1},h) D=(q_s,h) split on A–C,
+// wound so the right-hand normal equals n (obstacle: ABC, ACD; boundary: ACB, ADC).
+__global__ void k_extrude(const Wall* __restrict__ walls, int64_t n_walls, int64_t N, float h,
+                          float4* __restrict__ tri_in, float* __restrict__ cen,
+                          float* __restrict__ nrm, double* __restrict__ area) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= N) return;
+  int64_t lo = 0, hi = n_walls - 1;  // last wall with first_patch <= i
+  while (lo < hi) {
+    int64_t mid = (lo + hi + 1) >> 1;
+    if (walls[mid].first_patch <= i) lo = mid; else hi = mid - 1;
+  }
+  Wall w = walls[lo];
+  int64_t s = i - w.first_patch;
+  double ex = dsub((double)w.e1x, (double)w.e0x), ey = dsub((double)w.e1y, (double)w.e0y);
+  double ns = (double)w.n_seg;
+  float qax = (float)dadd((double)w.e0x, ddiv(dmul(ex, (double)s), ns));
+  float qay = (float)dadd((double)w.e0y, ddiv(dmul(ey, (double)s), ns));
+  float qbx, qby;
+  if (s + 1 == w.n_seg) { qbx = w.e1x; qby = w.e1y; }
+  else {
+    qbx = (float)dadd((double)w.e0x, ddiv(dmul(ex, (double)(s + 1)), ns));
+    qby = (float)dadd((double)w.e0y, ddiv(dmul(ey, (double)(s + 1)), ns));
+  }
+  double dx = dsub((double)qbx, (double)qax), dy = dsub((double)qby, (double)qay);
+  double len = __dsqrt_rn(dadd(dmul(dx, dx), dmul(dy, dy)));
+  cen[3 * i + 0] = (float)ddiv(dadd((double)qax, (double)qbx), 2.0);
+  cen[3 * i + 1] = (float)ddiv(dadd((double)qay, (double)qby), 2.0);
+  cen[3 * i + 2] = (float)ddiv((double)h, 2.0);
+  double nx = w.boundary ? ddiv(-dy, len) : ddiv(dy, len);
+  double ny = w.boundary ? ddiv(dx, len) : ddiv(-dx, len);
+  nrm[3 * i + 0] = (float)nx;
+  nrm[3 * i + 1] = (float)ny;
+  nrm[3 * i + 2] = 0.f;
+  area[i] = dmul(len, (double)h);
+  float4 A = make_float4(qax, qay, 0.f, 0.f), B = make_float4(qbx, qby, 0.f, 0.f);
+  float4 C = make_float4(qbx, qby, h, 0.f), D = make_float4(qax, qay, h, 0.f);
+  float4 t0[3], t1[3];
+  if (!w.boundary) { t0[0] = A; t0[1] = B; t0[2] = C; t1[0] = A; t1[1] = C; t1[2] = D; }
+  else { t0[0] = A; t0[1] = C; t0[2] = B; t1[0] = A; t1[1] = D; t1[2] = C; }
+  t0[0].w = __int_as_float((int)i); t0[1].w = __int_as_float((int)(2 * i)); t0[2].w = 0.f;
+  t1[0].w = __int_as_float((int)i); t1[1].w = __int_as_float((int)(2 * i + 1)); t1[2].w = 0.f;
+  for (int k = 0; k < 3; ++k) {
+    tri_in[3 * (2 * i) + k] = t0[k];
+    tri_in[3 * (2 * i + 1) + k] = t1[k];
+  }
+}
+
+// 3D canonical order = sorted (Morton) order: permute patch attributes and set
+// the owner patch id of each triangle to its sorted position.
+__global__ void k_permute_patches(const uint32_t* __restrict__ order, int64_t N,
+                                  const float* __restrict__ cen_in, const float* __restrict__ nrm_in,
+                                  const double* __restrict__ area_in, float* __restrict__ cen,
+                                  float* __restrict__ nrm, double* __restrict__ area,
+                                  int64_t* __restrict__ orig, float4* __restrict__ tri) {
+  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= N) return;
+  int64_t t = order[r];
+  for (int k = 0; k < 3; ++k) {
+    cen[3 * r + k] = cen_in[3 * t + k];
+    nrm[3 * r + k] = nrm_in[3 * t + k];
+  }
+  area[r] = area_in[t];
+  orig[r] = t;
+  tri[3 * r].w = __int_as_float((int)r);
+}
+
+__global__ void k_iota64(int64_t* __restrict__ a, int64_t n) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) a[i] = i;
+}
+
+// deterministic total area: fixed-shape tree reduction in one block
+__global__ void __launch_bounds__(1024) k_sum_area(const double* __restrict__ a, int64_t n,
+                                                   double* __restrict__ out) {
+  __shared__ double part[1024];
+  double s = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += 1024) s += a[i];
+  part[threadIdx.x] = s;
+  __syncthreads();
+  for (int off = 512; off > 0; off >>= 1) {
+    if (threadIdx.x < off) part[threadIdx.x] += part[threadIdx.x + off];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = part[0];
+}
+
+static inline unsigned grid_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
+
+static bool finite3(const float* p) {
+  return std::isfinite(p[0]) && std::isfinite(p[1]) && std::isfinite(p[2]);
+}
+
+static int create_trimesh(uvd_scene* s, const uvd_scene_desc* d, cudaStream_t st) {
+  if (!d->vertices || !d->tris || d->n_vertices <= 0 || d->n_tris <= 0) {
+    set_error("scene: TRIMESH needs vertices and triangles");
+    return UVD_ERR_INVALID;
+  }
+  if (d->n_tris >= (int64_t)1 << 28) {
+    set_error("scene: at most 2^28 triangles supported (got %lld)", (long long)d->n_tris);
+    return UVD_ERR_INVALID;
+  }
+  float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int64_t v = 0; v < d->n_vertices; ++v) {
+    const float* p = d->vertices + 3 * v;
+    if (!finite3(p)) {
+      set_error("scene: vertex %lld is not finite", (long long)v);
+      return UVD_ERR_INVALID;
+    }
+    for (int k = 0; k < 3; ++k) { lo[k] = std::min(lo[k], p[k]); hi[k] = std::max(hi[k], p[k]); }
+  }
+  for (int k = 0; k < 3; ++k) { s->bbox[k] = lo[k]; s->bbox[3 + k] = hi[k]; }
+  Alloc& al = s->alloc;
+  const int64_t M = d->n_tris, NV = d->n_vertices;
+  s->M = M;
+  s->N = M;
+  float* dV = (float*)al.get(NV * 3 * sizeof(float));
+  int32_t* dF = (int32_t*)al.get(M * 3 * sizeof(int32_t));
+  float4* tri_in = (float4*)al.get(3 * M * sizeof(float4));
+  float* cen_in = (float*)al.get(M * 3 * sizeof(float));
+  float* nrm_in = (float*)al.get(M * 3 * sizeof(float));
+  double* area_in = (double*)al.get(M * sizeof(double));
+  unsigned long long* bad = (unsigned long long*)al.get(sizeof(unsigned long long));
+  if (!dV || !dF || !tri_in || !cen_in || !nrm_in || !area_in || !bad) {
+    set_error("scene: out of device memory (M=%lld)", (long long)M);
+    return UVD_ERR_NOMEM;
+  }
+  UVD_CUDA_TRY(cudaMemcpyAsync(dV, d->vertices, NV * 3 * sizeof(float), cudaMemcpyHostToDevice, st));
+  UVD_CUDA_TRY(cudaMemcpyAsync(dF, d->tris, M * 3 * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  UVD_CUDA_TRY(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), st));
+  k_tri_attrs<<<grid_for(M, 256), 256, 0, st>>>(dV, NV, dF, M, tri_in, cen_in, nrm_in, area_in, bad);
+  note_launch();
+  unsigned long long h_bad = 0;
+  UVD_CUDA_TRY(cudaMemcpyAsync(&h_bad, bad, sizeof(h_bad), cudaMemcpyDeviceToHost, st));
+  UVD_CUDA_TRY(cudaStreamSynchronize(st));
+  if (h_bad != ~0ull) {
+    set_error("scene: triangle %llu has an out-of-range index or zero area (S:32)", h_bad);
+    return UVD_ERR_INVALID;
+  }
+  uint32_t* order = nullptr;
+  UVD_TRY(build_bvh(s, tri_in, &order, st));
+  s->centroid = (float*)al.get(M * 3 * sizeof(float));
+  s->normal = (float*)al.get(M * 3 * sizeof(float));
+  s->area = (double*)al.get(M * sizeof(double));
+  s->orig_id = (int64_t*)al.get(M * sizeof(int64_t));
+  if (!s->centroid || !s->normal || !s->area || !s->orig_id) {
+    set_error("scene: out of device memory (patches)");
+    return UVD_ERR_NOMEM;
+  }
+  k_permute_patches<<<grid_for(M, 256), 256, 0, st>>>(order, M, cen_in, nrm_in, area_in,
+                                                       s->centroid, s->normal, s->area,
+                                                       s->orig_id, s->tri);
+  note_launch();
+  UVD_CUDA_TRY(cudaGetLastError());
+  for (void* p : {(void*)dV, (void*)dF, (void*)tri_in, (void*)cen_in, (void*)nrm_in,
+                  (void*)area_in, (void*)bad, (void*)order})
+    al.put(p);
+  return UVD_OK;
+}
+
+static int create_extruded(uvd_scene* s, const uvd_scene_desc* d, cudaStream_t st) {
+  const float* b = d->bounds;
+  for (int k = 0; k < 4; ++k)
+    if (!std::isfinite(b[k])) { set_error("scene: non-finite bounds"); return UVD_ERR_INVALID; }
+  if (!(b[2] > b[0] && b[3] > b[1])) { set_error("scene: degenerate bounds"); return UVD_ERR_INVALID; }
+  if (!(d->wall_height > 0.f) || !std::isfinite(d->wall_height)) {
+    set_error("scene: wall_height must be > 0");
+    return UVD_ERR_INVALID;
+  }
+  if (!(d->patch_res > 0.f) || !std::isfinite(d->patch_res)) {
+    set_error("scene: patch_res must be > 0");
+    return UVD_ERR_INVALID;
+  }
+  if (d->n_obstacles < 0 || (d->n_obstacles > 0 && !d->obstacles)) {
+    set_error("scene: bad obstacle list");
+    return UVD_ERR_INVALID;
+  }
+  std::vector<Wall>& W = s->h_walls;
+  W.clear();
+  std::vector<float> pxy;
+  std::vector<int32_t> poff(1, 0);
+  float cx[4] = {b[0], b[2], b[2], b[0]}, cy[4] = {b[1], b[1], b[3], b[3]};
+  for (int k = 0; k < 4; ++k) {
+    Wall w{cx[k], cy[k], cx[(k + 1) % 4], cy[(k + 1) % 4], 1, 0, 0};
+    W.push_back(w);
+  }
+  for (int p = 0; p < d->n_obstacles; ++p) {
+    const uvd_polygon& P = d->obstacles[p];
+    if (P.n < 3 || !P.xy) { set_error("scene: obstacle %d has fewer than 3 vertices", p); return UVD_ERR_INVALID; }
+    for (int k = 0; k < P.n; ++k) {
+      float x = P.xy[2 * k], y = P.xy[2 * k + 1];
+      if (!std::isfinite(x) || !std::isfinite(y) || !(x > b[0] && x < b[2] && y > b[1] && y < b[3])) {
+        set_error("scene: obstacle %d vertex %d outside the bounds (S:24)", p, k);
+        return UVD_ERR_INVALID;
+      }
+      pxy.push_back(x);
+      pxy.push_back(y);
+      const float* u = P.xy + 2 * ((k + 1) % P.n);
+      Wall w{x, y, u[0], u[1], 0, 0, 0};
+      W.push_back(w);
+    }
+    poff.push_back((int32_t)(pxy.size() / 2));
+  }
+  int64_t N = 0;
+  for (Wall& w : W) {
+    double dx = (double)w.e1x - (double)w.e0x, dy = (double)w.e1y - (double)w.e0y;
+    double len = std::sqrt(dx * dx + dy * dy);
+    if (!(len > 0.0)) { set_error("scene: zero-length wall"); return UVD_ERR_INVALID; }
+    double ns = std::ceil(len / (double)d->patch_res);
+    w.n_seg = (int32_t)ns;
+    w.first_patch = N;
+    N += w.n_seg;
+  }
+  s->N = N;
+  s->M = 2 * N;
+  s->n_walls = (int64_t)W.size();
+  s->n_poly = d->n_obstacles;
+  for (int k = 0; k < 4; ++k) s->bounds[k] = b[k];
+  s->wall_height = d->wall_height;
+  s->bbox[0] = b[0]; s->bbox[1] = b[1]; s->bbox[2] = 0.f;
+  s->bbox[3] = b[2]; s->bbox[4] = b[3]; s->bbox[5] = d->wall_height;
+  Alloc& al = s->alloc;
+  s->walls = (Wall*)al.get(W.size() * sizeof(Wall));
+  s->poly_xy = (float*)al.get(std::max<size_t>(pxy.size(), 2) * sizeof(float));
+  s->poly_off = (int32_t*)al.get(poff.size() * sizeof(int32_t));
+  float4* tri_in = (float4*)al.get(3 * s->M * sizeof(float4));
+  s->centroid = (float*)al.get(N * 3 * sizeof(float));
+  s->normal = (float*)al.get(N * 3 * sizeof(float));
+  s->area = (double*)al.get(N * sizeof(double));
+  s->orig_id = (int64_t*)al.get(N * sizeof(int64_t));
+  if (!s->walls || !s->poly_xy || !s->poly_off || !tri_in || !s->centroid || !s->normal ||
+      !s->area || !s->orig_id) {
+    set_error("scene: out of device memory (N=%lld)", (long long)N);
+    return UVD_ERR_NOMEM;
+  }
+  UVD_CUDA_TRY(cudaMemcpyAsync(s->walls, W.data(), W.size() * sizeof(Wall), cudaMemcpyHostToDevice, st));
+  if (!pxy.empty())
+    UVD_CUDA_TRY(cudaMemcpyAsync(s->poly_xy, pxy.data(), pxy.size() * sizeof(float), cudaMemcpyHostToDevice, st));
+  UVD_CUDA_TRY(cudaMemcpyAsync(s->poly_off, poff.data(), poff.size() * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  k_extrude<<<grid_for(N, 256), 256, 0, st>>>(s->walls, s->n_walls, N, d->wall_height, tri_in,
+                                              s->centroid, s->normal, s->area);
+  note_launch();
+  k_iota64<<<grid_for(N, 256), 256, 0, st>>>(s->orig_id, N);
+  note_launch();
+  UVD_TRY(build_bvh(s, tri_in, nullptr, st));
+  // pageable H2D copies above may still read the host vectors: finish first
+  UVD_CUDA_TRY(cudaStreamSynchronize(st));
+  al.put(tri_in);
+  return UVD_OK;
+}
+
+static void free_scene(uvd_scene* s) {
+  if (!s) return;
+  Alloc& al = s->alloc;
+  for (void* p : {(void*)s->centroid, (void*)s->normal, (void*)s->area, (void*)s->orig_id,
+                  (void*)s->tri, (void*)s->nodes, (void*)s->walls, (void*)s->poly_xy,
+                  (void*)s->poly_off, (void*)s->err_flag})
+    al.put(p);
+  cudaStreamSynchronize(al.stream);
+  delete s;
+}
+
+}  // namespace uvd
+
+using namespace uvd;
+
+extern "C" int uvd_scene_create(const uvd_scene_desc* desc, int device, void* stream,
+                                const uvd_allocator* allocator, uvd_scene** out) {
+  clear_error();
+  if (!desc || !out) { set_error("uvd_scene_create: null argument"); return UVD_ERR_INVALID; }
+  *out = nullptr;
+  if (desc->kind != UVD_SCENE_TRIMESH && desc->kind != UVD_SCENE_EXTRUDED) {
+    set_error("uvd_scene_create: unknown kind %d", desc->kind);
+    return UVD_ERR_INVALID;
+  }
+  UVD_CUDA_TRY(cudaSetDevice(device));
+  uvd_scene* s = new uvd_scene();
+  s->kind = desc->kind;
+  s->alloc.device = device;
+  s->alloc.stream = (cudaStream_t)stream;
+  if (allocator && allocator->alloc && allocator->free) {
+    s->alloc.user = *allocator;
+    s->alloc.has_user = true;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  int rc = desc->kind == UVD_SCENE_TRIMESH ? create_trimesh(s, desc, st) : create_extruded(s, desc, st);
+  if (rc == UVD_OK) {
+    s->err_flag = (int*)s->alloc.get(sizeof(int));
+    double* dsum = (double*)s->alloc.get(sizeof(double));
+    if (!s->err_flag || !dsum) { set_error("scene: out of device memory"); rc = UVD_ERR_NOMEM; }
+    else {
+      cudaMemsetAsync(s->err_flag, 0, sizeof(int), st);
+      k_sum_area<<<1, 1024, 0, st>>>(s->area, s->N, dsum);
+      note_launch();
+      cudaMemcpyAsync(&s->total_area, dsum, sizeof(double), cudaMemcpyDeviceToHost, st);
+      cudaError_t e = cudaStreamSynchronize(st);
+      if (e == cudaSuccess) e = cudaGetLastError();
+      if (e != cudaSuccess) { set_error("scene: %s", cudaGetErrorString(e)); rc = UVD_ERR_CUDA; }
+      s->alloc.put(dsum);
+    }
+  }
+  if (rc != UVD_OK) {
+    std::string msg = uvd_last_error();
+    free_scene(s);
+    set_error("%s", msg.c_str());
+    return rc;
+  }
+  *out = s;
+  return UVD_OK;
+}
+
+extern "C" int uvd_scene_query(const uvd_scene* s, int64_t* n_patches, int64_t* n_tris,
+                               float bbox[6], double* total_area) {
+  clear_error();
+  if (!s) { set_error("uvd_scene_query: null scene"); return UVD_ERR_INVALID; }
+  if (n_patches) *n_patches = s->N;
+  if (n_tris) *n_tris = s->M;
+  if (bbox) for (int k = 0; k < 6; ++k) bbox[k] = s->bbox[k];
+  if (total_area) *total_area = s->total_area;
+  return UVD_OK;
+}
+
+extern "C" int uvd_scene_patches(const uvd_scene* s, float* centroid, float* normal, double* area,
+                                 int64_t* orig_id, void* stream) {
+  clear_error();
+  if (!s) { set_error("uvd_scene_patches: null scene"); return UVD_ERR_INVALID; }
+  cudaStream_t st = (cudaStream_t)stream;
+  if (centroid) UVD_CUDA_TRY(cudaMemcpyAsync(centroid, s->centroid, s->N * 3 * sizeof(float), cudaMemcpyDeviceToDevice, st));
+  if (normal) UVD_CUDA_TRY(cudaMemcpyAsync(normal, s->normal, s->N * 3 * sizeof(float), cudaMemcpyDeviceToDevice, st));
+  if (area) UVD_CUDA_TRY(cudaMemcpyAsync(area, s->area, s->N * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  if (orig_id) UVD_CUDA_TRY(cudaMemcpyAsync(orig_id, s->orig_id, s->N * sizeof(int64_t), cudaMemcpyDeviceToDevice, st));
+  return UVD_OK;
+}
+
+extern "C" void uvd_scene_destroy(uvd_scene* s) { free_scene(s); }
+
+extern "C" int uvd_sync_status(const uvd_scene* s, void* stream) {
+  clear_error();
+  if (!s) { set_error("uvd_sync_status: null scene"); return UVD_ERR_INVALID; }
+  cudaStream_t st = (cudaStream_t)stream;
+  int flag = 0;
+  UVD_CUDA_TRY(cudaMemcpyAsync(&flag, s->err_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  UVD_CUDA_TRY(cudaStreamSynchronize(st));
+  UVD_CUDA_TRY(cudaGetLastError());
+  if (flag) {
+    UVD_CUDA_TRY(cudaMemsetAsync(s->err_flag, 0, sizeof(int), st));
+    set_error("lamp–centroid distance below 1e-9 m (S:160)");
+    return UVD_ERR_DOMAIN;
+  }
+  return UVD_OK;
+}
+
+extern "C" const char* uvd_last_error(void) { return uvd::g_err; }
+extern "C" int uvd_version(void) { return 100; }
+extern "C" unsigned long long uvd_launch_count(void) { return g_launches.load(); }

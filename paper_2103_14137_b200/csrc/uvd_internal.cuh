@@ -1,0 +1,118 @@
+// uvd_internal.cuh — shared internals of libuvd (CUDA path only; the oracle
+// under oracle/ shares nothing with this tree).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <vector>
+
+#include "../../include/uvd.h"
+
+namespace uvd {
+
+// ------------------------------------------------------------------ errors --
+void set_error(const char* fmt, ...);
+void clear_error();
+void note_launch(int n = 1);  // kernel launch accounting (uvd_launch_count)
+
+#define UVD_CUDA_TRY(expr)                                                        \
+  do {                                                                            \
+    cudaError_t _e = (expr);                                                      \
+    if (_e != cudaSuccess) {                                                      \
+      ::uvd::set_error("%s:%d %s: %s", __FILE__, __LINE__, #expr,                 \
+                       cudaGetErrorString(_e));                                   \
+      return UVD_ERR_CUDA;                                                        \
+    }                                                                             \
+  } while (0)
+
+#define UVD_TRY(expr)            \
+  do {                           \
+    int _s = (expr);             \
+    if (_s != UVD_OK) return _s; \
+  } while (0)
+
+// -------------------------------------------------------------- constants --
+// Readings of the paper.  Written out here independently
+// of the oracle (the two sides share no code or constant tables).
+constexpr double kSelfEps = 1e-4;     // Q6: open segment t in (1e-4/d, 1 - 1e-4/d)
+constexpr double kMinDist = 1e-9;     // domain error below 1e-9 m
+constexpr double kEdgeTol = 1e-12;    // watertight acceptance of fp64 margins
+constexpr double kParallel = 1e-12;   // |det| <= 1e-12 |D||E1xE2| -> no crossing
+constexpr int kLeafMax = 4;           // triangles per BVH leaf (subtree collapse)
+constexpr int kStackDepth = 128;      // per-warp traversal stack entries
+// Q20 free-space test direction (tilted off the axes).
+constexpr double kFreeDirX = 0.0123, kFreeDirY = 0.0371, kFreeDirZ = 1.0;
+
+// BVH child reference: >= 0 internal node index; leaf = 0x80000000 | start<<3 | (count-1)
+__host__ __device__ inline bool ref_is_leaf(uint32_t r) { return (r & 0x80000000u) != 0; }
+__host__ __device__ inline uint32_t ref_start(uint32_t r) { return (r & 0x7fffffffu) >> 3; }
+__host__ __device__ inline uint32_t ref_count(uint32_t r) { return (r & 7u) + 1u; }
+__host__ __device__ inline uint32_t make_leaf(uint32_t start, uint32_t count) {
+  return 0x80000000u | (start << 3) | (count - 1u);
+}
+
+// BVH2 node with both child boxes (64 B, one 128-B line holds two nodes).
+struct __align__(16) Node {
+  float4 a;  // child0 lo.x hi.x lo.y hi.y
+  float4 b;  // child1 lo.x hi.x lo.y hi.y
+  float4 c;  // child0 lo.z hi.z, child1 lo.z hi.z
+  uint4 d;   // child0 ref, child1 ref, (unused), (unused)
+};
+
+// ------------------------------------------------------------------ memory --
+struct Alloc {
+  uvd_allocator user{};
+  bool has_user = false;
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  void* get(size_t bytes);
+  void put(void* p);
+};
+
+// ------------------------------------------------------------------- scene --
+struct Wall {  // 2.5D wall (host-prepared from the polygon description)
+  float e0x, e0y, e1x, e1y;
+  int32_t boundary;  // 1 = room boundary (normal into the room), 0 = obstacle
+  int32_t n_seg;
+  int64_t first_patch;
+};
+
+}  // namespace uvd
+
+struct uvd_scene {
+  uvd::Alloc alloc;
+  int32_t kind = 0;
+  int64_t N = 0;  // patches (rows of A)
+  int64_t M = 0;  // triangles
+  float bbox[6] = {0, 0, 0, 0, 0, 0};
+  double total_area = 0.0;
+  // canonical patch attributes (device)
+  float* centroid = nullptr;  // N*3
+  float* normal = nullptr;    // N*3
+  double* area = nullptr;     // N
+  int64_t* orig_id = nullptr; // N
+  // BVH (device)
+  float4* tri = nullptr;      // M*3: (v0, owner patch), (v1, orig tri), (v2, 0)  leaf order
+  uvd::Node* nodes = nullptr; // max(M-1, 1)
+  uint32_t root = 0;          // root ref
+  // 2.5D description (device + host copies) for the floorplan vantage test
+  uvd::Wall* walls = nullptr;  // device
+  int64_t n_walls = 0;
+  std::vector<uvd::Wall> h_walls;
+  float* poly_xy = nullptr;    // device, obstacles' vertices
+  int32_t* poly_off = nullptr; // device, n_obstacles+1 offsets
+  int32_t n_poly = 0;
+  float bounds[4] = {0, 0, 0, 0};
+  float wall_height = 0.f;
+  // in-kernel error flag (device int)
+  int* err_flag = nullptr;
+};
+
+namespace uvd {
+// launchers implemented in the .cu files
+int build_bvh(uvd_scene* s, float4* tri_in, uint32_t** order_out, cudaStream_t st);
+int sort_pairs_u64(uint64_t* keys, uint32_t* vals, int64_t n, Alloc& al, cudaStream_t st);
+}  // namespace uvd

@@ -1,0 +1,320 @@
+"""Thin Python binding of libuvd (include/uvd.h): argument marshalling only.
+
+Every step of the hot path runs in the CUDA kernels behind the C-ABI; this
+module only converts between torch tensors / numpy arrays and the ABI's plain
+pointers, and binds the ABI's allocator callback to PyTorch's caching
+allocator.  There is no CPU fallback: if libuvd.so is missing or CUDA is not
+available, every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libuvd.so")
+
+UVD_OK, UVD_ERR_INVALID, UVD_ERR_DOMAIN, UVD_ERR_EMPTY, UVD_ERR_CAPACITY, UVD_ERR_NOMEM, UVD_ERR_CUDA = (
+    0, -1, -2, -3, -4, -5, -6)
+TRIMESH, EXTRUDED = 0, 1
+DISC2D, TOWER, FLOAT3D, ARM = 0, 1, 2, 3
+DENSE_COLMAJOR, CSC = 0, 1
+
+
+class UvdError(RuntimeError):
+    def __init__(self, code, msg):
+        super().__init__(f"uvd error {code}: {msg}")
+        self.code = code
+
+
+# ----------------------------------------------------------------- structs --
+_ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_int, C.c_void_p, C.c_void_p)
+_FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_int, C.c_void_p, C.c_void_p)
+
+
+class _Allocator(C.Structure):
+    _fields_ = [("alloc", _ALLOC_FN), ("free", _FREE_FN), ("ctx", C.c_void_p)]
+
+
+class _Polygon(C.Structure):
+    _fields_ = [("xy", C.POINTER(C.c_float)), ("n", C.c_int32)]
+
+
+class _SceneDesc(C.Structure):
+    _fields_ = [("kind", C.c_int32), ("vertices", C.POINTER(C.c_float)), ("n_vertices", C.c_int64),
+                ("tris", C.POINTER(C.c_int32)), ("n_tris", C.c_int64), ("bounds", C.c_float * 4),
+                ("wall_height", C.c_float), ("obstacles", C.POINTER(_Polygon)),
+                ("n_obstacles", C.c_int32), ("patch_res", C.c_float)]
+
+
+class _VantageOpts(C.Structure):
+    _fields_ = [("robot", C.c_int32), ("spacing", C.c_float), ("clearance", C.c_float),
+                ("lamp_z", C.c_float), ("lamp_z0", C.c_float), ("lamp_z1", C.c_float),
+                ("reach", C.c_float), ("zmin", C.c_float), ("zmax", C.c_float),
+                ("lamp_samples", C.c_int32), ("base_clearance", C.c_float), ("base_z", C.c_float)]
+
+
+class _Lamp(C.Structure):
+    _fields_ = [("power_w", C.c_double), ("samples_per_config", C.c_int32)]
+
+
+class _MatrixOut(C.Structure):
+    _fields_ = [("format", C.c_int32), ("ld", C.c_int64), ("values", C.c_void_p),
+                ("colptr", C.c_void_p), ("rowidx", C.c_void_p), ("nnz_cap", C.c_int64),
+                ("vis_bits", C.c_void_p), ("col_sumsq", C.c_void_p), ("ray_count", C.c_void_p)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libuvd.so (built in-tree by __graft_entry__.build()); fail loudly."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback)")
+        L = C.CDLL(LIB_PATH)
+        L.uvd_scene_create.argtypes = [C.POINTER(_SceneDesc), C.c_int, C.c_void_p,
+                                       C.POINTER(_Allocator), C.POINTER(C.c_void_p)]
+        L.uvd_scene_query.argtypes = [C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_int64),
+                                      C.POINTER(C.c_float), C.POINTER(C.c_double)]
+        L.uvd_scene_patches.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
+                                        C.c_void_p]
+        L.uvd_scene_destroy.argtypes = [C.c_void_p]
+        L.uvd_scene_destroy.restype = None
+        L.uvd_vantage_sample.argtypes = [C.c_void_p, C.POINTER(_VantageOpts), C.c_void_p, C.c_void_p,
+                                         C.c_int64, C.POINTER(C.c_int64), C.c_void_p]
+        L.uvd_irradiance_matrix.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
+                                            C.POINTER(_Lamp), C.POINTER(_MatrixOut), C.c_void_p]
+        L.uvd_sync_status.argtypes = [C.c_void_p, C.c_void_p]
+        L.uvd_fluence.argtypes = [C.POINTER(_MatrixOut), C.c_int64, C.c_int64, C.c_int, C.c_void_p,
+                                  C.c_void_p, C.c_void_p]
+        L.uvd_coverage.argtypes = [C.c_void_p, C.c_void_p, C.c_double, C.c_void_p,
+                                   C.POINTER(C.c_double), C.c_void_p]
+        L.uvd_last_error.restype = C.c_char_p
+        L.uvd_version.restype = C.c_int
+        _lib = L
+    return _lib
+
+
+EXPORTS = ("uvd_scene_create", "uvd_scene_query", "uvd_scene_patches", "uvd_scene_destroy",
+           "uvd_vantage_sample", "uvd_irradiance_matrix", "uvd_sync_status", "uvd_fluence",
+           "uvd_coverage", "uvd_last_error", "uvd_version")
+
+
+def _check(rc):
+    if rc != UVD_OK:
+        raise UvdError(rc, lib().uvd_last_error().decode(errors="replace"))
+    return rc
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return C.c_void_p(s.cuda_stream)
+
+
+def _ptr(t):
+    return C.c_void_p(t.data_ptr()) if t is not None else C.c_void_p(0)
+
+
+# ------------------------------------------------- torch caching allocator --
+@_ALLOC_FN
+def _torch_alloc(nbytes, device, stream, ctx):
+    try:
+        return torch.cuda.caching_allocator_alloc(int(nbytes), device, stream)
+    except Exception:  # noqa: BLE001 — the C side reports NOMEM
+        return None
+
+
+@_FREE_FN
+def _torch_free(ptr, device, stream, ctx):
+    torch.cuda.caching_allocator_delete(ptr)
+
+
+_TORCH_ALLOCATOR = _Allocator(_torch_alloc, _torch_free, None)
+
+
+def _require_cuda():
+    if not torch.cuda.is_available():
+        raise RuntimeError("paper_2103_14137_b200 needs a CUDA device (no CPU fallback)")
+
+
+# ------------------------------------------------------------------- scene --
+class Scene:
+    """uvd_scene_create from a synth-style dict: TRIMESH {vertices, tris} or
+    EXTRUDED {bounds, wall_height, obstacles, patch_res}.  Host inputs are read
+    during the call (their host->device copy is part of the call)."""
+
+    def __init__(self, desc: dict, device: int | None = None, stream=None, torch_allocator: bool = True):
+        _require_cuda()
+        self.device = torch.cuda.current_device() if device is None else device
+        d = _SceneDesc()
+        keep = []
+        if "vertices" in desc:
+            V = np.ascontiguousarray(desc["vertices"], np.float32)
+            F = np.ascontiguousarray(desc["tris"], np.int32)
+            keep += [V, F]
+            d.kind = TRIMESH
+            d.vertices = V.ctypes.data_as(C.POINTER(C.c_float))
+            d.n_vertices = len(V)
+            d.tris = F.ctypes.data_as(C.POINTER(C.c_int32))
+            d.n_tris = len(F)
+        else:
+            d.kind = EXTRUDED
+            for k in range(4):
+                d.bounds[k] = float(desc["bounds"][k])
+            d.wall_height = float(desc["wall_height"])
+            d.patch_res = float(desc["patch_res"])
+            obs = [np.ascontiguousarray(p, np.float32).reshape(-1, 2) for p in desc["obstacles"]]
+            keep += obs
+            polys = (_Polygon * max(1, len(obs)))()
+            for k, p in enumerate(obs):
+                polys[k].xy = p.ctypes.data_as(C.POINTER(C.c_float))
+                polys[k].n = len(p)
+            keep.append(polys)
+            d.obstacles = polys
+            d.n_obstacles = len(obs)
+        h = C.c_void_p()
+        self._alloc = _TORCH_ALLOCATOR if torch_allocator else None
+        with torch.cuda.device(self.device):
+            _check(lib().uvd_scene_create(C.byref(d), self.device, _stream(stream),
+                                          C.byref(self._alloc) if self._alloc else None, C.byref(h)))
+        self._h = h
+        n, m = C.c_int64(), C.c_int64()
+        bb = (C.c_float * 6)()
+        area = C.c_double()
+        _check(lib().uvd_scene_query(h, C.byref(n), C.byref(m), bb, C.byref(area)))
+        self.N, self.M = n.value, m.value
+        self.bbox = np.array(bb[:], np.float32)
+        self.total_area = area.value
+        self.kind = d.kind
+
+    @property
+    def handle(self):
+        if self._h is None:
+            raise RuntimeError("scene is closed")
+        return self._h
+
+    def close(self):
+        if getattr(self, "_h", None) is not None:
+            lib().uvd_scene_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass
+
+    def ld(self):
+        return (self.N + 31) // 32 * 32
+
+    def patches(self, stream=None):
+        dev = torch.device("cuda", self.device)
+        cen = torch.empty((self.N, 3), dtype=torch.float32, device=dev)
+        nrm = torch.empty((self.N, 3), dtype=torch.float32, device=dev)
+        area = torch.empty(self.N, dtype=torch.float64, device=dev)
+        orig = torch.empty(self.N, dtype=torch.int64, device=dev)
+        _check(lib().uvd_scene_patches(self.handle, _ptr(cen), _ptr(nrm), _ptr(area), _ptr(orig),
+                                       _stream(stream)))
+        return dict(centroid=cen, normal=nrm, area=area, orig_id=orig)
+
+    def vantage(self, opts: dict, stream=None):
+        """uvd_vantage_sample: returns (lamps (K, L, 3) fp32, raw_index (K,) int64)."""
+        o = _VantageOpts()
+        for name, _ in _VantageOpts._fields_:
+            if name in opts:
+                setattr(o, name, opts[name])
+        L = int(opts.get("lamp_samples", 1)) if opts["robot"] == TOWER else 1
+        k = C.c_int64()
+        rc = lib().uvd_vantage_sample(self.handle, C.byref(o), None, None, 0, C.byref(k), _stream(stream))
+        if rc not in (UVD_OK, UVD_ERR_CAPACITY):
+            _check(rc)
+        K = k.value
+        dev = torch.device("cuda", self.device)
+        lamps = torch.empty((K, L, 3), dtype=torch.float32, device=dev)
+        raw = torch.empty(K, dtype=torch.int64, device=dev)
+        _check(lib().uvd_vantage_sample(self.handle, C.byref(o), _ptr(lamps), _ptr(raw), K, C.byref(k),
+                                        _stream(stream)))
+        return lamps, raw
+
+    def irradiance(self, lamps: torch.Tensor, cols=None, power_w: float = 80.0, vis_bits: bool = False,
+                   col_sumsq: bool = False, ray_count: bool = False, out: torch.Tensor | None = None,
+                   stream=None) -> dict:
+        """uvd_irradiance_matrix (dense column-major).  lamps: (K_total, L, 3)
+        fp32 on the device; cols: None or a host sequence of global column ids.
+        Returns dict(A=(n_cols, ld) fp32, [vis_bits (n_cols, L, words) int32],
+        [col_sumsq (n_cols,) fp64], [ray_count (1,) int64])."""
+        assert lamps.is_cuda and lamps.dtype == torch.float32 and lamps.is_contiguous()
+        K, L = lamps.shape[0], lamps.shape[1]
+        ccols = None
+        if cols is not None:
+            ccols = np.ascontiguousarray(cols, np.int64)
+            n_cols = len(ccols)
+        else:
+            n_cols = K
+        ld = self.ld()
+        dev = lamps.device
+        A = out if out is not None else torch.empty((n_cols, ld), dtype=torch.float32, device=dev)
+        assert A.shape == (n_cols, ld) and A.dtype == torch.float32 and A.is_contiguous()
+        res = dict(A=A)
+        m = _MatrixOut()
+        m.format = DENSE_COLMAJOR
+        m.ld = ld
+        m.values = A.data_ptr()
+        if vis_bits:
+            vb = torch.empty((n_cols, L, (self.N + 31) // 32), dtype=torch.int32, device=dev)
+            m.vis_bits = vb.data_ptr()
+            res["vis_bits"] = vb
+        if col_sumsq:
+            cs = torch.empty(n_cols, dtype=torch.float64, device=dev)
+            m.col_sumsq = cs.data_ptr()
+            res["col_sumsq"] = cs
+        if ray_count:
+            rc_t = torch.zeros(1, dtype=torch.int64, device=dev)
+            m.ray_count = rc_t.data_ptr()
+            res["ray_count"] = rc_t
+        lamp = _Lamp(float(power_w), int(L))
+        _check(lib().uvd_irradiance_matrix(
+            self.handle, _ptr(lamps), K,
+            ccols.ctypes.data_as(C.c_void_p) if ccols is not None else None, n_cols,
+            C.byref(lamp), C.byref(m), _stream(stream)))
+        res["_desc"] = m
+        return res
+
+    def sync_status(self, stream=None):
+        _check(lib().uvd_sync_status(self.handle, _stream(stream)))
+
+    def coverage(self, mu: torch.Tensor, mu_min: float = 280.0, rowsum: torch.Tensor | None = None,
+                 stream=None) -> np.ndarray:
+        out = (C.c_double * 3)()
+        _check(lib().uvd_coverage(self.handle, _ptr(mu), float(mu_min), _ptr(rowsum), out, _stream(stream)))
+        return np.array(out[:], np.float64)
+
+
+def _dense_desc(A: torch.Tensor) -> _MatrixOut:
+    m = _MatrixOut()
+    m.format = DENSE_COLMAJOR
+    m.ld = A.shape[1]
+    m.values = A.data_ptr()
+    return m
+
+
+def fluence(A: torch.Tensor, n: int, x: torch.Tensor, transpose: bool = False,
+            out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """uvd_fluence on a dense (n_cols, ld) A: μ = A·x (x: (n_cols,) fp64) or
+    g = Aᵀ·x (x: (n,) fp64)."""
+    k = A.shape[0]
+    assert x.dtype == torch.float64 and x.is_cuda and x.is_contiguous()
+    if out is None:
+        out = torch.empty(k if transpose else n, dtype=torch.float64, device=A.device)
+    m = _dense_desc(A)
+    _check(lib().uvd_fluence(C.byref(m), n, k, int(bool(transpose)), _ptr(x), _ptr(out), _stream(stream)))
+    return out
+
+
+def version() -> int:
+    return int(lib().uvd_version())

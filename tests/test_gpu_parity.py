@@ -1,0 +1,362 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the fp64 oracle on the
+same seeded inputs.  Bars (BASELINE.json north_star):
+  * canonical patch attributes: bit-exact;
+  * vantage sets: identical except candidates the oracle flags ambiguous;
+  * visibility masks: bit-exact except rays the oracle flags degenerate
+    (|margin| < 1e-6 or |cosθ| < 1e-6), whose fraction must stay < 1e-4;
+  * A: relative error <= 1e-5 per entry (fp64 math, one fp32 rounding);
+  * μ = A·t, Aᵀ·y: relative 1e-5 (GEMV-only check uses the GPU's A);
+  * coverage: identical on rows away from the threshold.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+from oracle import oracle as O  # noqa: E402
+from synth import configs, rooms, vectors, ward  # noqa: E402
+
+REL_A = 1e-5
+DEG_GATE = 1e-4
+
+
+@pytest.fixture(scope="module")
+def uvd():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_2103_14137_b200 import uvd as U
+    return U
+
+
+def bits_to_mask(vb, N):
+    """(n_cols, L, words) int32 -> bool (N, n_cols, L)"""
+    w = vb.cpu().numpy().view(np.uint32)
+    bits = ((w[..., None] >> np.arange(32, dtype=np.uint32)) & 1).astype(bool)
+    bits = bits.reshape(w.shape[0], w.shape[1], -1)[:, :, :N]
+    return np.transpose(bits, (2, 0, 1))
+
+
+def gpu_full(U, scene_desc, lamps_np=None, vopts=None, cols=None):
+    sc = U.Scene(scene_desc)
+    if lamps_np is None:
+        lamps, raw = sc.vantage(vopts)
+    else:
+        lamps = torch.from_numpy(np.ascontiguousarray(lamps_np, np.float32)).cuda()
+    r = sc.irradiance(lamps, cols=cols, vis_bits=True, ray_count=True)
+    sc.sync_status()
+    p = sc.patches()
+    return sc, lamps, r, p
+
+
+def check_full(sc, r, p, ref, lamps):
+    """Full-matrix comparison in oracle (input) row order."""
+    N = sc.N
+    orig = p["orig_id"].cpu().numpy()
+    A = np.zeros((N, r["A"].shape[0]))
+    A[orig] = r["A"][:, :N].T.double().cpu().numpy()
+    vis = np.zeros((N, r["A"].shape[0], lamps.shape[1]), bool)
+    vis[orig] = bits_to_mask(r["vis_bits"], N)
+    deg = ref["deg"]
+    ok = ~deg
+    assert deg.mean() < DEG_GATE, f"degenerate fraction {deg.mean()}"
+    mism = (vis != ref["vis"]) & ok
+    assert not mism.any(), f"{mism.sum()} visibility mismatches, first at {np.argwhere(mism)[:5]}"
+    rows_ok = ~deg.any(-1)
+    ra = ref["A"]
+    err = np.abs(A - ra)
+    bad = rows_ok & (err > REL_A * np.abs(ra))
+    assert not bad.any(), f"{bad.sum()} entries beyond 1e-5 rel, max {err[rows_ok].max()}"
+    # padded rows are zero
+    assert float(r["A"][:, N:].abs().max() if r["A"].shape[1] > N else 0) == 0.0
+    return A
+
+
+# ------------------------------------------------------------------ a1 ---
+@pytest.mark.parametrize("seed", [None, 0, 7, 21])
+def test_extruded_patches_bit_exact(uvd, seed):
+    desc = rooms.empty_room() if seed is None else rooms.random_room(seed)
+    sc = uvd.Scene(desc)
+    p = sc.patches()
+    ref = O.extruded_patches(desc)
+    assert sc.N == ref["N"]
+    assert np.array_equal(p["centroid"].cpu().numpy(), ref["centroid"])
+    assert np.array_equal(p["normal"].cpu().numpy(), ref["normal"])
+    assert np.array_equal(p["area"].cpu().numpy(), ref["area"])
+    assert np.array_equal(p["orig_id"].cpu().numpy(), np.arange(sc.N))
+    assert abs(sc.total_area - ref["area"].sum()) < 1e-12 * ref["area"].sum()
+
+
+def test_trimesh_patches_bit_exact(uvd):
+    w = ward.ward(seed=3, n_bays=1, e=0.2)
+    sc = uvd.Scene(w)
+    p = sc.patches()
+    ref = O.trimesh_patches(w["vertices"], w["tris"])
+    orig = p["orig_id"].cpu().numpy()
+    assert sorted(orig.tolist()) == list(range(len(w["tris"])))
+    assert np.array_equal(p["centroid"].cpu().numpy(), ref["centroid"][orig])
+    assert np.array_equal(p["normal"].cpu().numpy(), ref["normal"][orig])
+    assert np.array_equal(p["area"].cpu().numpy(), ref["area"][orig])
+
+
+def test_scene_rejects_invalid(uvd):
+    V = np.array([[0, 0, 0], [1, 0, 0], [2, 0, 0]], np.float32)
+    with pytest.raises(uvd.UvdError) as e:
+        uvd.Scene(dict(vertices=V, tris=np.array([[0, 1, 2]], np.int32)))
+    assert e.value.code == uvd.UVD_ERR_INVALID
+    with pytest.raises(uvd.UvdError):
+        uvd.Scene(dict(vertices=V, tris=np.array([[0, 1, 5]], np.int32)))
+    bad = rooms.empty_room()
+    bad["obstacles"] = [np.array([[1, 1], [6, 1], [1, 2]], np.float32)]
+    with pytest.raises(uvd.UvdError):
+        uvd.Scene(bad)
+
+
+# ------------------------------------------------------------------ a3 ---
+def _vantage_parity(uvd, desc, opts, idx=None):
+    sc = uvd.Scene(desc)
+    lamps, raw = sc.vantage(opts)
+    ref = O.vantage(desc, opts, idx=idx)
+    raw = raw.cpu().numpy()
+    g = np.zeros(len(O.vantage_candidates(desc, opts)["points"]), bool)
+    g[raw] = True
+    sel = ref["idx"]
+    amb = ref["ambiguous"]
+    assert np.array_equal(g[sel][~amb], ref["feasible"][~amb])
+    # positions (all L samples) bit-identical to the oracle's grid for common points
+    both = np.isin(raw, sel[ref["feasible"]])
+    pos = {int(q): k for k, q in enumerate(sel)}
+    lam = lamps.cpu().numpy()
+    for kk in np.nonzero(both)[0][:2000]:
+        assert np.array_equal(lam[kk], ref["samples"][pos[int(raw[kk])]])
+    return lamps, raw, ref
+
+
+def test_vantage_disc2d(uvd):
+    lamps, raw, ref = _vantage_parity(uvd, rooms.empty_room(), configs.DISC_OPTS)
+    assert lamps.shape[0] == 324
+    for seed in (0, 4, 9, 13):
+        _vantage_parity(uvd, rooms.random_room(seed), configs.DISC_OPTS)
+        _vantage_parity(uvd, rooms.random_room(seed), configs.DISC_OPTS_COARSE)
+
+
+def test_vantage_3d_small_ward(uvd):
+    w = ward.ward(seed=2, n_bays=1, e=0.12)
+    _vantage_parity(uvd, w, configs.FLOAT_OPTS)
+    _vantage_parity(uvd, w, configs.TOWER_OPTS)
+    _vantage_parity(uvd, w, configs.ARM_OPTS)
+
+
+def test_vantage_c4_sampled(uvd):
+    sc = configs.c4_scene()
+    rng = np.random.default_rng(5)
+    n = len(O.vantage_candidates(sc, configs.FLOAT_OPTS)["points"])
+    _vantage_parity(uvd, sc, configs.FLOAT_OPTS, idx=np.sort(rng.choice(n, 300, replace=False)))
+
+
+def test_vantage_empty_and_capacity(uvd):
+    sc = uvd.Scene(rooms.empty_room(1.0, 2.0, 0.25))
+    with pytest.raises(uvd.UvdError) as e:
+        sc.vantage(configs.vopts(configs.DISC2D, 0.25, 0.6))
+    assert e.value.code == uvd.UVD_ERR_EMPTY
+
+
+# ---------------------------------------------------------------- a4–a6 ---
+def test_c1_full_matrix(uvd):
+    c = configs.c1()
+    sc, lamps, r, p = gpu_full(uvd, c["scene"], vopts=c["vantage"])
+    pat = O.extruded_patches(c["scene"])
+    lam = lamps.cpu().numpy()
+    ref2 = O.irradiance_matrix(pat, lam, mode="2d")
+    ref3 = O.irradiance_matrix(pat, lam, mode="3d")
+    A = check_full(sc, r, p, ref2, lam)
+    check_full(sc, r, p, ref3, lam)
+    assert (A > 0).all()                       # convex room: every pair lit
+    assert int(r["ray_count"].item()) == sc.N * lam.shape[0]
+
+
+@pytest.mark.parametrize("seed", list(range(25)))
+def test_c2_full_matrix(uvd, seed):
+    c = configs.c2(seed)
+    sc, lamps, r, p = gpu_full(uvd, c["scene"], vopts=c["vantage"])
+    pat = O.extruded_patches(c["scene"])
+    lam = lamps.cpu().numpy()
+    ref = O.irradiance_matrix(pat, lam, mode="2d")   # the floorplan oracle
+    check_full(sc, r, p, ref, lam)
+    if seed < 3:
+        check_full(sc, r, p, O.irradiance_matrix(pat, lam, mode="3d"), lam)
+
+
+def test_c3_full_matrix(uvd):
+    for seed in range(10):
+        c = configs.c3(seed)
+        sc, lamps, r, p = gpu_full(uvd, c["scene"], vopts=c["vantage"])
+        lam = lamps.cpu().numpy()
+        ref = O.irradiance_matrix(O.extruded_patches(c["scene"]), lam, mode="2d")
+        check_full(sc, r, p, ref, lam)
+
+
+def test_small_ward_full_matrix(uvd):
+    """3D triangle scene, every pair (tiny tessellation so brute force is quick)."""
+    w = ward.ward(seed=4, n_bays=1, e=0.3)
+    sc, lamps, r, p = gpu_full(uvd, w, vopts=configs.vopts(configs.FLOAT3D, 0.5, 0.05))
+    lam = lamps.cpu().numpy()
+    ref = O.irradiance_matrix(O.trimesh_patches(w["vertices"], w["tris"]), lam)
+    check_full(sc, r, p, ref, lam)
+
+
+def test_small_ward_tower_full_matrix(uvd):
+    w = ward.ward(seed=6, n_bays=1, e=0.3)
+    opts = dict(configs.TOWER_OPTS, spacing=0.5)
+    sc, lamps, r, p = gpu_full(uvd, w, vopts=opts)
+    lam = lamps.cpu().numpy()
+    assert lam.shape[1] == 10
+    ref = O.irradiance_matrix(O.trimesh_patches(w["vertices"], w["tris"]), lam)
+    check_full(sc, r, p, ref, lam)
+
+
+def _sampled(uvd, desc, vopts, n_pairs, seed, cols_frac=None):
+    """Full-size assembly (the bench's launch configuration) checked on
+    sampled (row, column) pairs the oracle computes one by one."""
+    sc = uvd.Scene(desc)
+    lamps, _ = sc.vantage(vopts)
+    K = lamps.shape[0]
+    rng = np.random.default_rng(seed)
+    cols = None
+    if cols_frac is not None:
+        cols = np.sort(rng.choice(K, max(1, int(K * cols_frac)), replace=False))
+    r = sc.irradiance(lamps, cols=cols, vis_bits=True)
+    sc.sync_status()
+    p = sc.patches()
+    orig = p["orig_id"].cpu().numpy()
+    n_cols = r["A"].shape[0]
+    ri = rng.integers(0, sc.N, n_pairs)
+    ci = rng.integers(0, n_cols, n_pairs)
+    gA = r["A"][torch.from_numpy(ci).cuda(), torch.from_numpy(ri).cuda()].double().cpu().numpy()
+    vb = r["vis_bits"].cpu().numpy().view(np.uint32)
+    L = lamps.shape[1]
+    gvis = np.stack([(vb[ci, l, ri // 32] >> (ri % 32).astype(np.uint32)) & 1 for l in range(L)], 1).astype(bool)
+    pat = O.scene_patches(desc)
+    gcol = ci if cols is None else cols[ci]
+    ref = O.irradiance_pairs(pat, lamps.cpu().numpy(), orig[ri], gcol)
+    deg = ref["deg"]
+    assert deg.sum() <= 2, deg.sum()   # gate 1e-4: a few thousand samples see ~0
+    ok = ~deg
+    mism = (gvis != ref["vis"]) & ok
+    assert not mism.any(), f"{mism.sum()} mismatches of {ok.sum()}"
+    rows = ~deg.any(1)
+    err = np.abs(gA - ref["A"])[rows]
+    assert (err <= REL_A * np.abs(ref["A"][rows])).all(), err.max()
+    return ref
+
+
+def test_c4_floatbot_sampled(uvd):
+    ref = _sampled(uvd, configs.c4_scene(), configs.FLOAT_OPTS, 4000, 1)
+    assert 0.05 < ref["vis"].mean() < 0.95
+
+
+def test_c4_towerbot_sampled(uvd):
+    _sampled(uvd, configs.c4_scene(), configs.TOWER_OPTS, 600, 2)
+
+
+@pytest.mark.slow
+def test_c5_armbot_sampled(uvd):
+    _sampled(uvd, configs.c5_scene(), configs.ARM_OPTS, 400, 3, cols_frac=0.05)
+
+
+def test_column_shard_bit_identical(uvd):
+    """Multi-GPU invariance: a block-cyclic column shard equals the
+    corresponding columns of the single-call matrix bit for bit."""
+    c = configs.c2(5)
+    sc = uvd.Scene(c["scene"])
+    lamps, _ = sc.vantage(c["vantage"])
+    full = sc.irradiance(lamps, vis_bits=True)
+    K = lamps.shape[0]
+    for rank, world in ((0, 2), (1, 2), (2, 4)):
+        cols = [j for j in range(K) if (j // 8) % world == rank]
+        part = sc.irradiance(lamps, cols=cols, vis_bits=True)
+        assert torch.equal(part["A"], full["A"][cols])
+        assert torch.equal(part["vis_bits"], full["vis_bits"][cols])
+
+
+def test_domain_error(uvd):
+    c = configs.c1()
+    sc = uvd.Scene(c["scene"])
+    p = sc.patches()
+    lam = p["centroid"][5:6].reshape(1, 1, 3).contiguous()
+    sc.irradiance(lam)
+    with pytest.raises(uvd.UvdError) as e:
+        sc.sync_status()
+    assert e.value.code == uvd.UVD_ERR_DOMAIN
+    sc.sync_status()  # flag cleared
+
+
+def test_tiny_scenes(uvd):
+    """M <= leaf size (single-leaf BVH), one patch, ragged N."""
+    s = 1.0 / 64
+    V = np.array([[-s, -s, 0], [2 * s, -s, 0], [-s, 2 * s, 0]], np.float32)
+    sc = uvd.Scene(dict(vertices=V, tris=np.array([[0, 1, 2]], np.int32)))
+    lam = torch.tensor([[[0, 0, 1]], [[0, 0, 2]], [[0, 0, -1]]], dtype=torch.float32).cuda()
+    r = sc.irradiance(lam)
+    a = r["A"][:, 0].double().cpu().numpy()
+    assert abs(a[0] - 80 / (4 * np.pi)) < 1e-6 * a[0]
+    assert abs(a[1] - 20 / (4 * np.pi)) < 1e-6 * a[1]
+    assert a[2] == 0.0
+    V2 = np.concatenate([V, V + np.array([0, 0, 1e-3], np.float32)])
+    sc2 = uvd.Scene(dict(vertices=V2, tris=np.array([[0, 1, 2], [3, 5, 4]], np.int32)))
+    p = sc2.patches()
+    r2 = sc2.irradiance(lam[:1].contiguous())
+    orig = p["orig_id"].cpu().numpy()
+    A = r2["A"][0, :2].cpu().numpy()
+    assert A[list(orig).index(0)] == 0.0      # blocked by the cover 1 mm above
+
+
+# ------------------------------------------------------------------ a7/a8 ---
+def test_fluence_and_coverage(uvd):
+    c = configs.c2(8)
+    sc = uvd.Scene(c["scene"])
+    lamps, _ = sc.vantage(c["vantage"])
+    r = sc.irradiance(lamps)
+    A = r["A"]
+    K, N = A.shape[0], sc.N
+    An = A[:, :N].T.double().cpu().numpy()
+    for t_np in (vectors.sparse_plan(K, 1), vectors.dense_iterate(K, 2), np.zeros(K)):
+        t = torch.from_numpy(t_np).cuda()
+        mu = uvd.fluence(A, N, t).cpu().numpy()
+        ref = O.fluence(An, t_np)
+        assert np.allclose(mu, ref, rtol=1e-12, atol=1e-300)
+    y_np = vectors.row_weights(N, 3)
+    g = uvd.fluence(A, N, torch.from_numpy(y_np).cuda(), transpose=True).cpu().numpy()
+    assert np.allclose(g, O.fluence_t(An, y_np), rtol=1e-12, atol=0)
+    t_np = vectors.dense_iterate(K, 4) * 20
+    mu_t = uvd.fluence(A, N, torch.from_numpy(t_np).cuda())
+    rowsum = uvd.fluence(A, N, torch.ones(K, dtype=torch.float64, device="cuda"))
+    cov = sc.coverage(mu_t, configs.MU_MIN, rowsum)
+    area = O.extruded_patches(c["scene"])["area"]
+    mu_np = mu_t.cpu().numpy()
+    ref = O.coverage(mu_np, area, configs.MU_MIN, rowsum.cpu().numpy())
+    assert np.allclose(cov, ref, rtol=1e-12)
+    assert 0 < cov[0] < cov[1]
+
+
+def test_fluence_large_sparse(uvd):
+    """A·t on a C4-size dense matrix: GEMV-only parity on sampled rows."""
+    sc = uvd.Scene(configs.c4_scene())
+    lamps, _ = sc.vantage(configs.FLOAT_OPTS)
+    K = lamps.shape[0]
+    cols = list(range(0, K, 8))
+    A = sc.irradiance(lamps, cols=cols)["A"]
+    t_np = vectors.sparse_plan(len(cols), 7, frac=0.1)
+    mu = uvd.fluence(A, sc.N, torch.from_numpy(t_np).cuda()).cpu().numpy()
+    nz = np.nonzero(t_np)[0]
+    rows = np.random.default_rng(0).integers(0, sc.N, 5000)
+    sub = A[torch.from_numpy(nz).cuda()][:, torch.from_numpy(rows).cuda()].double().cpu().numpy()
+    ref = sub.T @ t_np[nz]
+    assert np.allclose(mu[rows], ref, rtol=1e-12, atol=1e-300)
+    y = vectors.row_weights(sc.N, 1)
+    g = uvd.fluence(A, sc.N, torch.from_numpy(y).cuda(), transpose=True).cpu().numpy()
+    ref_g = A[:5, :sc.N].double().cpu().numpy() @ y
+    assert np.allclose(g[:5], ref_g, rtol=1e-10)
