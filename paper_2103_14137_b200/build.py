@@ -28,23 +28,28 @@ def stale() -> bool:
     return any(os.path.getmtime(p) > t for p in deps)
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, defines=(), out: str | None = None) -> str:
+    """Compile every csrc/*.cu for sm_100a and link libuvd.so (or `out`, with
+    extra -D `defines`, for experiment builds)."""
+    lib = out or LIB
+    if not force and not defines and out is None and not stale():
         return LIB
     objs = []
     os.makedirs(os.path.join(HERE, "build"), exist_ok=True)
     for src in sources():
-        obj = os.path.join(HERE, "build", os.path.basename(src) + ".o")
-        cmd = [NVCC, *FLAGS, "-c", src, "-o", obj]
+        tag = "_".join(d.replace("=", "") for d in defines)
+        obj = os.path.join(HERE, "build", os.path.basename(src) + (("." + tag) if tag else "") + ".o")
+        cmd = [NVCC, *FLAGS, *["-D" + d for d in defines], "-c", src, "-o", obj]
         if verbose:
             cmd += ["-Xptxas", "-v"]
         subprocess.check_call(cmd)
         objs.append(obj)
     subprocess.check_call([NVCC, "-gencode", "arch=compute_100a,code=sm_100a", "-shared",
-                           "-o", LIB, *objs, "-lcudart"])
-    return LIB
+                           "-o", lib, *objs, "-lcudart"])
+    return lib
 
 
 if __name__ == "__main__":
-    build(force=True, verbose="-v" in sys.argv)
-    print(LIB)
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    outs = [a[6:] for a in sys.argv[1:] if a.startswith("--out=")]
+    print(build(force=True, verbose="-v" in sys.argv, defines=defs, out=outs[0] if outs else None))

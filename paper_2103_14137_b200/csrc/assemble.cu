@@ -17,6 +17,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "traverse.cuh"
 #include "uvd_internal.cuh"
@@ -25,10 +26,15 @@ namespace uvd {
 
 constexpr int kAsmWarps = 8;
 constexpr int kAsmThreads = kAsmWarps * 32;
+#ifndef UVD_ASM_MINB
+#define UVD_ASM_MINB 4
+#endif
+constexpr int kAsmMinBlocks = UVD_ASM_MINB;  // <= 85 registers: 24 warps per SM to hide node-fetch latency
 
 struct AsmParams {
   const float4* __restrict__ tri;
-  const Node* __restrict__ nodes;
+  const Node4* __restrict__ nodes4;
+  const Node* __restrict__ nodes;  // BVH2 (per-lane traversal)
   uint32_t root;
   const float* __restrict__ centroid;
   const float* __restrict__ normal;
@@ -48,75 +54,198 @@ struct AsmParams {
   int* __restrict__ err;
 };
 
-// warp-cooperative any-hit walk; returns false for active lanes whose segment is
-// blocked (inactive lanes return true: the caller ANDs with its own mask).
+// rare path (fp32 filter ambiguous): exact fp64 re-test of segment p -> c from
+// the fp32 inputs.  Kept out of line so its fp64 registers do not count
+// against the traversal loop's occupancy.
+__device__ __forceinline__ int exact_retest(float px, float py, float pz, float cx, float cy, float cz,
+                                         float4 a, float4 b, float4 c) {
+  D3 O = d3(px, py, pz);
+  D3 D = d3((double)cx - O.x, (double)cy - O.y, (double)cz - O.z);
+  double dd = ddot3(D, D);
+  double t_lo = kSelfEps / sqrt(dd);
+  return seg_hits_tri(O, D, dd, t_lo, 1.0 - t_lo, a, b, c) ? 1 : 0;
+}
+
+// Per-warp shared state of the pair-parallel walk.
+constexpr int kAmbCap = 32 + 4 * 32;  // deferred fp64 re-tests per warp: < 32 pending + one leaf (<= 4 rounds x 32)
+struct WarpSmem {
+  uint2 stack[kStackDepth];  // (node ref, ray mask)
+  uint32_t list[32];         // compaction: k-th ray of the current mask -> lane
+  float4 ray[32][3];         // per ray: (1/d, -), (d, t_lo), (t_hi, owner, |d|_1, -)
+  uint2 amb[kAmbCap];        // (ray lane, triangle index) pairs the fp32 filter left open
+};
+
+// Warp-cooperative, pair-parallel any-hit walk over the BVH4.
+//
+// The 32 rays of a warp share the lamp origin o.  The warp keeps ONE current
+// node and a stack of (ref, ray mask) entries; the mask holds the rays whose
+// segment entered that node's box.  Work on a node or leaf is spread over
+// (ray, child) PAIRS rather than over rays: lane l takes child/triangle l&3 of
+// the (q·8 + l>>2)-th ray of the mask (compaction list in shared memory), so a
+// node needed by n rays costs ceil(n/8) slab rounds instead of 4 tests per
+// lane, and a 4-triangle leaf ceil(n/8) triangle rounds instead of 4.  Per-child
+// ray masks are rebuilt with warp OR-reductions; the fullest child is descended
+// next, the others pushed; entries whose rays have all been occluded meanwhile
+// are dropped unfetched.  Returns the warp's mask of occluded rays.
 template <bool COUNT>
-__device__ __forceinline__ bool warp_trace_clear(const AsmParams& P, uint32_t* __restrict__ stack,
-                                                 bool active, const Ray32& r32, D3 O, D3 D,
-                                                 double dd, double t_lo, double t_hi,
-                                                 int owner, unsigned long long* cnt) {
+__device__ __forceinline__ uint32_t warp_trace_pairs(const AsmParams& P, WarpSmem& W, uint32_t live,
+                                                     float ox, float oy, float oz,
+                                                     unsigned long long* cnt) {
   const int lane = threadIdx.x & 31;
-  bool occluded = false;
-  uint32_t live = __ballot_sync(0xffffffffu, active);
-  if (!live) return !occluded;
+  const int k = lane & 3;          // child / triangle slot of this lane
+  const int sub = lane >> 2;       // ray slot within a round of 8
+  uint32_t occ = 0;
+  uint32_t ref = P.root, mask = live;
   int sp = 0;
-  if (lane == 0) stack[0] = P.root;
-  sp = 1;
-  __syncwarp();
-  while (sp > 0) {
-    --sp;
-    uint32_t ref = stack[sp];
-    if (ref_is_leaf(ref)) {
-      uint32_t st = ref_start(ref), nt = ref_count(ref);
-      for (uint32_t k = 0; k < nt; ++k) {
-        const float4* t = P.tri + 3 * (int64_t)(st + k);
-        float4 a = __ldg(t), b = __ldg(t + 1), c = __ldg(t + 2);
-        bool test = active && !occluded && __float_as_int(a.w) != owner;
-        if (COUNT) cnt[2] += __popc(__ballot_sync(0xffffffffu, test));
-        if (test) occluded = seg_hits_tri(O, D, dd, t_lo, t_hi, a, b, c);
-      }
-      live = __ballot_sync(0xffffffffu, active && !occluded);
-      if (!live) break;
-    } else {
-      const Node* nd = P.nodes + ref;
-      float4 na = __ldg(&nd->a), nb = __ldg(&nd->b), nc = __ldg(&nd->c);
-      uint4 ndd = __ldg(&nd->d);
-      bool me = active && !occluded;
-      if (COUNT) {
-        cnt[1] += 2 * __popc(__ballot_sync(0xffffffffu, me));
-        cnt[3] += 1;
-      }
-      bool h0 = me && slab(r32, na.x, na.y, na.z, na.w, nc.x, nc.y, 1.0f);
-      bool h1 = me && slab(r32, nb.x, nb.y, nb.z, nb.w, nc.z, nc.w, 1.0f);
-      uint32_t m0 = __ballot_sync(0xffffffffu, h0), m1 = __ballot_sync(0xffffffffu, h1);
+  bool done = false;
+  for (;;) {
+    int n_amb = 0;
+    // ---- walk until done or until >= 32 fp64 re-tests are pending ----
+    while (!done && n_amb < 32) {
+      // compaction list of the rays in `mask`
+      const int n = __popc(mask);
+      if ((mask >> lane) & 1u) W.list[__popc(mask & ((1u << lane) - 1u))] = (uint32_t)lane;
       __syncwarp();
-      if (m0 && m1) {
-        // descend into the child more lanes want first (pushed last)
-        bool first0 = __popc(m0) >= __popc(m1);
-        if (lane == 0) {
-          stack[sp] = first0 ? ndd.y : ndd.x;
-          stack[sp + 1] = first0 ? ndd.x : ndd.y;
+      bool pop = false;
+      if (!ref_is_leaf(ref)) {
+        const Node4* nd = P.nodes4 + ref;
+        const float4 lo = __ldg(&nd->c[2 * k]), hi = __ldg(&nd->c[2 * k + 1]);
+        const uint32_t cref = __float_as_uint(lo.w);
+        uint32_t m0 = 0, m1 = 0, m2 = 0, m3 = 0;
+        for (int q = 0; q * 8 < n; ++q) {
+          const int s = q * 8 + sub;
+          uint32_t val = 0;
+          if (s < n && cref != kEmptyRef) {
+            const uint32_t r = W.list[s];
+            const float4 iv = W.ray[r][0];
+            const float tx0 = (lo.x - ox) * iv.x, tx1 = (hi.x - ox) * iv.x;
+            const float ty0 = (lo.y - oy) * iv.y, ty1 = (hi.y - oy) * iv.y;
+            const float tz0 = (lo.z - oz) * iv.z, tz1 = (hi.z - oz) * iv.z;
+            const float tn = fmaxf(fmaxf(fminf(tx0, tx1), fminf(ty0, ty1)), fmaxf(fminf(tz0, tz1), 0.0f));
+            const float tf = fminf(fminf(fmaxf(tx0, tx1), fmaxf(ty0, ty1)), fminf(fmaxf(tz0, tz1), 1.0f));
+            if (tn <= tf * 1.000002f + 1e-7f) val = 1u << r;
+          }
+          m0 |= __reduce_or_sync(0xffffffffu, k == 0 ? val : 0u);
+          m1 |= __reduce_or_sync(0xffffffffu, k == 1 ? val : 0u);
+          m2 |= __reduce_or_sync(0xffffffffu, k == 2 ? val : 0u);
+          m3 |= __reduce_or_sync(0xffffffffu, k == 3 ? val : 0u);
         }
-        sp += 2;
-      } else if (m0 | m1) {
-        if (lane == 0) stack[sp] = m0 ? ndd.x : ndd.y;
-        sp += 1;
+        if (COUNT) {
+          cnt[1] += (unsigned long long)n * __popc(__ballot_sync(0xffffffffu, lane < 4 && cref != kEmptyRef));
+          cnt[3] += 1;
+        }
+        const int p0 = __popc(m0), p1 = __popc(m1), p2 = __popc(m2), p3 = __popc(m3);
+        int best = 0, pb = p0;
+        if (p1 > pb) { best = 1; pb = p1; }
+        if (p2 > pb) { best = 2; pb = p2; }
+        if (p3 > pb) { best = 3; pb = p3; }
+        if (pb == 0) {
+          pop = true;
+        } else {
+          const bool q0 = p0 && best != 0, q1 = p1 && best != 1, q2 = p2 && best != 2, q3 = p3 && best != 3;
+          const uint32_t mk = k == 0 ? m0 : k == 1 ? m1 : k == 2 ? m2 : m3;
+          const bool mine = lane < 4 && (k == 0 ? q0 : k == 1 ? q1 : k == 2 ? q2 : q3);
+          if (mine) {
+            const int slot = sp + (k > 0 && q0) + (k > 1 && q1) + (k > 2 && q2);
+            W.stack[slot] = make_uint2(cref, mk);
+          }
+          sp += (int)q0 + (int)q1 + (int)q2 + (int)q3;
+          ref = __shfl_sync(0xffffffffu, cref, best);
+          mask = best == 0 ? m0 : best == 1 ? m1 : best == 2 ? m2 : m3;
+          if (sp > kStackDepth - 4) {  // cannot happen for depth < 40; fail loudly
+            if (lane == 0) atomicExch(P.err, 2);
+            return occ;
+          }
+        }
+      } else {
+        const uint32_t st = ref_start(ref), nt = ref_count(ref);
+        const bool have = (uint32_t)k < nt;
+        const uint32_t ti = st + (uint32_t)k;
+        float4 a = make_float4(0.f, 0.f, 0.f, 0.f), b = a, c = a;
+        if (have) {
+          const float4* t = P.tri + 3 * (int64_t)ti;
+          a = __ldg(t); b = __ldg(t + 1); c = __ldg(t + 2);
+        }
+        uint32_t hits = 0;
+        for (int q = 0; q * 8 < n; ++q) {
+          const int s = q * 8 + sub;
+          uint32_t val = 0;
+          bool test = false, amb = false;
+          uint32_t r = 0;
+          if (s < n && have) {
+            r = W.list[s];
+            test = __float_as_int(a.w) != __float_as_int(W.ray[r][2].y);  // not the target's own
+          }
+          if (COUNT) cnt[2] += __popc(__ballot_sync(0xffffffffu, test));
+          if (test) {
+            const float4 d = W.ray[r][1], e = W.ray[r][2];
+            const int cls = seg_tri_filter32(ox, oy, oz, d.x, d.y, d.z, e.z, d.w, e.x, a, b, c);
+            if (cls == 1) val = 1u << r;
+            amb = cls == 2;
+          }
+          hits |= __reduce_or_sync(0xffffffffu, val);
+          // defer fp64 re-tests (queue; flushed outside this loop)
+          const uint32_t am = __ballot_sync(0xffffffffu, amb);
+          if (amb) W.amb[n_amb + __popc(am & ((1u << lane) - 1u))] = make_uint2(r, ti);
+          n_amb += __popc(am);
+        }
+        occ |= hits;
+        live &= ~hits;
+        pop = true;
       }
-      if (sp > kStackDepth - 2) {  // cannot happen for depth < 126; fail loudly
-        if (lane == 0) atomicExch(P.err, 2);
-        break;
+      if (pop) {
+        for (;;) {
+          if (sp == 0 || !live) { done = true; break; }
+          const uint2 e = W.stack[--sp];
+          ref = e.x;
+          mask = e.y & live;
+          if (mask) break;
+        }
       }
       __syncwarp();
     }
+    // ---- exact fp64 re-tests of the pending ambiguous pairs ----
+    if (n_amb) {
+      __syncwarp();
+      uint32_t hits = 0;
+      for (int e0 = 0; e0 < n_amb; e0 += 32) {
+        uint32_t val = 0;
+        const int e = e0 + lane;
+        if (e < n_amb) {
+          const uint2 q = W.amb[e];
+          if ((live >> q.x) & 1u) {
+            const int row = __float_as_int(W.ray[q.x][2].y);
+            const float4* t = P.tri + 3 * (int64_t)q.y;
+            if (exact_retest(ox, oy, oz, P.centroid[3 * row], P.centroid[3 * row + 1],
+                             P.centroid[3 * row + 2], __ldg(t), __ldg(t + 1), __ldg(t + 2)))
+              val = 1u << q.x;
+          }
+        }
+        hits |= __reduce_or_sync(0xffffffffu, val);
+      }
+      occ |= hits;
+      live &= ~hits;
+      __syncwarp();
+      if (!live) done = true;
+      if (!done && !mask) {  // the current entry lost all its rays: pop
+        for (;;) {
+          if (sp == 0) { done = true; break; }
+          const uint2 e = W.stack[--sp];
+          ref = e.x;
+          mask = e.y & live;
+          if (mask) break;
+        }
+      }
+    }
+    if (done) return occ;
+    mask &= live;
   }
-  return !occluded;
 }
 
 template <bool COUNT>
-__global__ void __launch_bounds__(kAsmThreads) k_assemble(AsmParams P) {
-  __shared__ uint32_t s_stack[kAsmWarps][kStackDepth];
+__global__ void __launch_bounds__(kAsmThreads, kAsmMinBlocks) k_assemble(AsmParams P) {
+  __shared__ WarpSmem s_w[kAsmWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  uint32_t* stack = s_stack[warp];
   unsigned long long cnt[4] = {0, 0, 0, 0};  // warp-uniform tallies (COUNT only)
   const int64_t total = P.n_cols * P.tiles;
   for (int64_t item = (int64_t)blockIdx.x * kAsmWarps + warp; item < total;
@@ -125,41 +254,56 @@ __global__ void __launch_bounds__(kAsmThreads) k_assemble(AsmParams P) {
     const int64_t j = P.cols ? P.cols[c] : c;
     const int64_t r = tile * 32 + lane;
     const bool valid = r < P.N;
-    float cx = 0.f, cy = 0.f, cz = 0.f, nx = 0.f, ny = 0.f, nz = 0.f;
-    if (valid) {
-      cx = P.centroid[3 * r]; cy = P.centroid[3 * r + 1]; cz = P.centroid[3 * r + 2];
-      nx = P.normal[3 * r]; ny = P.normal[3 * r + 1]; nz = P.normal[3 * r + 2];
-    }
     double acc = 0.0;
     for (int l = 0; l < P.L; ++l) {
       const float* pl = P.lamps + 3 * (j * P.L + l);
-      const float px = pl[0], py = pl[1], pz = pl[2];
       // a4: ray p -> c in fp64 (exact differences of fp32 inputs), front-face cull
-      D3 O = d3(px, py, pz);
-      D3 D = d3((double)cx - (double)px, (double)cy - (double)py, (double)cz - (double)pz);
-      double dd = ddot3(D, D);
-      double d = sqrt(dd);
-      double cosd = -(D.x * (double)nx + D.y * (double)ny + D.z * (double)nz);  // <p - c, n>
-      bool front = valid && cosd > 0.0;
-      if (valid && d < kMinDist) {
-        atomicExch(P.err, 1);
-        front = false;
+      bool front = false;
+      float ox, oy, oz;
+      {
+        ox = pl[0]; oy = pl[1]; oz = pl[2];
+        float fdx = 0.f, fdy = 0.f, fdz = 0.f, tlo32 = 0.f, thi32 = 0.f;
+        if (valid) {
+          const float cx = P.centroid[3 * r], cy = P.centroid[3 * r + 1], cz = P.centroid[3 * r + 2];
+          const float nx = P.normal[3 * r], ny = P.normal[3 * r + 1], nz = P.normal[3 * r + 2];
+          D3 D = d3((double)cx - (double)ox, (double)cy - (double)oy, (double)cz - (double)oz);
+          double dd = ddot3(D, D);
+          double d = sqrt(dd);
+          double cosd = -(D.x * (double)nx + D.y * (double)ny + D.z * (double)nz);  // <p - c, n>
+          front = cosd > 0.0;
+          if (d < kMinDist) {
+            atomicExch(P.err, 1);
+            front = false;
+          }
+          const double t_lo = kSelfEps / d;
+          fdx = (float)D.x; fdy = (float)D.y; fdz = (float)D.z;
+          tlo32 = (float)t_lo;
+          thi32 = (float)(1.0 - t_lo);
+        }
+        WarpSmem& W = s_w[warp];
+        W.ray[lane][0] = make_float4(safe_inv(fdx), safe_inv(fdy), safe_inv(fdz), 0.f);
+        W.ray[lane][1] = make_float4(fdx, fdy, fdz, tlo32);
+        W.ray[lane][2] = make_float4(thi32, __int_as_float((int)r), fabsf(fdx) + fabsf(fdy) + fabsf(fdz), 0.f);
       }
       uint32_t fm = __ballot_sync(0xffffffffu, front);
       if (COUNT) cnt[0] += __popc(fm);
-      bool vis = front;
+      uint32_t vm = fm;
       if (fm) {
         // a5: occlusion of the open segment, t in (1e-4/d, 1 - 1e-4/d)
-        double t_lo = front ? kSelfEps / d : 0.0;
-        Ray32 r32 = make_ray32(px, py, pz, (float)D.x, (float)D.y, (float)D.z);
-        vis = warp_trace_clear<COUNT>(P, stack, front, r32, O, D, dd, t_lo, 1.0 - t_lo, (int)r, cnt) &&
-              front;
+        __syncwarp();
+        vm &= ~warp_trace_pairs<COUNT>(P, s_w[warp], fm, ox, oy, oz, cnt);
+        __syncwarp();
       }
-      uint32_t vm = __ballot_sync(0xffffffffu, vis);
       if (P.vis_bits && lane == 0 && tile < P.words)
         P.vis_bits[(c * P.L + l) * P.words + tile] = vm;
-      // a6: Eq. 7 in fp64
-      if (vis) acc += cosd / (dd * d);
+      if ((vm >> lane) & 1u) {  // a6: Eq. 7 in fp64 (recomputed from the fp32 inputs)
+        const float cx = P.centroid[3 * r], cy = P.centroid[3 * r + 1], cz = P.centroid[3 * r + 2];
+        const float nx = P.normal[3 * r], ny = P.normal[3 * r + 1], nz = P.normal[3 * r + 2];
+        D3 D = d3((double)cx - (double)ox, (double)cy - (double)oy, (double)cz - (double)oz);
+        double dd = ddot3(D, D);
+        double cosd = -(D.x * (double)nx + D.y * (double)ny + D.z * (double)nz);
+        acc += cosd / (dd * sqrt(dd));
+      }
     }
     const float a = (float)(acc * P.scale);
     if (P.values) P.values[c * P.ld + r] = a;
@@ -174,12 +318,171 @@ __global__ void __launch_bounds__(kAsmThreads) k_assemble(AsmParams P) {
       if (cnt[k]) atomicAdd(P.counters + k, cnt[k]);
 }
 
+// ---------------------------------------------------------------------------
+// Per-lane traversal (Aila & Laine 2009 "while-while"): every lane walks its
+// own shadow ray through the BVH2 with a private stack (local memory, L1
+// resident at the top), near child first; triangles are tested with the fp32
+// filter and ambiguous cases re-tested exactly in fp64; any hit ends the ray.
+// The 32 rays of a warp share the lamp origin and end on 32 Morton-adjacent
+// patches, so the lanes fetch mostly the same nodes (L1 broadcast) and
+// diverge little.
+constexpr int kLaneStack = 64;
+constexpr int kLaneAmb = 16;  // deferred fp64 re-tests per lane before a flush
+constexpr uint32_t kDone = 0xffffffffu;
+
+enum { kWalkClear = 0, kWalkBlocked = 1, kWalkFlush = 2 };
+
+// One lane's walk; returns kWalkClear (stack exhausted), kWalkBlocked (a
+// certain hit) or kWalkFlush (the ambiguous list is full; state kept in
+// ref/sp/stk so the walk resumes after the flush).
 template <bool COUNT>
-static int grid_size_assemble() {
+__device__ __forceinline__ int lane_walk(const AsmParams& P, uint32_t* stk, int& sp, uint32_t& ref,
+                                         uint32_t* amb, int& namb, float ox, float oy, float oz,
+                                         float dx, float dy, float dz, float ix, float iy, float iz,
+                                         float nD, float tlo, float thi, int owner,
+                                         unsigned long long* cnt) {
+  for (;;) {
+    // ---- inner nodes until this lane holds a leaf (or is done) ----
+    while (!ref_is_leaf(ref)) {
+      const Node* nd = P.nodes + ref;
+      const float4 na = __ldg(&nd->a), nb = __ldg(&nd->b), nc = __ldg(&nd->c);
+      const uint2 ch = __ldg(reinterpret_cast<const uint2*>(&nd->d));
+      if (COUNT) { cnt[1] += 2; cnt[3] += 1; }
+      const float ax0 = (na.x - ox) * ix, ax1 = (na.y - ox) * ix;
+      const float ay0 = (na.z - oy) * iy, ay1 = (na.w - oy) * iy;
+      const float az0 = (nc.x - oz) * iz, az1 = (nc.y - oz) * iz;
+      const float bx0 = (nb.x - ox) * ix, bx1 = (nb.y - ox) * ix;
+      const float by0 = (nb.z - oy) * iy, by1 = (nb.w - oy) * iy;
+      const float bz0 = (nc.z - oz) * iz, bz1 = (nc.w - oz) * iz;
+      const float an = fmaxf(fmaxf(fminf(ax0, ax1), fminf(ay0, ay1)), fmaxf(fminf(az0, az1), 0.0f));
+      const float af = fminf(fminf(fmaxf(ax0, ax1), fmaxf(ay0, ay1)), fminf(fmaxf(az0, az1), 1.0f));
+      const float bn = fmaxf(fmaxf(fminf(bx0, bx1), fminf(by0, by1)), fmaxf(fminf(bz0, bz1), 0.0f));
+      const float bf = fminf(fminf(fmaxf(bx0, bx1), fmaxf(by0, by1)), fminf(fmaxf(bz0, bz1), 1.0f));
+      const bool h0 = an <= af * 1.000002f + 1e-7f;
+      const bool h1 = bn <= bf * 1.000002f + 1e-7f;
+      if (h0 && h1) {
+        const bool swap = bn < an;  // near child first
+        ref = swap ? ch.y : ch.x;
+        if (sp < kLaneStack) stk[sp++] = swap ? ch.x : ch.y;
+        else atomicExch(P.err, 2);  // cannot happen for depth < 64; fail loudly
+      } else if (h0 || h1) {
+        ref = h0 ? ch.x : ch.y;
+      } else {
+        ref = sp ? stk[--sp] : kDone;
+      }
+    }
+    if (ref == kDone) return kWalkClear;
+    // ---- leaf: up to 4 triangles ----
+    const uint32_t st = ref_start(ref), nt = ref_count(ref);
+    for (uint32_t k = 0; k < nt; ++k) {
+      const float4* t = P.tri + 3 * (int64_t)(st + k);
+      const float4 a = __ldg(t);
+      if (__float_as_int(a.w) == owner) continue;  // the target's own triangles
+      const float4 b = __ldg(t + 1), c = __ldg(t + 2);
+      if (COUNT) cnt[2] += 1;
+      const int cls = seg_tri_filter32(ox, oy, oz, dx, dy, dz, nD, tlo, thi, a, b, c);
+      if (cls == 1) return kWalkBlocked;
+      if (cls == 2) amb[namb++] = st + k;  // exact re-test deferred (outside the walk)
+    }
+    ref = sp ? stk[--sp] : kDone;
+    if (namb > kLaneAmb - 4) return kWalkFlush;  // room for one more leaf
+    if (ref == kDone) return kWalkClear;
+  }
+}
+
+// Is the open segment p -> c (t in (t_lo, t_hi)) clear of every scene triangle
+// except patch `owner`'s own?
+template <bool COUNT>
+__device__ __forceinline__ bool lane_trace_clear(const AsmParams& P, float ox, float oy, float oz,
+                                                 float dx, float dy, float dz, float tlo, float thi,
+                                                 int owner, unsigned long long* cnt) {
+  uint32_t stk[kLaneStack];
+  uint32_t amb[kLaneAmb];
+  int sp = 0, namb = 0;
+  uint32_t ref = P.root;
+  const float ix = safe_inv(dx), iy = safe_inv(dy), iz = safe_inv(dz);
+  const float nD = fabsf(dx) + fabsf(dy) + fabsf(dz);
+  for (;;) {
+    const int st = lane_walk<COUNT>(P, stk, sp, ref, amb, namb, ox, oy, oz, dx, dy, dz, ix, iy, iz, nD,
+                                    tlo, thi, owner, cnt);
+    if (st == kWalkBlocked) return false;
+    // exact fp64 re-tests of the triangles the fp32 filter could not decide
+    if (namb) {
+      const float cx = P.centroid[3 * owner], cy = P.centroid[3 * owner + 1], cz = P.centroid[3 * owner + 2];
+      for (int e = 0; e < namb; ++e) {
+        const float4* t = P.tri + 3 * (int64_t)amb[e];
+        if (exact_retest(ox, oy, oz, cx, cy, cz, __ldg(t), __ldg(t + 1), __ldg(t + 2))) return false;
+      }
+      namb = 0;
+    }
+    if (st == kWalkClear) return true;
+  }
+}
+
+template <bool COUNT>
+__global__ void __launch_bounds__(kAsmThreads, kAsmMinBlocks) k_assemble_lane(AsmParams P) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  unsigned long long cnt[4] = {0, 0, 0, 0};  // per-lane tallies (COUNT only)
+  const int64_t total = P.n_cols * P.tiles;
+  for (int64_t item = (int64_t)blockIdx.x * kAsmWarps + warp; item < total;
+       item += (int64_t)gridDim.x * kAsmWarps) {
+    const int64_t c = item / P.tiles, tile = item - c * P.tiles;
+    const int64_t j = P.cols ? P.cols[c] : c;
+    const int64_t r = tile * 32 + lane;
+    const bool valid = r < P.N;
+    double acc = 0.0;
+    for (int l = 0; l < P.L; ++l) {
+      const float* pl = P.lamps + 3 * (j * P.L + l);
+      const float ox = pl[0], oy = pl[1], oz = pl[2];
+      bool vis = false;
+      if (valid) {
+        const float cx = P.centroid[3 * r], cy = P.centroid[3 * r + 1], cz = P.centroid[3 * r + 2];
+        const float nx = P.normal[3 * r], ny = P.normal[3 * r + 1], nz = P.normal[3 * r + 2];
+        // a4: ray p -> c in fp64 (exact differences of fp32 inputs), front-face cull
+        const D3 D = d3((double)cx - (double)ox, (double)cy - (double)oy, (double)cz - (double)oz);
+        const double dd = ddot3(D, D);
+        const double d = sqrt(dd);
+        const double cosd = -(D.x * (double)nx + D.y * (double)ny + D.z * (double)nz);  // <p - c, n>
+        bool front = cosd > 0.0;
+        if (d < kMinDist) {
+          atomicExch(P.err, 1);
+          front = false;
+        }
+        if (front) {
+          if (COUNT) cnt[0] += 1;
+          // a5: occlusion of the open segment, t in (1e-4/d, 1 - 1e-4/d)
+          const double t_lo = kSelfEps / d;
+          vis = lane_trace_clear<COUNT>(P, ox, oy, oz, (float)D.x, (float)D.y, (float)D.z,
+                                        (float)t_lo, (float)(1.0 - t_lo), (int)r, cnt);
+          if (vis) acc += cosd / (dd * d);  // a6: Eq. 7 in fp64
+        }
+      }
+      const uint32_t vm = __ballot_sync(0xffffffffu, vis);
+      if (P.vis_bits && lane == 0 && tile < P.words) P.vis_bits[(c * P.L + l) * P.words + tile] = vm;
+    }
+    const float a = (float)(acc * P.scale);
+    if (P.values) P.values[c * P.ld + r] = a;
+    if (P.col_sumsq) {
+      double q = (double)a * (double)a;
+      for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+      if (lane == 0 && q != 0.0) atomicAdd(P.col_sumsq + c, q);
+    }
+  }
+  if (COUNT)
+    for (int k = 0; k < 4; ++k) {
+      unsigned long long v = cnt[k];
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0 && v) atomicAdd(P.counters + k, v);
+    }
+}
+
+template <bool COUNT>
+static int grid_size_assemble(int algo) {
   int dev = 0, sms = 0, per = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_assemble<COUNT>, kAsmThreads, 0);
+  if (algo == 1) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_assemble<COUNT>, kAsmThreads, 0);
+  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_assemble_lane<COUNT>, kAsmThreads, 0);
   return std::max(1, sms * std::max(per, 1));
 }
 
@@ -227,6 +530,7 @@ extern "C" int uvd_irradiance_matrix(const uvd_scene* s, const float* lamp_xyz, 
   }
   AsmParams P;
   P.tri = s->tri;
+  P.nodes4 = s->nodes4;
   P.nodes = s->nodes;
   P.root = s->root;
   P.centroid = s->centroid;
@@ -246,14 +550,22 @@ extern "C" int uvd_irradiance_matrix(const uvd_scene* s, const float* lamp_xyz, 
   P.counters = out->counters;
   P.err = s->err_flag;
   if (P.col_sumsq) UVD_CUDA_TRY(cudaMemsetAsync(P.col_sumsq, 0, n_cols * sizeof(double), st));
+  // algorithm: 0 = per-lane while-while over the BVH2 (default), 1 = warp
+  // pair-parallel packets over the BVH4 (UVD_ASM_ALGO=1, kept for comparison)
+  static int algo = -1;
+  if (algo < 0) {
+    const char* e = getenv("UVD_ASM_ALGO");
+    algo = e ? atoi(e) : 0;
+  }
+  static int grid_c = 0, grid = 0;
   if (P.counters) {
-    static int grid_c = 0;
-    if (!grid_c) grid_c = grid_size_assemble<true>();
-    k_assemble<true><<<grid_c, kAsmThreads, 0, st>>>(P);
+    if (!grid_c) grid_c = grid_size_assemble<true>(algo);
+    if (algo == 1) k_assemble<true><<<grid_c, kAsmThreads, 0, st>>>(P);
+    else k_assemble_lane<true><<<grid_c, kAsmThreads, 0, st>>>(P);
   } else {
-    static int grid = 0;
-    if (!grid) grid = grid_size_assemble<false>();
-    k_assemble<false><<<grid, kAsmThreads, 0, st>>>(P);
+    if (!grid) grid = grid_size_assemble<false>(algo);
+    if (algo == 1) k_assemble<false><<<grid, kAsmThreads, 0, st>>>(P);
+    else k_assemble_lane<false><<<grid, kAsmThreads, 0, st>>>(P);
   }
   note_launch();
   UVD_CUDA_TRY(cudaGetLastError());

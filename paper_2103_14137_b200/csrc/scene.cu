@@ -189,8 +189,43 @@ __global__ void __launch_bounds__(1024) k_sum_area(const double* __restrict__ a,
 
 static inline unsigned grid_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
-static bool finite3(const float* p) {
-  return std::isfinite(p[0]) && std::isfinite(p[1]) && std::isfinite(p[2]);
+// vertex validation + bbox on the device: per-block min/max partials and the
+// first non-finite vertex index
+constexpr int kBoxThreads = 256;
+__global__ void __launch_bounds__(kBoxThreads) k_vert_bbox(const float* __restrict__ V, int64_t nv,
+                                                           float* __restrict__ part,
+                                                           unsigned long long* __restrict__ bad) {
+  __shared__ float s[6][kBoxThreads];
+  float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int64_t v = blockIdx.x * (int64_t)kBoxThreads + threadIdx.x; v < nv;
+       v += (int64_t)gridDim.x * kBoxThreads) {
+    float p[3] = {V[3 * v], V[3 * v + 1], V[3 * v + 2]};
+    for (int k = 0; k < 3; ++k) {
+      if (!isfinite(p[k])) atomicMin(bad, (unsigned long long)v);
+      lo[k] = fminf(lo[k], p[k]);
+      hi[k] = fmaxf(hi[k], p[k]);
+    }
+  }
+  for (int k = 0; k < 3; ++k) { s[k][threadIdx.x] = lo[k]; s[3 + k][threadIdx.x] = hi[k]; }
+  __syncthreads();
+  for (int off = kBoxThreads / 2; off > 0; off >>= 1) {
+    if (threadIdx.x < off)
+      for (int k = 0; k < 3; ++k) {
+        s[k][threadIdx.x] = fminf(s[k][threadIdx.x], s[k][threadIdx.x + off]);
+        s[3 + k][threadIdx.x] = fmaxf(s[3 + k][threadIdx.x], s[3 + k][threadIdx.x + off]);
+      }
+    __syncthreads();
+  }
+  if (threadIdx.x < 6) part[6 * blockIdx.x + threadIdx.x] = s[threadIdx.x][0];
+}
+
+__global__ void k_bbox_final(const float* __restrict__ part, int nb, float* __restrict__ out) {
+  if (threadIdx.x < 6) {
+    float v = threadIdx.x < 3 ? INFINITY : -INFINITY;
+    for (int b = 0; b < nb; ++b)
+      v = threadIdx.x < 3 ? fminf(v, part[6 * b + threadIdx.x]) : fmaxf(v, part[6 * b + threadIdx.x]);
+    out[threadIdx.x] = v;
+  }
 }
 
 static int create_trimesh(uvd_scene* s, const uvd_scene_desc* d, cudaStream_t st) {
@@ -202,16 +237,6 @@ static int create_trimesh(uvd_scene* s, const uvd_scene_desc* d, cudaStream_t st
     set_error("scene: at most 2^28 triangles supported (got %lld)", (long long)d->n_tris);
     return UVD_ERR_INVALID;
   }
-  float lo[3] = {INFINITY, INFINITY, INFINITY}, hi[3] = {-INFINITY, -INFINITY, -INFINITY};
-  for (int64_t v = 0; v < d->n_vertices; ++v) {
-    const float* p = d->vertices + 3 * v;
-    if (!finite3(p)) {
-      set_error("scene: vertex %lld is not finite", (long long)v);
-      return UVD_ERR_INVALID;
-    }
-    for (int k = 0; k < 3; ++k) { lo[k] = std::min(lo[k], p[k]); hi[k] = std::max(hi[k], p[k]); }
-  }
-  for (int k = 0; k < 3; ++k) { s->bbox[k] = lo[k]; s->bbox[3 + k] = hi[k]; }
   Alloc& al = s->alloc;
   const int64_t M = d->n_tris, NV = d->n_vertices;
   s->M = M;
@@ -227,9 +252,32 @@ static int create_trimesh(uvd_scene* s, const uvd_scene_desc* d, cudaStream_t st
     set_error("scene: out of device memory (M=%lld)", (long long)M);
     return UVD_ERR_NOMEM;
   }
-  UVD_CUDA_TRY(cudaMemcpyAsync(dV, d->vertices, NV * 3 * sizeof(float), cudaMemcpyHostToDevice, st));
-  UVD_CUDA_TRY(cudaMemcpyAsync(dF, d->tris, M * 3 * sizeof(int32_t), cudaMemcpyHostToDevice, st));
+  const cudaMemcpyKind kind = d->device_input ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+  UVD_CUDA_TRY(cudaMemcpyAsync(dV, d->vertices, NV * 3 * sizeof(float), kind, st));
+  UVD_CUDA_TRY(cudaMemcpyAsync(dF, d->tris, M * 3 * sizeof(int32_t), kind, st));
   UVD_CUDA_TRY(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), st));
+  {
+    int nb = (int)std::min<int64_t>((NV + kBoxThreads - 1) / kBoxThreads, 1184);
+    float* part = (float*)al.get((size_t)nb * 6 * sizeof(float) + 6 * sizeof(float) + 64);
+    unsigned long long* vbad = (unsigned long long*)al.get(sizeof(unsigned long long));
+    if (!part || !vbad) { set_error("scene: out of device memory"); return UVD_ERR_NOMEM; }
+    float* box = part + 6 * nb;
+    UVD_CUDA_TRY(cudaMemsetAsync(vbad, 0xff, sizeof(unsigned long long), st));
+    k_vert_bbox<<<nb, kBoxThreads, 0, st>>>(dV, NV, part, vbad);
+    note_launch();
+    k_bbox_final<<<1, 32, 0, st>>>(part, nb, box);
+    note_launch();
+    unsigned long long h_vbad = 0;
+    UVD_CUDA_TRY(cudaMemcpyAsync(s->bbox, box, 6 * sizeof(float), cudaMemcpyDeviceToHost, st));
+    UVD_CUDA_TRY(cudaMemcpyAsync(&h_vbad, vbad, sizeof(h_vbad), cudaMemcpyDeviceToHost, st));
+    UVD_CUDA_TRY(cudaStreamSynchronize(st));
+    al.put(part);
+    al.put(vbad);
+    if (h_vbad != ~0ull) {
+      set_error("scene: vertex %llu is not finite", h_vbad);
+      return UVD_ERR_INVALID;
+    }
+  }
   k_tri_attrs<<<grid_for(M, 256), 256, 0, st>>>(dV, NV, dF, M, tri_in, cen_in, nrm_in, area_in, bad);
   note_launch();
   unsigned long long h_bad = 0;
@@ -355,7 +403,7 @@ static void free_scene(uvd_scene* s) {
   if (!s) return;
   Alloc& al = s->alloc;
   for (void* p : {(void*)s->centroid, (void*)s->normal, (void*)s->area, (void*)s->orig_id,
-                  (void*)s->tri, (void*)s->nodes, (void*)s->walls, (void*)s->poly_xy,
+                  (void*)s->tri, (void*)s->nodes, (void*)s->nodes4, (void*)s->walls, (void*)s->poly_xy,
                   (void*)s->poly_off, (void*)s->err_flag})
     al.put(p);
   cudaStreamSynchronize(al.stream);

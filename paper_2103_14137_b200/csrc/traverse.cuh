@@ -79,6 +79,47 @@ __device__ __forceinline__ bool seg_hits_tri(D3 O, D3 D, double dd /* D·D */, d
   return W - t_lo * A >= -tol && t_hi * A - W >= -tol;
 }
 
+// fp32 filtered segment/triangle test.  Same division-free Möller–Trumbore in
+// fp32 from the exact fp32 vertices and lamp origin, with the fp32-rounded
+// direction; every quantity carries a forward error bound (32 ulp × the 1-norm
+// product of its factors — the rounding of D, T, E1, E2 and of the products
+// are all below that), so each margin is classified as a certain miss (< -err),
+// a certain hit (> +err) or ambiguous.  Returns 0 miss, 1 hit, 2 ambiguous
+// (the caller re-tests those in fp64 with seg_hits_tri).
+__device__ __forceinline__ int seg_tri_filter32(float ox, float oy, float oz, float dx, float dy,
+                                                float dz, float nD, float t_lo, float t_hi,
+                                                float4 a, float4 b, float4 c) {
+  const float k = 32.0f * 5.9604645e-08f;
+  float e1x = b.x - a.x, e1y = b.y - a.y, e1z = b.z - a.z;
+  float e2x = c.x - a.x, e2y = c.y - a.y, e2z = c.z - a.z;
+  float tx = ox - a.x, ty = oy - a.y, tz = oz - a.z;
+  float px = dy * e2z - dz * e2y, py = dz * e2x - dx * e2z, pz = dx * e2y - dy * e2x;
+  float det = e1x * px + e1y * py + e1z * pz;
+  float nE1 = fabsf(e1x) + fabsf(e1y) + fabsf(e1z);
+  float nE2 = fabsf(e2x) + fabsf(e2y) + fabsf(e2z);
+  float nT = fabsf(tx) + fabsf(ty) + fabsf(tz);
+  float eDet = k * nE1 * nD * nE2;
+  float A = fabsf(det);
+  if (A <= eDet) return 2;
+  float s = det > 0.f ? 1.f : -1.f;
+  float U = s * (tx * px + ty * py + tz * pz);
+  float eU = k * nT * nD * nE2;
+  if (U < -eU) return 0;
+  float qx = ty * e1z - tz * e1y, qy = tz * e1x - tx * e1z, qz = tx * e1y - ty * e1x;
+  float V = s * (dx * qx + dy * qy + dz * qz);
+  float eV = k * nD * nT * nE1;
+  if (V < -eV) return 0;
+  float Wm = A - U - V, eWm = eDet + eU + eV;
+  if (Wm < -eWm) return 0;
+  float W = s * (e2x * qx + e2y * qy + e2z * qz);
+  float eW = k * nE2 * nT * nE1;
+  float m0 = W - t_lo * A, e0 = eW + t_lo * eDet;
+  float m1 = t_hi * A - W, e1 = eW + eDet;
+  if (m0 < -e0 || m1 < -e1) return 0;
+  if (U > eU && V > eV && Wm > eWm && m0 > e0 && m1 > e1) return 1;
+  return 2;
+}
+
 // fp64 ray/triangle for the closest-hit free-space test (t > 0, no upper bound).
 // Returns t (or a negative value for no hit) and the facing sign of the normal.
 __device__ __forceinline__ double ray_tri_t(D3 O, D3 D, double dd, float4 a, float4 b, float4 c,

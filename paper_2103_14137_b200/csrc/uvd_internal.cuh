@@ -62,6 +62,16 @@ struct __align__(16) Node {
   uint4 d;   // child0 ref, child1 ref, (unused), (unused)
 };
 
+// BVH4 node (128 B = one L2 line), child-major: child k occupies c[2k] =
+// (lo.x, lo.y, lo.z, ref bits) and c[2k+1] = (hi.x, hi.y, hi.z, 0), so lane
+// (·, k) of a warp loads exactly its child's 32 B.  An unused slot has
+// ref = kEmptyRef and a point box at +1e30 that no segment with t in [0,1]
+// can reach.
+constexpr uint32_t kEmptyRef = 0xffffffffu;
+struct __align__(16) Node4 {
+  float4 c[8];
+};
+
 // ------------------------------------------------------------------ memory --
 struct Alloc {
   uvd_allocator user{};
@@ -96,8 +106,10 @@ struct uvd_scene {
   int64_t* orig_id = nullptr; // N
   // BVH (device)
   float4* tri = nullptr;      // M*3: (v0, owner patch), (v1, orig tri), (v2, 0)  leaf order
-  uvd::Node* nodes = nullptr; // max(M-1, 1)
+  uvd::Node* nodes = nullptr; // max(M-1, 1)   BVH2 (vantage queries)
   uint32_t root = 0;          // root ref
+  uvd::Node4* nodes4 = nullptr;  // BVH4 collapsed from the BVH2 (assembly)
+  int64_t n_nodes4 = 0;
   // 2.5D description (device + host copies) for the floorplan vantage test
   uvd::Wall* walls = nullptr;  // device
   int64_t n_walls = 0;

@@ -15,7 +15,7 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libuvd.so")
+LIB_PATH = os.environ.get("UVD_LIB", os.path.join(_HERE, "libuvd.so"))  # UVD_LIB: dev builds
 
 UVD_OK, UVD_ERR_INVALID, UVD_ERR_DOMAIN, UVD_ERR_EMPTY, UVD_ERR_CAPACITY, UVD_ERR_NOMEM, UVD_ERR_CUDA = (
     0, -1, -2, -3, -4, -5, -6)
@@ -47,7 +47,7 @@ class _SceneDesc(C.Structure):
     _fields_ = [("kind", C.c_int32), ("vertices", C.POINTER(C.c_float)), ("n_vertices", C.c_int64),
                 ("tris", C.POINTER(C.c_int32)), ("n_tris", C.c_int64), ("bounds", C.c_float * 4),
                 ("wall_height", C.c_float), ("obstacles", C.POINTER(_Polygon)),
-                ("n_obstacles", C.c_int32), ("patch_res", C.c_float)]
+                ("n_obstacles", C.c_int32), ("patch_res", C.c_float), ("device_input", C.c_int32)]
 
 
 class _VantageOpts(C.Structure):
@@ -64,7 +64,7 @@ class _Lamp(C.Structure):
 class _MatrixOut(C.Structure):
     _fields_ = [("format", C.c_int32), ("ld", C.c_int64), ("values", C.c_void_p),
                 ("colptr", C.c_void_p), ("rowidx", C.c_void_p), ("nnz_cap", C.c_int64),
-                ("vis_bits", C.c_void_p), ("col_sumsq", C.c_void_p), ("ray_count", C.c_void_p)]
+                ("vis_bits", C.c_void_p), ("col_sumsq", C.c_void_p), ("counters", C.c_void_p)]
 
 
 _lib = None
@@ -96,13 +96,14 @@ def lib():
                                    C.POINTER(C.c_double), C.c_void_p]
         L.uvd_last_error.restype = C.c_char_p
         L.uvd_version.restype = C.c_int
+        L.uvd_launch_count.restype = C.c_ulonglong
         _lib = L
     return _lib
 
 
 EXPORTS = ("uvd_scene_create", "uvd_scene_query", "uvd_scene_patches", "uvd_scene_destroy",
            "uvd_vantage_sample", "uvd_irradiance_matrix", "uvd_sync_status", "uvd_fluence",
-           "uvd_coverage", "uvd_last_error", "uvd_version")
+           "uvd_coverage", "uvd_last_error", "uvd_version", "uvd_launch_count")
 
 
 def _check(rc):
@@ -145,8 +146,9 @@ def _require_cuda():
 # ------------------------------------------------------------------- scene --
 class Scene:
     """uvd_scene_create from a synth-style dict: TRIMESH {vertices, tris} or
-    EXTRUDED {bounds, wall_height, obstacles, patch_res}.  Host inputs are read
-    during the call (their host->device copy is part of the call)."""
+    EXTRUDED {bounds, wall_height, obstacles, patch_res}.  TRIMESH vertices /
+    tris may be numpy arrays (host; the host->device copy is part of the call)
+    or CUDA tensors (float32 (nv,3) / int32 (nt,3), already resident)."""
 
     def __init__(self, desc: dict, device: int | None = None, stream=None, torch_allocator: bool = True):
         _require_cuda()
@@ -154,14 +156,22 @@ class Scene:
         d = _SceneDesc()
         keep = []
         if "vertices" in desc:
-            V = np.ascontiguousarray(desc["vertices"], np.float32)
-            F = np.ascontiguousarray(desc["tris"], np.int32)
-            keep += [V, F]
+            V, F = desc["vertices"], desc["tris"]
             d.kind = TRIMESH
-            d.vertices = V.ctypes.data_as(C.POINTER(C.c_float))
-            d.n_vertices = len(V)
-            d.tris = F.ctypes.data_as(C.POINTER(C.c_int32))
-            d.n_tris = len(F)
+            if isinstance(V, torch.Tensor) and V.is_cuda:
+                assert V.dtype == torch.float32 and F.dtype == torch.int32 and F.is_cuda
+                V, F = V.contiguous(), F.contiguous()
+                d.device_input = 1
+                d.vertices = C.cast(C.c_void_p(V.data_ptr()), C.POINTER(C.c_float))
+                d.tris = C.cast(C.c_void_p(F.data_ptr()), C.POINTER(C.c_int32))
+            else:
+                V = np.ascontiguousarray(V, np.float32)
+                F = np.ascontiguousarray(F, np.int32)
+                d.vertices = V.ctypes.data_as(C.POINTER(C.c_float))
+                d.tris = F.ctypes.data_as(C.POINTER(C.c_int32))
+            keep += [V, F]
+            d.n_vertices = V.shape[0]
+            d.n_tris = F.shape[0]
         else:
             d.kind = EXTRUDED
             for k in range(4):
@@ -242,12 +252,13 @@ class Scene:
         return lamps, raw
 
     def irradiance(self, lamps: torch.Tensor, cols=None, power_w: float = 80.0, vis_bits: bool = False,
-                   col_sumsq: bool = False, ray_count: bool = False, out: torch.Tensor | None = None,
+                   col_sumsq: bool = False, counters: bool = False, out: torch.Tensor | None = None,
                    stream=None) -> dict:
         """uvd_irradiance_matrix (dense column-major).  lamps: (K_total, L, 3)
         fp32 on the device; cols: None or a host sequence of global column ids.
         Returns dict(A=(n_cols, ld) fp32, [vis_bits (n_cols, L, words) int32],
-        [col_sumsq (n_cols,) fp64], [ray_count (1,) int64])."""
+        [col_sumsq (n_cols,) fp64], [counters (4,) int64: rays, box tests,
+        triangle tests, warp node fetches — instrumented kernel])."""
         assert lamps.is_cuda and lamps.dtype == torch.float32 and lamps.is_contiguous()
         K, L = lamps.shape[0], lamps.shape[1]
         ccols = None
@@ -273,10 +284,10 @@ class Scene:
             cs = torch.empty(n_cols, dtype=torch.float64, device=dev)
             m.col_sumsq = cs.data_ptr()
             res["col_sumsq"] = cs
-        if ray_count:
-            rc_t = torch.zeros(1, dtype=torch.int64, device=dev)
-            m.ray_count = rc_t.data_ptr()
-            res["ray_count"] = rc_t
+        if counters:
+            ct = torch.zeros(4, dtype=torch.int64, device=dev)
+            m.counters = ct.data_ptr()
+            res["counters"] = ct
         lamp = _Lamp(float(power_w), int(L))
         _check(lib().uvd_irradiance_matrix(
             self.handle, _ptr(lamps), K,
@@ -318,3 +329,8 @@ def fluence(A: torch.Tensor, n: int, x: torch.Tensor, transpose: bool = False,
 
 def version() -> int:
     return int(lib().uvd_version())
+
+
+def launch_count() -> int:
+    """Kernels libuvd has launched in this process (uvd_launch_count)."""
+    return int(lib().uvd_launch_count())

@@ -30,8 +30,8 @@ DISC_OPTS = vopts(DISC2D, 0.25, 0.15, lamp_z=1.0)                      # C1/C2 (
 DISC_OPTS_COARSE = vopts(DISC2D, 0.5, 0.15, lamp_z=1.0)                # C3
 FLOAT_OPTS = vopts(FLOAT3D, 0.25, 0.05)                                # C4 Floatbot
 TOWER_OPTS = vopts(TOWER, 0.25, 0.325, lamp_z0=0.37, lamp_z1=1.57, lamp_samples=10)  # C4 Towerbot (Q11)
-ARM_OPTS = vopts(ARM, 0.25, 0.05, zmin=0.3, zmax=1.9, reach=0.85,
-                 base_clearance=0.325, base_z=0.4)                     # C5 Armbot (Q12)
+ARM_OPTS = vopts(ARM, 0.2, 0.05, zmin=0.3, zmax=1.9, reach=0.85,
+                 base_clearance=0.325, base_z=0.4)   # C5 Armbot (Q12); ρ=0.2 m so K ≥ 10⁴
 
 
 def c1():

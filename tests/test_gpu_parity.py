@@ -46,7 +46,7 @@ def gpu_full(U, scene_desc, lamps_np=None, vopts=None, cols=None):
         lamps, raw = sc.vantage(vopts)
     else:
         lamps = torch.from_numpy(np.ascontiguousarray(lamps_np, np.float32)).cuda()
-    r = sc.irradiance(lamps, cols=cols, vis_bits=True, ray_count=True)
+    r = sc.irradiance(lamps, cols=cols, vis_bits=True, counters=True)
     sc.sync_status()
     p = sc.patches()
     return sc, lamps, r, p
@@ -175,7 +175,9 @@ def test_c1_full_matrix(uvd):
     A = check_full(sc, r, p, ref2, lam)
     check_full(sc, r, p, ref3, lam)
     assert (A > 0).all()                       # convex room: every pair lit
-    assert int(r["ray_count"].item()) == sc.N * lam.shape[0]
+    cnt = r["counters"].cpu().numpy()
+    assert cnt[0] == sc.N * lam.shape[0]      # every ray front-facing
+    assert cnt[1] > 0 and cnt[3] > 0
 
 
 @pytest.mark.parametrize("seed", list(range(25)))
@@ -292,6 +294,36 @@ def test_domain_error(uvd):
         sc.sync_status()
     assert e.value.code == uvd.UVD_ERR_DOMAIN
     sc.sync_status()  # flag cleared
+
+
+def test_device_input_scene_matches_host_input(uvd):
+    w = ward.ward(seed=3, n_bays=1, e=0.2)
+    a = uvd.Scene(w)
+    b = uvd.Scene(dict(vertices=torch.from_numpy(w["vertices"]).cuda(),
+                       tris=torch.from_numpy(w["tris"]).cuda()))
+    pa, pb = a.patches(), b.patches()
+    for k in pa:
+        assert torch.equal(pa[k], pb[k])
+    assert np.array_equal(a.bbox, b.bbox)
+    lamps, _ = a.vantage(configs.FLOAT_OPTS)
+    assert torch.equal(a.irradiance(lamps)["A"], b.irradiance(lamps)["A"])
+    bad = torch.from_numpy(w["vertices"]).cuda()
+    bad[7, 1] = float("nan")
+    with pytest.raises(uvd.UvdError):
+        uvd.Scene(dict(vertices=bad, tris=torch.from_numpy(w["tris"]).cuda()))
+
+
+def test_counters_and_launch_count(uvd):
+    c = configs.c2(1)
+    sc = uvd.Scene(c["scene"])
+    lamps, _ = sc.vantage(c["vantage"])
+    n0 = uvd.launch_count()
+    plain = sc.irradiance(lamps)
+    assert uvd.launch_count() == n0 + 1
+    inst = sc.irradiance(lamps, counters=True)
+    assert torch.equal(plain["A"], inst["A"])
+    cnt = inst["counters"].cpu().numpy()
+    assert 0 < cnt[0] <= sc.N * lamps.shape[0] and cnt[2] > 0
 
 
 def test_tiny_scenes(uvd):
