@@ -181,10 +181,11 @@ enum { UVD_DENSE_COLMAJOR = 0, UVD_CSC = 1 };
  *  vis_bits  (optional): [n_cols][L][ceil(N/32)] uint32, bit (i%32) of word i/32 =
  *            patch i front-facing and unoccluded from lamp sample l.
  *  col_sumsq (optional): [n_cols] fp64 Σ_i A[i,c]² (for ‖A‖_F).
- *  counters  (optional): 4 uint64 accumulated by the call (instrumented,
+ *  counters  (optional): 6 uint64 accumulated by the call (instrumented,
  *            slower path, for the roofline accounting): [0] front-facing rays
  *            that entered traversal, [1] per-ray child-box tests, [2] per-ray
- *            triangle tests, [3] warp node fetches. */
+ *            triangle tests, [3] node fetches, [4] entries the fp32 pass left
+ *            undecided and re-traced with fp64 triangle tests, [5] reserved. */
 typedef struct {
   int32_t format;
   int64_t ld;

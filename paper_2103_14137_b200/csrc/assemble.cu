@@ -50,7 +50,8 @@ struct AsmParams {
   int64_t ld;
   uint32_t* __restrict__ vis_bits;  // [n_cols][L][words] or nullptr
   double* __restrict__ col_sumsq;
-  unsigned long long* __restrict__ counters;  // [4] or nullptr (instrumented kernel)
+  unsigned long long* __restrict__ counters;  // [6] or nullptr (instrumented kernel)
+  uint32_t* __restrict__ pending;  // [n_cols][words] entries left undecided in fp32
   int* __restrict__ err;
 };
 
@@ -246,7 +247,7 @@ template <bool COUNT>
 __global__ void __launch_bounds__(kAsmThreads, kAsmMinBlocks) k_assemble(AsmParams P) {
   __shared__ WarpSmem s_w[kAsmWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  unsigned long long cnt[4] = {0, 0, 0, 0};  // warp-uniform tallies (COUNT only)
+  unsigned long long cnt[6] = {0, 0, 0, 0, 0, 0};  // warp-uniform tallies (COUNT only)
   const int64_t total = P.n_cols * P.tiles;
   for (int64_t item = (int64_t)blockIdx.x * kAsmWarps + warp; item < total;
        item += (int64_t)gridDim.x * kAsmWarps) {
@@ -307,11 +308,6 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmMinBlocks) k_assemble(AsmPara
     }
     const float a = (float)(acc * P.scale);
     if (P.values) P.values[c * P.ld + r] = a;
-    if (P.col_sumsq) {
-      double q = (double)a * (double)a;
-      for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
-      if (lane == 0 && q != 0.0) atomicAdd(P.col_sumsq + c, q);
-    }
   }
   if (COUNT && lane == 0)
     for (int k = 0; k < 4; ++k)
@@ -327,20 +323,24 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmMinBlocks) k_assemble(AsmPara
 // patches, so the lanes fetch mostly the same nodes (L1 broadcast) and
 // diverge little.
 constexpr int kLaneStack = 64;
-constexpr int kLaneAmb = 16;  // deferred fp64 re-tests per lane before a flush
 constexpr uint32_t kDone = 0xffffffffu;
 
-enum { kWalkClear = 0, kWalkBlocked = 1, kWalkFlush = 2 };
+enum { kClear = 0, kBlocked = 1, kUndecided = 2 };
 
-// One lane's walk; returns kWalkClear (stack exhausted), kWalkBlocked (a
-// certain hit) or kWalkFlush (the ambiguous list is full; state kept in
-// ref/sp/stk so the walk resumes after the flush).
+// One lane's any-hit walk with fp32 decisions only.  Returns kBlocked on a
+// certain hit, kClear when every triangle the segment may meet was a certain
+// miss, kUndecided when no certain hit was found but the fp32 filter could not
+// decide some triangle (the caller flags the entry for exact re-tracing).
 template <bool COUNT>
-__device__ __forceinline__ int lane_walk(const AsmParams& P, uint32_t* stk, int& sp, uint32_t& ref,
-                                         uint32_t* amb, int& namb, float ox, float oy, float oz,
-                                         float dx, float dy, float dz, float ix, float iy, float iz,
-                                         float nD, float tlo, float thi, int owner,
-                                         unsigned long long* cnt) {
+__device__ __forceinline__ int lane_walk32(const AsmParams& P, float ox, float oy, float oz,
+                                           float dx, float dy, float dz, int owner,
+                                           unsigned long long* cnt) {
+  uint32_t stk[kLaneStack];
+  int sp = 0;
+  bool undecided = false;
+  const float ix = safe_inv(dx), iy = safe_inv(dy), iz = safe_inv(dz);
+  const float oix = ox * ix, oiy = oy * iy, oiz = oz * iz;
+  uint32_t ref = P.root;
   for (;;) {
     // ---- inner nodes until this lane holds a leaf (or is done) ----
     while (!ref_is_leaf(ref)) {
@@ -348,18 +348,23 @@ __device__ __forceinline__ int lane_walk(const AsmParams& P, uint32_t* stk, int&
       const float4 na = __ldg(&nd->a), nb = __ldg(&nd->b), nc = __ldg(&nd->c);
       const uint2 ch = __ldg(reinterpret_cast<const uint2*>(&nd->d));
       if (COUNT) { cnt[1] += 2; cnt[3] += 1; }
-      const float ax0 = (na.x - ox) * ix, ax1 = (na.y - ox) * ix;
-      const float ay0 = (na.z - oy) * iy, ay1 = (na.w - oy) * iy;
-      const float az0 = (nc.x - oz) * iz, az1 = (nc.y - oz) * iz;
-      const float bx0 = (nb.x - ox) * ix, bx1 = (nb.y - ox) * ix;
-      const float by0 = (nb.z - oy) * iy, by1 = (nb.w - oy) * iy;
-      const float bz0 = (nc.z - oz) * iz, bz1 = (nc.w - oz) * iz;
+      // t = b/d - o/d as one FFMA per plane: fma(b, 1/d, -fl(o/d)) is the exact
+      // slab parameter of the plane b shifted by at most eps|o| (<= 1.2e-6 m for
+      // |o| <= 20 m), which the build-time box padding (>= 1e-5 m + 4 eps x the
+      // scene's largest coordinate) absorbs; the final rounding is covered by
+      // the 2e-6 relative widening
+      const float ax0 = fmaf(na.x, ix, -oix), ax1 = fmaf(na.y, ix, -oix);
+      const float ay0 = fmaf(na.z, iy, -oiy), ay1 = fmaf(na.w, iy, -oiy);
+      const float az0 = fmaf(nc.x, iz, -oiz), az1 = fmaf(nc.y, iz, -oiz);
+      const float bx0 = fmaf(nb.x, ix, -oix), bx1 = fmaf(nb.y, ix, -oix);
+      const float by0 = fmaf(nb.z, iy, -oiy), by1 = fmaf(nb.w, iy, -oiy);
+      const float bz0 = fmaf(nc.z, iz, -oiz), bz1 = fmaf(nc.w, iz, -oiz);
       const float an = fmaxf(fmaxf(fminf(ax0, ax1), fminf(ay0, ay1)), fmaxf(fminf(az0, az1), 0.0f));
       const float af = fminf(fminf(fmaxf(ax0, ax1), fmaxf(ay0, ay1)), fminf(fmaxf(az0, az1), 1.0f));
       const float bn = fmaxf(fmaxf(fminf(bx0, bx1), fminf(by0, by1)), fmaxf(fminf(bz0, bz1), 0.0f));
       const float bf = fminf(fminf(fmaxf(bx0, bx1), fmaxf(by0, by1)), fminf(fmaxf(bz0, bz1), 1.0f));
-      const bool h0 = an <= af * 1.000002f + 1e-7f;
-      const bool h1 = bn <= bf * 1.000002f + 1e-7f;
+      const bool h0 = an <= fmaf(af, 1.000002f, 1e-7f);
+      const bool h1 = bn <= fmaf(bf, 1.000002f, 1e-7f);
       if (h0 && h1) {
         const bool swap = bn < an;  // near child first
         ref = swap ? ch.y : ch.x;
@@ -371,8 +376,11 @@ __device__ __forceinline__ int lane_walk(const AsmParams& P, uint32_t* stk, int&
         ref = sp ? stk[--sp] : kDone;
       }
     }
-    if (ref == kDone) return kWalkClear;
+    if (ref == kDone) return undecided ? kUndecided : kClear;
     // ---- leaf: up to 4 triangles ----
+    const float nD = fabsf(dx) + fabsf(dy) + fabsf(dz);
+    const float tlo = (float)kSelfEps * rsqrtf(dx * dx + dy * dy + dz * dz);
+    const float thi = 1.0f - tlo;
     const uint32_t st = ref_start(ref), nt = ref_count(ref);
     for (uint32_t k = 0; k < nt; ++k) {
       const float4* t = P.tri + 3 * (int64_t)(st + k);
@@ -381,56 +389,27 @@ __device__ __forceinline__ int lane_walk(const AsmParams& P, uint32_t* stk, int&
       const float4 b = __ldg(t + 1), c = __ldg(t + 2);
       if (COUNT) cnt[2] += 1;
       const int cls = seg_tri_filter32(ox, oy, oz, dx, dy, dz, nD, tlo, thi, a, b, c);
-      if (cls == 1) return kWalkBlocked;
-      if (cls == 2) amb[namb++] = st + k;  // exact re-test deferred (outside the walk)
+      if (cls == 1) return kBlocked;
+      undecided |= cls == 2;
     }
     ref = sp ? stk[--sp] : kDone;
-    if (namb > kLaneAmb - 4) return kWalkFlush;  // room for one more leaf
-    if (ref == kDone) return kWalkClear;
-  }
-}
-
-// Is the open segment p -> c (t in (t_lo, t_hi)) clear of every scene triangle
-// except patch `owner`'s own?
-template <bool COUNT>
-__device__ __forceinline__ bool lane_trace_clear(const AsmParams& P, float ox, float oy, float oz,
-                                                 float dx, float dy, float dz, float tlo, float thi,
-                                                 int owner, unsigned long long* cnt) {
-  uint32_t stk[kLaneStack];
-  uint32_t amb[kLaneAmb];
-  int sp = 0, namb = 0;
-  uint32_t ref = P.root;
-  const float ix = safe_inv(dx), iy = safe_inv(dy), iz = safe_inv(dz);
-  const float nD = fabsf(dx) + fabsf(dy) + fabsf(dz);
-  for (;;) {
-    const int st = lane_walk<COUNT>(P, stk, sp, ref, amb, namb, ox, oy, oz, dx, dy, dz, ix, iy, iz, nD,
-                                    tlo, thi, owner, cnt);
-    if (st == kWalkBlocked) return false;
-    // exact fp64 re-tests of the triangles the fp32 filter could not decide
-    if (namb) {
-      const float cx = P.centroid[3 * owner], cy = P.centroid[3 * owner + 1], cz = P.centroid[3 * owner + 2];
-      for (int e = 0; e < namb; ++e) {
-        const float4* t = P.tri + 3 * (int64_t)amb[e];
-        if (exact_retest(ox, oy, oz, cx, cy, cz, __ldg(t), __ldg(t + 1), __ldg(t + 2))) return false;
-      }
-      namb = 0;
-    }
-    if (st == kWalkClear) return true;
+    if (ref == kDone) return undecided ? kUndecided : kClear;
   }
 }
 
 template <bool COUNT>
 __global__ void __launch_bounds__(kAsmThreads, kAsmMinBlocks) k_assemble_lane(AsmParams P) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  unsigned long long cnt[4] = {0, 0, 0, 0};  // per-lane tallies (COUNT only)
+  unsigned long long cnt[6] = {0, 0, 0, 0, 0, 0};  // per-lane tallies (COUNT only)
   const int64_t total = P.n_cols * P.tiles;
   for (int64_t item = (int64_t)blockIdx.x * kAsmWarps + warp; item < total;
        item += (int64_t)gridDim.x * kAsmWarps) {
     const int64_t c = item / P.tiles, tile = item - c * P.tiles;
     const int64_t j = P.cols ? P.cols[c] : c;
-    const int64_t r = tile * 32 + lane;
+    const int r = (int)(tile * 32 + lane);
     const bool valid = r < P.N;
     double acc = 0.0;
+    bool pend = false;
     for (int l = 0; l < P.L; ++l) {
       const float* pl = P.lamps + 3 * (j * P.L + l);
       const float ox = pl[0], oy = pl[1], oz = pl[2];
@@ -450,30 +429,123 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmMinBlocks) k_assemble_lane(As
         }
         if (front) {
           if (COUNT) cnt[0] += 1;
-          // a5: occlusion of the open segment, t in (1e-4/d, 1 - 1e-4/d)
-          const double t_lo = kSelfEps / d;
-          vis = lane_trace_clear<COUNT>(P, ox, oy, oz, (float)D.x, (float)D.y, (float)D.z,
-                                        (float)t_lo, (float)(1.0 - t_lo), (int)r, cnt);
+          // a5: occlusion of the open segment, t in (1e-4/d, 1 - 1e-4/d), fp32 decisions
+          const int res = lane_walk32<COUNT>(P, ox, oy, oz, cx - ox, cy - oy, cz - oz, r, cnt);
+          vis = res == kClear;
+          pend |= res == kUndecided;
           if (vis) acc += cosd / (dd * d);  // a6: Eq. 7 in fp64
         }
       }
       const uint32_t vm = __ballot_sync(0xffffffffu, vis);
       if (P.vis_bits && lane == 0 && tile < P.words) P.vis_bits[(c * P.L + l) * P.words + tile] = vm;
     }
+    // entries with an undecided ray are re-traced exactly by k_fixup
+    const uint32_t pm = __ballot_sync(0xffffffffu, pend);
+    if (lane == 0 && tile < P.words) P.pending[c * P.words + tile] = pm;
+    if (COUNT) cnt[4] += pend;
     const float a = (float)(acc * P.scale);
     if (P.values) P.values[c * P.ld + r] = a;
-    if (P.col_sumsq) {
-      double q = (double)a * (double)a;
-      for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
-      if (lane == 0 && q != 0.0) atomicAdd(P.col_sumsq + c, q);
-    }
   }
   if (COUNT)
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < 6; ++k) {
       unsigned long long v = cnt[k];
       for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
       if (lane == 0 && v) atomicAdd(P.counters + k, v);
     }
+}
+
+// Exact (fp64 triangle tests) any-hit walk for one ray, used by k_fixup.
+__device__ bool lane_clear_exact(const AsmParams& P, float ox, float oy, float oz, float cx, float cy,
+                                 float cz, int owner) {
+  uint32_t stk[kLaneStack];
+  int sp = 0;
+  const D3 O = d3(ox, oy, oz);
+  const D3 D = d3((double)cx - O.x, (double)cy - O.y, (double)cz - O.z);
+  const double dd = ddot3(D, D);
+  const double t_lo = kSelfEps / sqrt(dd);
+  const Ray32 r32 = make_ray32(ox, oy, oz, (float)D.x, (float)D.y, (float)D.z);
+  uint32_t ref = P.root;
+  for (;;) {
+    if (ref_is_leaf(ref)) {
+      const uint32_t st = ref_start(ref), nt = ref_count(ref);
+      for (uint32_t k = 0; k < nt; ++k) {
+        const float4* t = P.tri + 3 * (int64_t)(st + k);
+        if (__float_as_int(t[0].w) == owner) continue;
+        if (seg_hits_tri(O, D, dd, t_lo, 1.0 - t_lo, t[0], t[1], t[2])) return false;
+      }
+      if (!sp) return true;
+      ref = stk[--sp];
+    } else {
+      const Node nd = P.nodes[ref];
+      const bool h0 = slab(r32, nd.a.x, nd.a.y, nd.a.z, nd.a.w, nd.c.x, nd.c.y, 1.0f);
+      const bool h1 = slab(r32, nd.b.x, nd.b.y, nd.b.z, nd.b.w, nd.c.z, nd.c.w, 1.0f);
+      if (h0 && h1) {
+        ref = nd.d.x;
+        if (sp < kLaneStack) stk[sp++] = nd.d.y;
+        else atomicExch(P.err, 2);
+      } else if (h0 || h1) {
+        ref = h0 ? nd.d.x : nd.d.y;
+      } else {
+        if (!sp) return true;
+        ref = stk[--sp];
+      }
+    }
+  }
+}
+
+// Re-trace, with exact fp64 triangle tests, every entry flagged by
+// k_assemble_lane and rewrite its value and visibility bits.
+__global__ void k_fixup(AsmParams P) {
+  const int64_t nwords = P.n_cols * P.words;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nwords;
+       w += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t bits = P.pending[w];
+    if (!bits) continue;
+    const int64_t c = w / P.words, word = w - c * P.words;
+    const int64_t j = P.cols ? P.cols[c] : c;
+    while (bits) {
+      const int b = __ffs(bits) - 1;
+      bits &= bits - 1;
+      const int r = (int)(word * 32 + b);
+      const float cx = P.centroid[3 * r], cy = P.centroid[3 * r + 1], cz = P.centroid[3 * r + 2];
+      const float nx = P.normal[3 * r], ny = P.normal[3 * r + 1], nz = P.normal[3 * r + 2];
+      double acc = 0.0;
+      for (int l = 0; l < P.L; ++l) {
+        const float* pl = P.lamps + 3 * (j * P.L + l);
+        const float ox = pl[0], oy = pl[1], oz = pl[2];
+        const D3 D = d3((double)cx - (double)ox, (double)cy - (double)oy, (double)cz - (double)oz);
+        const double dd = ddot3(D, D);
+        const double d = sqrt(dd);
+        const double cosd = -(D.x * (double)nx + D.y * (double)ny + D.z * (double)nz);
+        const bool vis = cosd > 0.0 && d >= kMinDist && lane_clear_exact(P, ox, oy, oz, cx, cy, cz, r);
+        if (vis) acc += cosd / (dd * d);
+        if (P.vis_bits) {
+          uint32_t* vw = P.vis_bits + (c * P.L + l) * P.words + word;
+          if (vis) atomicOr(vw, 1u << b);
+          else atomicAnd(vw, ~(1u << b));
+        }
+      }
+      if (P.values) P.values[c * P.ld + r] = (float)(acc * P.scale);
+    }
+  }
+}
+
+// ‖A‖_F by-product: per-column Σ A² (fp64, fixed order within a column tile)
+__global__ void k_col_sumsq(const AsmParams P, double* __restrict__ out) {
+  const int64_t c = blockIdx.x;
+  double s = 0.0;
+  for (int64_t r = threadIdx.x; r < P.N; r += blockDim.x) {
+    const double a = P.values[c * P.ld + r];
+    s += a * a;
+  }
+  __shared__ double red[256];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[c] = red[0];
 }
 
 template <bool COUNT>
@@ -549,7 +621,8 @@ extern "C" int uvd_irradiance_matrix(const uvd_scene* s, const float* lamp_xyz, 
   P.col_sumsq = out->col_sumsq;
   P.counters = out->counters;
   P.err = s->err_flag;
-  if (P.col_sumsq) UVD_CUDA_TRY(cudaMemsetAsync(P.col_sumsq, 0, n_cols * sizeof(double), st));
+  P.pending = (uint32_t*)al.get((size_t)n_cols * P.words * sizeof(uint32_t));
+  if (!P.pending) { set_error("uvd_irradiance_matrix: out of device memory"); return UVD_ERR_NOMEM; }
   // algorithm: 0 = per-lane while-while over the BVH2 (default), 1 = warp
   // pair-parallel packets over the BVH4 (UVD_ASM_ALGO=1, kept for comparison)
   static int algo = -1;
@@ -557,6 +630,8 @@ extern "C" int uvd_irradiance_matrix(const uvd_scene* s, const float* lamp_xyz, 
     const char* e = getenv("UVD_ASM_ALGO");
     algo = e ? atoi(e) : 0;
   }
+  if (algo == 1)  // the packet kernel resolves undecided tests inline
+    UVD_CUDA_TRY(cudaMemsetAsync(P.pending, 0, (size_t)n_cols * P.words * sizeof(uint32_t), st));
   static int grid_c = 0, grid = 0;
   if (P.counters) {
     if (!grid_c) grid_c = grid_size_assemble<true>(algo);
@@ -568,6 +643,20 @@ extern "C" int uvd_irradiance_matrix(const uvd_scene* s, const float* lamp_xyz, 
     else k_assemble_lane<false><<<grid, kAsmThreads, 0, st>>>(P);
   }
   note_launch();
+  {  // exact fp64 re-trace of the (rare) entries the fp32 pass left undecided
+    int dev = 0, sms = 148;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    const int64_t nwords = n_cols * P.words;
+    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nwords + 255) / 256, 4 * sms));
+    k_fixup<<<g, 256, 0, st>>>(P);
+    note_launch();
+  }
+  if (P.col_sumsq) {
+    k_col_sumsq<<<(unsigned)n_cols, 256, 0, st>>>(P, P.col_sumsq);
+    note_launch();
+  }
+  al.put(P.pending);
   UVD_CUDA_TRY(cudaGetLastError());
   if (dcols) al.put(dcols);
   return UVD_OK;

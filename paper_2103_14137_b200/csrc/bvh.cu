@@ -13,6 +13,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 
 #include "uvd_internal.cuh"
 
@@ -259,8 +260,12 @@ __global__ void k_refit(const float4* __restrict__ tri, int64_t n, const int32_t
   }
 }
 
-__device__ __forceinline__ float pad_lo(float x) { return x - (1e-5f + 1e-6f * fabsf(x)); }
-__device__ __forceinline__ float pad_hi(float x) { return x + (1e-5f + 1e-6f * fabsf(x)); }
+// Outward box padding: 1e-5 m + 1e-6 |x| + c_pad, where c_pad = 4 eps32 x the
+// scene's largest |coordinate| (set per build) covers the rounding of the
+// traversal's fp32 ray (its direction is fl32 of the exact one) and of the
+// FFMA-form slab parameters (plane shift <= eps |origin|).
+__device__ __forceinline__ float pad_lo(float x, float cp) { return x - (1e-5f + 1e-6f * fabsf(x) + cp); }
+__device__ __forceinline__ float pad_hi(float x, float cp) { return x + (1e-5f + 1e-6f * fabsf(x) + cp); }
 
 __device__ __forceinline__ void child_info(const float4* __restrict__ tri, const float* __restrict__ ibox,
                                            const int32_t* __restrict__ rfirst,
@@ -281,7 +286,7 @@ __device__ __forceinline__ void child_info(const float4* __restrict__ tri, const
 __global__ void k_emit(const float4* __restrict__ tri, int64_t n, const int32_t* __restrict__ left,
                        const int32_t* __restrict__ right, const int32_t* __restrict__ rfirst,
                        const int32_t* __restrict__ rlast, const float* __restrict__ ibox,
-                       Node* __restrict__ nodes) {
+                       Node* __restrict__ nodes, float cp) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n - 1) return;
   Box b0, b1;
@@ -289,22 +294,22 @@ __global__ void k_emit(const float4* __restrict__ tri, int64_t n, const int32_t*
   child_info(tri, ibox, rfirst, rlast, left[i], &b0, &r0);
   child_info(tri, ibox, rfirst, rlast, right[i], &b1, &r1);
   Node nd;
-  nd.a = make_float4(pad_lo(b0.lx), pad_hi(b0.hx), pad_lo(b0.ly), pad_hi(b0.hy));
-  nd.b = make_float4(pad_lo(b1.lx), pad_hi(b1.hx), pad_lo(b1.ly), pad_hi(b1.hy));
-  nd.c = make_float4(pad_lo(b0.lz), pad_hi(b0.hz), pad_lo(b1.lz), pad_hi(b1.hz));
+  nd.a = make_float4(pad_lo(b0.lx, cp), pad_hi(b0.hx, cp), pad_lo(b0.ly, cp), pad_hi(b0.hy, cp));
+  nd.b = make_float4(pad_lo(b1.lx, cp), pad_hi(b1.hx, cp), pad_lo(b1.ly, cp), pad_hi(b1.hy, cp));
+  nd.c = make_float4(pad_lo(b0.lz, cp), pad_hi(b0.hz, cp), pad_lo(b1.lz, cp), pad_hi(b1.hz, cp));
   nd.d = make_uint4(r0, r1, 0u, 0u);
   nodes[i] = nd;
 }
 
 // single-leaf scene (M <= kLeafMax): a root node with one leaf child and an
 // empty second child
-__global__ void k_emit_small(const float4* __restrict__ tri, int64_t n, Node* nodes) {
+__global__ void k_emit_small(const float4* __restrict__ tri, int64_t n, Node* nodes, float cp) {
   Box b = tri_box(tri, 0);
   for (int64_t r = 1; r < n; ++r) b = join(b, tri_box(tri, r));
   Node nd;
-  nd.a = make_float4(pad_lo(b.lx), pad_hi(b.hx), pad_lo(b.ly), pad_hi(b.hy));
+  nd.a = make_float4(pad_lo(b.lx, cp), pad_hi(b.hx, cp), pad_lo(b.ly, cp), pad_hi(b.hy, cp));
   nd.b = make_float4(1.f, -1.f, 1.f, -1.f);  // empty box: never hit
-  nd.c = make_float4(pad_lo(b.lz), pad_hi(b.hz), 1.f, -1.f);
+  nd.c = make_float4(pad_lo(b.lz, cp), pad_hi(b.hz, cp), 1.f, -1.f);
   nd.d = make_uint4(make_leaf(0u, (uint32_t)n), make_leaf(0u, 1u), 0u, 0u);
   nodes[0] = nd;
 }
@@ -327,7 +332,7 @@ __global__ void k_collapse4(const float4* __restrict__ tri, const int32_t* __res
                             const int32_t* __restrict__ rlast, const float* __restrict__ ibox,
                             const Frontier* __restrict__ cur, const int* __restrict__ cur_n,
                             Frontier* __restrict__ nxt, int* __restrict__ nxt_n,
-                            int* __restrict__ n4_count, Node4* __restrict__ nodes4) {
+                            int* __restrict__ n4_count, Node4* __restrict__ nodes4, float cp) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= *cur_n) return;
   Frontier f = cur[i];
@@ -364,9 +369,9 @@ __global__ void k_collapse4(const float4* __restrict__ tri, const int32_t* __res
       nxt[q] = Frontier{ch[k], m};
       ref[k] = (uint32_t)m;
     }
-    lo[0][k] = pad_lo(bx.lx); hi[0][k] = pad_hi(bx.hx);
-    lo[1][k] = pad_lo(bx.ly); hi[1][k] = pad_hi(bx.hy);
-    lo[2][k] = pad_lo(bx.lz); hi[2][k] = pad_hi(bx.hz);
+    lo[0][k] = pad_lo(bx.lx, cp); hi[0][k] = pad_hi(bx.hx, cp);
+    lo[1][k] = pad_lo(bx.ly, cp); hi[1][k] = pad_hi(bx.hy, cp);
+    lo[2][k] = pad_lo(bx.lz, cp); hi[2][k] = pad_hi(bx.hz, cp);
   }
   Node4 nd;
   for (int k = 0; k < 4; ++k) {
@@ -388,12 +393,12 @@ __global__ void k_collapse4_swap(int* cur_n, int* nxt_n) {
 }
 
 // single-leaf scene (M <= kLeafMax): root with one leaf child
-__global__ void k_emit4_small(const float4* __restrict__ tri, int64_t n, Node4* nodes4) {
+__global__ void k_emit4_small(const float4* __restrict__ tri, int64_t n, Node4* nodes4, float cp) {
   Box b = tri_box(tri, 0);
   for (int64_t r = 1; r < n; ++r) b = join(b, tri_box(tri, r));
   Node4 nd;
-  nd.c[0] = make_float4(pad_lo(b.lx), pad_lo(b.ly), pad_lo(b.lz), __uint_as_float(make_leaf(0u, (uint32_t)n)));
-  nd.c[1] = make_float4(pad_hi(b.hx), pad_hi(b.hy), pad_hi(b.hz), 0.f);
+  nd.c[0] = make_float4(pad_lo(b.lx, cp), pad_lo(b.ly, cp), pad_lo(b.lz, cp), __uint_as_float(make_leaf(0u, (uint32_t)n)));
+  nd.c[1] = make_float4(pad_hi(b.hx, cp), pad_hi(b.hy, cp), pad_hi(b.hz, cp), 0.f);
   for (int k = 1; k < 4; ++k) {
     nd.c[2 * k] = make_float4(1e30f, 1e30f, 1e30f, __uint_as_float(kEmptyRef));
     nd.c[2 * k + 1] = make_float4(1e30f, 1e30f, 1e30f, 0.f);
@@ -429,6 +434,9 @@ int build_bvh(uvd_scene* s, float4* tri_in, uint32_t** order_out, cudaStream_t s
     set_error("scene: out of device memory building the BVH (M=%lld)", (long long)M);
     return UVD_ERR_NOMEM;
   }
+  float cp = 0.f;  // padding term 4 eps32 x the scene's largest |coordinate|
+  for (int k = 0; k < 6; ++k) cp = std::max(cp, std::fabs(s->bbox[k]));
+  cp *= 4.0f * 5.9604645e-08f;
   float3 lo = make_float3(s->bbox[0], s->bbox[1], s->bbox[2]);
   float ex = s->bbox[3] - s->bbox[0], ey = s->bbox[4] - s->bbox[1], ez = s->bbox[5] - s->bbox[2];
   float3 inv = make_float3(ex > 0 ? 1.f / ex : 0.f, ey > 0 ? 1.f / ey : 0.f, ez > 0 ? 1.f / ez : 0.f);
@@ -438,9 +446,9 @@ int build_bvh(uvd_scene* s, float4* tri_in, uint32_t** order_out, cudaStream_t s
   k_gather_tri<<<grid_for(M, 256), 256, 0, st>>>(tri_in, vals, M, s->tri);
   note_launch();
   if (M <= kLeafMax) {
-    k_emit_small<<<1, 1, 0, st>>>(s->tri, M, s->nodes);
+    k_emit_small<<<1, 1, 0, st>>>(s->tri, M, s->nodes, cp);
     note_launch();
-    k_emit4_small<<<1, 1, 0, st>>>(s->tri, M, s->nodes4);
+    k_emit4_small<<<1, 1, 0, st>>>(s->tri, M, s->nodes4, cp);
     note_launch();
     s->root = 0;
     s->n_nodes4 = 1;
@@ -463,7 +471,7 @@ int build_bvh(uvd_scene* s, float4* tri_in, uint32_t** order_out, cudaStream_t s
     note_launch();
     k_refit<<<grid_for(M, 256), 256, 0, st>>>(s->tri, M, left, right, pint, pleaf, ibox, arrive);
     note_launch();
-    k_emit<<<grid_for(ni, 256), 256, 0, st>>>(s->tri, M, left, right, rf, rl, ibox, s->nodes);
+    k_emit<<<grid_for(ni, 256), 256, 0, st>>>(s->tri, M, left, right, rf, rl, ibox, s->nodes, cp);
     note_launch();
     s->root = 0;
     // BVH4: frontier capacity = number of BVH2 internal nodes (upper bound)
@@ -480,7 +488,7 @@ int build_bvh(uvd_scene* s, float4* tri_in, uint32_t** order_out, cudaStream_t s
       int64_t cap = std::min<int64_t>((int64_t)h_ctr[0], ni);
       for (int sub = 0; sub < 6; ++sub) {  // 6 levels per host round trip
         k_collapse4<<<grid_for(std::max<int64_t>(cap, 1), 128), 128, 0, st>>>(
-            s->tri, left, right, rf, rl, ibox, fa, ctr + 0, fb, ctr + 1, ctr + 2, s->nodes4);
+            s->tri, left, right, rf, rl, ibox, fa, ctr + 0, fb, ctr + 1, ctr + 2, s->nodes4, cp);
         note_launch();
         k_collapse4_swap<<<1, 1, 0, st>>>(ctr + 0, ctr + 1);
         note_launch();

@@ -257,8 +257,8 @@ class Scene:
         """uvd_irradiance_matrix (dense column-major).  lamps: (K_total, L, 3)
         fp32 on the device; cols: None or a host sequence of global column ids.
         Returns dict(A=(n_cols, ld) fp32, [vis_bits (n_cols, L, words) int32],
-        [col_sumsq (n_cols,) fp64], [counters (4,) int64: rays, box tests,
-        triangle tests, warp node fetches — instrumented kernel])."""
+        [col_sumsq (n_cols,) fp64], [counters (6,) int64: rays, box tests,
+        triangle tests, node fetches, entries re-traced in fp64, 0 — instrumented kernel])."""
         assert lamps.is_cuda and lamps.dtype == torch.float32 and lamps.is_contiguous()
         K, L = lamps.shape[0], lamps.shape[1]
         ccols = None
@@ -285,7 +285,7 @@ class Scene:
             m.col_sumsq = cs.data_ptr()
             res["col_sumsq"] = cs
         if counters:
-            ct = torch.zeros(4, dtype=torch.int64, device=dev)
+            ct = torch.zeros(6, dtype=torch.int64, device=dev)
             m.counters = ct.data_ptr()
             res["counters"] = ct
         lamp = _Lamp(float(power_w), int(L))
