@@ -340,6 +340,11 @@ __device__ __forceinline__ int lane_walk32(const AsmParams& P, float ox, float o
   bool undecided = false;
   const float ix = safe_inv(dx), iy = safe_inv(dy), iz = safe_inv(dz);
   const float oix = ox * ix, oiy = oy * iy, oiz = oz * iz;
+  // the segment's own extent t in (t_lo, t_hi) also bounds the box tests: boxes
+  // the segment only enters within 0.1 mm of the target (e.g. the target's own
+  // flat leaf and its flat ancestors) are never visited
+  const float tlo = (float)kSelfEps * rsqrtf(dx * dx + dy * dy + dz * dz);
+  const float thi = 1.0f - tlo;
   uint32_t ref = P.root;
   for (;;) {
     // ---- inner nodes until this lane holds a leaf (or is done) ----
@@ -360,9 +365,9 @@ __device__ __forceinline__ int lane_walk32(const AsmParams& P, float ox, float o
       const float by0 = fmaf(nb.z, iy, -oiy), by1 = fmaf(nb.w, iy, -oiy);
       const float bz0 = fmaf(nc.z, iz, -oiz), bz1 = fmaf(nc.w, iz, -oiz);
       const float an = fmaxf(fmaxf(fminf(ax0, ax1), fminf(ay0, ay1)), fmaxf(fminf(az0, az1), 0.0f));
-      const float af = fminf(fminf(fmaxf(ax0, ax1), fmaxf(ay0, ay1)), fminf(fmaxf(az0, az1), 1.0f));
+      const float af = fminf(fminf(fmaxf(ax0, ax1), fmaxf(ay0, ay1)), fminf(fmaxf(az0, az1), thi));
       const float bn = fmaxf(fmaxf(fminf(bx0, bx1), fminf(by0, by1)), fmaxf(fminf(bz0, bz1), 0.0f));
-      const float bf = fminf(fminf(fmaxf(bx0, bx1), fmaxf(by0, by1)), fminf(fmaxf(bz0, bz1), 1.0f));
+      const float bf = fminf(fminf(fmaxf(bx0, bx1), fmaxf(by0, by1)), fminf(fmaxf(bz0, bz1), thi));
       const bool h0 = an <= fmaf(af, 1.000002f, 1e-7f);
       const bool h1 = bn <= fmaf(bf, 1.000002f, 1e-7f);
       if (h0 && h1) {
@@ -379,8 +384,6 @@ __device__ __forceinline__ int lane_walk32(const AsmParams& P, float ox, float o
     if (ref == kDone) return undecided ? kUndecided : kClear;
     // ---- leaf: up to 4 triangles ----
     const float nD = fabsf(dx) + fabsf(dy) + fabsf(dz);
-    const float tlo = (float)kSelfEps * rsqrtf(dx * dx + dy * dy + dz * dz);
-    const float thi = 1.0f - tlo;
     const uint32_t st = ref_start(ref), nt = ref_count(ref);
     for (uint32_t k = 0; k < nt; ++k) {
       const float4* t = P.tri + 3 * (int64_t)(st + k);
@@ -445,6 +448,168 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmMinBlocks) k_assemble_lane(As
     if (COUNT) cnt[4] += pend;
     const float a = (float)(acc * P.scale);
     if (P.values) P.values[c * P.ld + r] = a;
+  }
+  if (COUNT)
+    for (int k = 0; k < 6; ++k) {
+      unsigned long long v = cnt[k];
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0 && v) atomicAdd(P.counters + k, v);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// Persistent per-lane traversal with dynamic ray refill (Aila & Laine 2009,
+// "replacing terminated rays").  A warp owns a chunk of kChunkRows consecutive
+// patches of one column; a lane whose ray ends (certain hit, stack exhausted)
+// or whose sample is back-facing immediately takes the next sample / the next
+// row of the chunk, so lanes do not idle while the slowest ray of a fixed tile
+// finishes.  Visibility and pending bits are OR-ed into the chunk's words,
+// which the warp clears first (chunks are word-aligned and owned by one warp).
+constexpr int kChunkRows = 256;
+
+template <bool COUNT>
+__global__ void __launch_bounds__(kAsmThreads, kAsmMinBlocks) k_assemble_dyn(AsmParams P) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const uint32_t lt = (1u << lane) - 1u;
+  unsigned long long cnt[6] = {0, 0, 0, 0, 0, 0};
+  const int ld = (int)P.ld, N = (int)P.N, words = (int)P.words;
+  const int64_t cpc = (P.ld + kChunkRows - 1) / kChunkRows;  // chunks per column
+  const int64_t total = P.n_cols * cpc;
+  uint32_t stk[kLaneStack];
+  for (int64_t item = (int64_t)blockIdx.x * kAsmWarps + warp; item < total;
+       item += (int64_t)gridDim.x * kAsmWarps) {
+    const int64_t c = item / cpc;
+    const int rb0 = (int)(item - c * cpc) * kChunkRows;
+    const int rb1 = min(rb0 + kChunkRows, ld);
+    const int64_t j = P.cols ? P.cols[c] : c;
+    const float* lamp = P.lamps + 3 * j * P.L;
+    {  // clear the chunk's bit words
+      const int w0 = rb0 >> 5, w1 = min((rb1 + 31) >> 5, words);
+      for (int w = w0 + lane; w < w1; w += 32) {
+        P.pending[c * words + w] = 0u;
+        if (P.vis_bits)
+          for (int l = 0; l < P.L; ++l) P.vis_bits[(c * P.L + l) * words + w] = 0u;
+      }
+      __syncwarp();
+    }
+    int cursor = rb0;
+    bool busy = false, has_row = false, pend = false, und = false;
+    int r = 0, l = 0, sp = 0;
+    double acc = 0.0;
+    float ox = 0.f, oy = 0.f, oz = 0.f, ix = 0.f, iy = 0.f, iz = 0.f, oix = 0.f, oiy = 0.f, oiz = 0.f;
+    float dx = 0.f, dy = 0.f, dz = 0.f;
+    uint32_t ref = kDone;
+    for (;;) {
+      // ---- idle lanes: claim rows / start the next front-facing sample ----
+      for (;;) {
+        const uint32_t want = __ballot_sync(0xffffffffu, !busy && !has_row);
+        if (want && cursor < rb1) {
+          const int row = cursor + __popc(want & lt);
+          if (!busy && !has_row && row < rb1) {
+            has_row = true; r = row; l = 0; acc = 0.0; pend = false;
+          }
+          cursor = min(cursor + __popc(want), rb1);
+        }
+        if (!busy && has_row) {
+          if (l < P.L && r < N) {
+            const float* pl = lamp + 3 * l;
+            ox = pl[0]; oy = pl[1]; oz = pl[2];
+            const float cx = P.centroid[3 * r], cy = P.centroid[3 * r + 1], cz = P.centroid[3 * r + 2];
+            const float nx = P.normal[3 * r], ny = P.normal[3 * r + 1], nz = P.normal[3 * r + 2];
+            // a4: front-face cull in fp64 (exact differences of fp32 inputs)
+            const double Dx = (double)cx - (double)ox, Dy = (double)cy - (double)oy, Dz = (double)cz - (double)oz;
+            const double dd = Dx * Dx + Dy * Dy + Dz * Dz;
+            const double cosd = -(Dx * (double)nx + Dy * (double)ny + Dz * (double)nz);
+            bool front = cosd > 0.0;
+            if (sqrt(dd) < kMinDist) { atomicExch(P.err, 1); front = false; }
+            if (front) {
+              if (COUNT) cnt[0] += 1;
+              dx = cx - ox; dy = cy - oy; dz = cz - oz;  // == fl32 of the exact difference
+              ix = safe_inv(dx); iy = safe_inv(dy); iz = safe_inv(dz);
+              oix = ox * ix; oiy = oy * iy; oiz = oz * iz;
+              ref = P.root; sp = 0; und = false;
+              busy = true;
+            } else {
+              ++l;  // back-facing sample: contributes 0, visibility bit stays 0
+            }
+          } else {  // row finished: store the entry (rows >= N are the zero padding)
+            if (P.values) P.values[c * P.ld + r] = (float)(acc * P.scale);
+            if (pend) atomicOr(P.pending + c * words + (r >> 5), 1u << (r & 31));
+            if (COUNT) cnt[4] += pend;
+            has_row = false;
+          }
+        }
+        if (!__ballot_sync(0xffffffffu, !busy && (has_row || cursor < rb1))) break;
+      }
+      if (!__any_sync(0xffffffffu, busy)) break;  // chunk done
+      if (!busy) continue;
+      // ---- a5: inner nodes until a leaf, then that leaf ----
+      int res = -1;
+      while (!ref_is_leaf(ref)) {
+        const Node* nd = P.nodes + ref;
+        const float4 na = __ldg(&nd->a), nb = __ldg(&nd->b), nc = __ldg(&nd->c);
+        const uint2 ch = __ldg(reinterpret_cast<const uint2*>(&nd->d));
+        if (COUNT) { cnt[1] += 2; cnt[3] += 1; }
+        const float ax0 = fmaf(na.x, ix, -oix), ax1 = fmaf(na.y, ix, -oix);
+        const float ay0 = fmaf(na.z, iy, -oiy), ay1 = fmaf(na.w, iy, -oiy);
+        const float az0 = fmaf(nc.x, iz, -oiz), az1 = fmaf(nc.y, iz, -oiz);
+        const float bx0 = fmaf(nb.x, ix, -oix), bx1 = fmaf(nb.y, ix, -oix);
+        const float by0 = fmaf(nb.z, iy, -oiy), by1 = fmaf(nb.w, iy, -oiy);
+        const float bz0 = fmaf(nc.z, iz, -oiz), bz1 = fmaf(nc.w, iz, -oiz);
+        const float an = fmaxf(fmaxf(fminf(ax0, ax1), fminf(ay0, ay1)), fmaxf(fminf(az0, az1), 0.0f));
+        const float af = fminf(fminf(fmaxf(ax0, ax1), fmaxf(ay0, ay1)), fminf(fmaxf(az0, az1), 1.0f));
+        const float bn = fmaxf(fmaxf(fminf(bx0, bx1), fminf(by0, by1)), fmaxf(fminf(bz0, bz1), 0.0f));
+        const float bf = fminf(fminf(fmaxf(bx0, bx1), fmaxf(by0, by1)), fminf(fmaxf(bz0, bz1), 1.0f));
+        const bool h0 = an <= fmaf(af, 1.000002f, 1e-7f);
+        const bool h1 = bn <= fmaf(bf, 1.000002f, 1e-7f);
+        if (h0 && h1) {
+          const bool swap = bn < an;  // near child first
+          ref = swap ? ch.y : ch.x;
+          if (sp < kLaneStack) stk[sp++] = swap ? ch.x : ch.y;
+          else atomicExch(P.err, 2);  // cannot happen for depth < 64; fail loudly
+        } else if (h0 || h1) {
+          ref = h0 ? ch.x : ch.y;
+        } else {
+          ref = sp ? stk[--sp] : kDone;
+        }
+      }
+      if (ref == kDone) {
+        res = und ? kUndecided : kClear;
+      } else {  // leaf: up to 4 triangles (fp32 filter)
+        const float nD = fabsf(dx) + fabsf(dy) + fabsf(dz);
+        const float tlo = (float)kSelfEps * rsqrtf(dx * dx + dy * dy + dz * dz);
+        const float thi = 1.0f - tlo;
+        const uint32_t st = ref_start(ref), nt = ref_count(ref);
+        for (uint32_t k = 0; k < nt && res < 0; ++k) {
+          const float4* t = P.tri + 3 * (int64_t)(st + k);
+          const float4 a = __ldg(t);
+          if (__float_as_int(a.w) == r) continue;  // the target's own triangles
+          const float4 b = __ldg(t + 1), cc = __ldg(t + 2);
+          if (COUNT) cnt[2] += 1;
+          const int cls = seg_tri_filter32(ox, oy, oz, dx, dy, dz, nD, tlo, thi, a, b, cc);
+          if (cls == 1) res = kBlocked;
+          und |= cls == 2;
+        }
+        if (res < 0) {
+          ref = sp ? stk[--sp] : kDone;
+          if (ref == kDone) res = und ? kUndecided : kClear;
+        }
+      }
+      if (res >= 0) {  // sample l decided
+        if (res == kClear) {  // a6: Eq. 7 in fp64
+          const float cx = P.centroid[3 * r], cy = P.centroid[3 * r + 1], cz = P.centroid[3 * r + 2];
+          const float nx = P.normal[3 * r], ny = P.normal[3 * r + 1], nz = P.normal[3 * r + 2];
+          const double Dx = (double)cx - (double)ox, Dy = (double)cy - (double)oy, Dz = (double)cz - (double)oz;
+          const double dd = Dx * Dx + Dy * Dy + Dz * Dz;
+          const double cosd = -(Dx * (double)nx + Dy * (double)ny + Dz * (double)nz);
+          acc += cosd / (dd * sqrt(dd));
+          if (P.vis_bits) atomicOr(P.vis_bits + (c * P.L + l) * words + (r >> 5), 1u << (r & 31));
+        }
+        pend |= res == kUndecided;
+        ++l;
+        busy = false;
+      }
+    }
   }
   if (COUNT)
     for (int k = 0; k < 6; ++k) {
@@ -554,7 +719,8 @@ static int grid_size_assemble(int algo) {
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
   if (algo == 1) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_assemble<COUNT>, kAsmThreads, 0);
-  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_assemble_lane<COUNT>, kAsmThreads, 0);
+  else if (algo == 2) cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_assemble_lane<COUNT>, kAsmThreads, 0);
+  else cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_assemble_dyn<COUNT>, kAsmThreads, 0);
   return std::max(1, sms * std::max(per, 1));
 }
 
@@ -623,12 +789,13 @@ extern "C" int uvd_irradiance_matrix(const uvd_scene* s, const float* lamp_xyz, 
   P.err = s->err_flag;
   P.pending = (uint32_t*)al.get((size_t)n_cols * P.words * sizeof(uint32_t));
   if (!P.pending) { set_error("uvd_irradiance_matrix: out of device memory"); return UVD_ERR_NOMEM; }
-  // algorithm: 0 = per-lane while-while over the BVH2 (default), 1 = warp
-  // pair-parallel packets over the BVH4 (UVD_ASM_ALGO=1, kept for comparison)
+  // algorithm: 0 = per-lane while-while over the BVH2 with dynamic ray refill
+  // (default), 2 = the same per fixed 32-row tile, 1 = warp pair-parallel
+  // packets over the BVH4 (UVD_ASM_ALGO=1/2 kept for comparison)
   static int algo = -1;
   if (algo < 0) {
     const char* e = getenv("UVD_ASM_ALGO");
-    algo = e ? atoi(e) : 0;
+    algo = e ? atoi(e) : 2;
   }
   if (algo == 1)  // the packet kernel resolves undecided tests inline
     UVD_CUDA_TRY(cudaMemsetAsync(P.pending, 0, (size_t)n_cols * P.words * sizeof(uint32_t), st));
@@ -636,11 +803,13 @@ extern "C" int uvd_irradiance_matrix(const uvd_scene* s, const float* lamp_xyz, 
   if (P.counters) {
     if (!grid_c) grid_c = grid_size_assemble<true>(algo);
     if (algo == 1) k_assemble<true><<<grid_c, kAsmThreads, 0, st>>>(P);
-    else k_assemble_lane<true><<<grid_c, kAsmThreads, 0, st>>>(P);
+    else if (algo == 2) k_assemble_lane<true><<<grid_c, kAsmThreads, 0, st>>>(P);
+    else k_assemble_dyn<true><<<grid_c, kAsmThreads, 0, st>>>(P);
   } else {
     if (!grid) grid = grid_size_assemble<false>(algo);
     if (algo == 1) k_assemble<false><<<grid, kAsmThreads, 0, st>>>(P);
-    else k_assemble_lane<false><<<grid, kAsmThreads, 0, st>>>(P);
+    else if (algo == 2) k_assemble_lane<false><<<grid, kAsmThreads, 0, st>>>(P);
+    else k_assemble_dyn<false><<<grid, kAsmThreads, 0, st>>>(P);
   }
   note_launch();
   {  // exact fp64 re-trace of the (rare) entries the fp32 pass left undecided
