@@ -13,6 +13,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <string>
 #include <cmath>
 
 #include "uvd_internal.cuh"
@@ -314,6 +316,209 @@ __global__ void k_emit_small(const float4* __restrict__ tri, int64_t n, Node* no
   nodes[0] = nd;
 }
 
+// ------------------------------------------------------------------ PLOC --
+// Parallel Locally-Ordered Clustering (Meister & Bittner 2018): start from one
+// cluster per triangle in Morton order; every round each cluster finds its
+// nearest neighbour (smallest surface area of the union box) within a window
+// of +-kPlocRadius positions, mutual nearest neighbours merge into a new
+// internal node, and the surviving clusters are compacted in order.  Yields a
+// tree of markedly better SAH quality than the Karras LBVH (fewer node visits
+// per shadow ray), in the same (left, right, range, box) arrays.
+constexpr int kPlocRadius = 16;
+
+__device__ __forceinline__ float union_area(const float* __restrict__ a, const float* __restrict__ b) {
+  float dx = fmaxf(a[3], b[3]) - fminf(a[0], b[0]);
+  float dy = fmaxf(a[4], b[4]) - fminf(a[1], b[1]);
+  float dz = fmaxf(a[5], b[5]) - fminf(a[2], b[2]);
+  return dx * dy + dy * dz + dz * dx;
+}
+
+// cluster k: box cbox[6k..6k+5], node id cid[k] (< 0: leaf triangle ~cid)
+__global__ void k_ploc_init(const float4* __restrict__ tri, int64_t n, float* __restrict__ cbox,
+                            int32_t* __restrict__ cid) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  Box x = tri_box(tri, i);
+  float* o = cbox + 6 * i;
+  o[0] = x.lx; o[1] = x.ly; o[2] = x.lz; o[3] = x.hx; o[4] = x.hy; o[5] = x.hz;
+  cid[i] = (int32_t)(0x80000000u | (uint32_t)i);
+}
+
+__global__ void k_ploc_nn(const float* __restrict__ cbox, const int* __restrict__ n_ptr,
+                          int32_t* __restrict__ nn) {
+  const int n = *n_ptr;
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float* bi = cbox + 6 * i;
+  float best = INFINITY;
+  int bj = -1;
+  const int lo = max(0, i - kPlocRadius), hi = min(n - 1, i + kPlocRadius);
+  for (int j = lo; j <= hi; ++j) {
+    if (j == i) continue;
+    float d = union_area(bi, cbox + 6 * j);
+    if (d < best || (d == best && j < bj)) { best = d; bj = j; }
+  }
+  nn[i] = bj;
+}
+
+// flag[i] = 1 if cluster i survives (merge leader or unmerged); merges[i] = 1
+// if i leads a merge
+__global__ void k_ploc_flags(const int32_t* __restrict__ nn, const int* __restrict__ n_ptr,
+                             int32_t* __restrict__ keep, int32_t* __restrict__ lead) {
+  const int n = *n_ptr;
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int j = nn[i];
+  const bool mutual = j >= 0 && nn[j] == i;
+  lead[i] = mutual && i < j;
+  keep[i] = !mutual || i < j;
+}
+
+// inclusive scans of two int32 arrays (<= 2^31) in one block
+__global__ void __launch_bounds__(1024) k_scan2_incl(int32_t* __restrict__ a, int32_t* __restrict__ b,
+                                                     const int* __restrict__ n_ptr) {
+  __shared__ int32_t pa[1024], pb[1024];
+  const int n = *n_ptr;
+  const int per = (n + 1023) / 1024;
+  const int s = threadIdx.x * per, e = min(s + per, n);
+  int32_t sa = 0, sb = 0;
+  for (int i = s; i < e; ++i) { sa += a[i]; sb += b[i]; }
+  pa[threadIdx.x] = sa;
+  pb[threadIdx.x] = sb;
+  __syncthreads();
+  for (int off = 1; off < 1024; off <<= 1) {
+    int32_t va = threadIdx.x >= off ? pa[threadIdx.x - off] : 0;
+    int32_t vb = threadIdx.x >= off ? pb[threadIdx.x - off] : 0;
+    __syncthreads();
+    pa[threadIdx.x] += va;
+    pb[threadIdx.x] += vb;
+    __syncthreads();
+  }
+  int32_t ra = threadIdx.x ? pa[threadIdx.x - 1] : 0, rb = threadIdx.x ? pb[threadIdx.x - 1] : 0;
+  for (int i = s; i < e; ++i) { ra += a[i]; a[i] = ra; rb += b[i]; b[i] = rb; }
+}
+
+// merge leaders create node (node_base + lead_rank); survivors compact into
+// the output arrays in order; the new cluster count is written to n_out
+__global__ void k_ploc_merge(const float* __restrict__ cbox, const int32_t* __restrict__ cid,
+                             const int32_t* __restrict__ nn, const int32_t* __restrict__ keep_incl,
+                             const int32_t* __restrict__ lead_incl, const int* __restrict__ n_ptr,
+                             const int* __restrict__ node_base, float* __restrict__ cbox_out,
+                             int32_t* __restrict__ cid_out, int32_t* __restrict__ left,
+                             int32_t* __restrict__ right, float* __restrict__ ibox,
+                             int32_t* __restrict__ parent_int, int32_t* __restrict__ parent_leaf,
+                             int* __restrict__ n_out, int* __restrict__ node_base_out) {
+  const int n = *n_ptr;
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i == 0) {
+    *n_out = keep_incl[n - 1];
+    *node_base_out = *node_base - lead_incl[n - 1];
+  }
+  if (i >= n) return;
+  const int kept = keep_incl[i] - (i ? keep_incl[i - 1] : 0);
+  if (!kept) return;
+  const int o = keep_incl[i] - 1;
+  const int j = nn[i];
+  const bool lead = (lead_incl[i] - (i ? lead_incl[i - 1] : 0)) != 0;
+  float* bo = cbox_out + 6 * o;
+  if (!lead) {
+    for (int k = 0; k < 6; ++k) bo[k] = cbox[6 * i + k];
+    cid_out[o] = cid[i];
+    return;
+  }
+  // internal nodes are numbered downwards from n_tris - 2 so the last merge is the root (0)
+  const int node = *node_base - lead_incl[i];
+  const float* a = cbox + 6 * i;
+  const float* b = cbox + 6 * j;
+  float u[6] = {fminf(a[0], b[0]), fminf(a[1], b[1]), fminf(a[2], b[2]),
+                fmaxf(a[3], b[3]), fmaxf(a[4], b[4]), fmaxf(a[5], b[5])};
+  for (int k = 0; k < 6; ++k) { bo[k] = u[k]; ibox[6 * node + k] = u[k]; }
+  const int32_t ci = cid[i], cj = cid[j];
+  left[node] = ci;
+  right[node] = cj;
+  if (ci < 0) parent_leaf[ci & 0x7fffffff] = node; else parent_int[ci] = node;
+  if (cj < 0) parent_leaf[cj & 0x7fffffff] = node; else parent_int[cj] = node;
+  cid_out[o] = node;
+}
+
+// subtree sizes bottom-up (arrival counters, like the refit)
+__global__ void k_subtree_size(const int32_t* __restrict__ parent_leaf, const int32_t* __restrict__ parent_int,
+                               const int32_t* __restrict__ left, const int32_t* __restrict__ right,
+                               int64_t n, int32_t* __restrict__ size, int* __restrict__ arrive) {
+  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  int32_t p = parent_leaf[r];
+  while (p >= 0) {
+    __threadfence();
+    if (atomicAdd(&arrive[p], 1) == 0) return;
+    __threadfence();
+    const int32_t l = left[p], q = right[p];
+    const int32_t sl = l < 0 ? 1 : ((volatile int32_t*)size)[l];
+    const int32_t sr = q < 0 ? 1 : ((volatile int32_t*)size)[q];
+    ((volatile int32_t*)size)[p] = sl + sr;
+    p = p == 0 ? -1 : parent_int[p];
+  }
+}
+
+// DFS leaf order: first[node] = number of leaves left of the subtree, found by
+// walking up from each node; each triangle's new position is first of its leaf
+__global__ void k_dfs_first(const int32_t* __restrict__ parent_int, const int32_t* __restrict__ left,
+                            const int32_t* __restrict__ size, int64_t n_int, int32_t* __restrict__ first) {
+  int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v >= n_int) return;
+  int32_t off = 0, c = (int32_t)v;
+  while (c != 0) {
+    const int32_t p = parent_int[c];
+    if (left[p] != c) {  // c is the right child: everything under the left sibling precedes it
+      const int32_t l = left[p];
+      off += l < 0 ? 1 : size[l];
+    }
+    c = p;
+  }
+  first[v] = off;
+}
+
+__global__ void k_leaf_pos(const int32_t* __restrict__ parent_leaf, const int32_t* __restrict__ left,
+                           const int32_t* __restrict__ right, const int32_t* __restrict__ size,
+                           const int32_t* __restrict__ first, int64_t n, int32_t* __restrict__ pos) {
+  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int32_t p = parent_leaf[r];
+  const int32_t me = (int32_t)(0x80000000u | (uint32_t)r);
+  if (left[p] == me) pos[r] = first[p];
+  else pos[r] = first[p] + (left[p] < 0 ? 1 : size[left[p]]);
+}
+
+// rewrite leaf refs to DFS positions and compute node ranges
+__global__ void k_ploc_finish(int32_t* __restrict__ left, int32_t* __restrict__ right,
+                              const int32_t* __restrict__ size, const int32_t* __restrict__ first,
+                              const int32_t* __restrict__ pos, int64_t n_int, int32_t* __restrict__ rfirst,
+                              int32_t* __restrict__ rlast) {
+  int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v >= n_int) return;
+  int32_t l = left[v], r = right[v];
+  if (l < 0) left[v] = (int32_t)(0x80000000u | (uint32_t)pos[l & 0x7fffffff]);
+  if (r < 0) right[v] = (int32_t)(0x80000000u | (uint32_t)pos[r & 0x7fffffff]);
+  rfirst[v] = first[v];
+  rlast[v] = first[v] + size[v] - 1;
+}
+
+__global__ void k_scatter_tri(const float4* __restrict__ in, const int32_t* __restrict__ pos, int64_t n,
+                              float4* __restrict__ out) {
+  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int64_t d = pos[r];
+  out[3 * d] = in[3 * r];
+  out[3 * d + 1] = in[3 * r + 1];
+  out[3 * d + 2] = in[3 * r + 2];
+}
+
+// 3D scenes: the owner (row) of the triangle at Morton position r is r
+__global__ void k_set_owner(float4* __restrict__ tri, int64_t n) {
+  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r < n) tri[3 * r].w = __int_as_float((int)r);
+}
+
 // ------------------------------------------------------------ BVH4 collapse --
 // Top-down, one frontier level per launch: BVH4 node n takes BVH2 node b's two
 // children and repeatedly opens the internal child of largest surface area
@@ -419,6 +624,66 @@ __global__ void k_gather_tri(const float4* __restrict__ tri_in, const uint32_t* 
 
 static inline unsigned grid_for(int64_t n, int t) { return (unsigned)((n + t - 1) / t); }
 
+// PLOC driver: clusters -> binary tree (left/right/ibox/parents), then DFS
+// leaf order (triangles reordered so every subtree is a contiguous range).
+static int build_ploc(uvd_scene* s, int64_t M, int32_t* left, int32_t* right, int32_t* rf, int32_t* rl,
+                      int32_t* pint, int32_t* pleaf, float* ibox, int* arrive, cudaStream_t st) {
+  Alloc& al = s->alloc;
+  float* cbA = (float*)al.get(M * 6 * sizeof(float));
+  float* cbB = (float*)al.get(M * 6 * sizeof(float));
+  int32_t* idA = (int32_t*)al.get(M * 4);
+  int32_t* idB = (int32_t*)al.get(M * 4);
+  int32_t* nn = (int32_t*)al.get(M * 4);
+  int32_t* keep = (int32_t*)al.get(M * 4);
+  int32_t* lead = (int32_t*)al.get(M * 4);
+  int* ctr = (int*)al.get(4 * sizeof(int));  // nA, baseA, nB, baseB
+  float4* tri2 = (float4*)al.get(3 * M * sizeof(float4));
+  if (!cbA || !cbB || !idA || !idB || !nn || !keep || !lead || !ctr || !tri2) {
+    set_error("scene: out of device memory (PLOC scratch)");
+    return UVD_ERR_NOMEM;
+  }
+  k_ploc_init<<<grid_for(M, 256), 256, 0, st>>>(s->tri, M, cbA, idA);
+  note_launch();
+  int h[4] = {(int)M, (int)(M - 1), 0, 0};
+  UVD_CUDA_TRY(cudaMemcpyAsync(ctr, h, 4 * sizeof(int), cudaMemcpyHostToDevice, st));
+  int n_host = (int)M, iters = 0;
+  while (n_host > 1) {
+    for (int sub = 0; sub < 4; ++sub, ++iters) {
+      const unsigned g = grid_for(n_host, 256);
+      k_ploc_nn<<<g, 256, 0, st>>>(cbA, ctr + 0, nn);
+      k_ploc_flags<<<g, 256, 0, st>>>(nn, ctr + 0, keep, lead);
+      k_scan2_incl<<<1, 1024, 0, st>>>(keep, lead, ctr + 0);
+      k_ploc_merge<<<g, 256, 0, st>>>(cbA, idA, nn, keep, lead, ctr + 0, ctr + 1, cbB, idB, left, right,
+                                      ibox, pint, pleaf, ctr + 2, ctr + 3);
+      note_launch(4);
+      UVD_CUDA_TRY(cudaMemcpyAsync(ctr, ctr + 2, 2 * sizeof(int), cudaMemcpyDeviceToDevice, st));
+      std::swap(cbA, cbB);
+      std::swap(idA, idB);
+    }
+    UVD_CUDA_TRY(cudaMemcpyAsync(h, ctr, 2 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    UVD_CUDA_TRY(cudaStreamSynchronize(st));
+    n_host = h[0];
+    if (iters > 8192) { set_error("scene: PLOC did not converge"); return UVD_ERR_CUDA; }
+  }
+  // subtree sizes, DFS positions, reorder triangles, leaf refs -> positions
+  const int64_t ni = M - 1;
+  int32_t* size = keep;   // reuse scratch (sizes of internal nodes)
+  int32_t* first = lead;
+  int32_t* pos = nn;
+  k_subtree_size<<<grid_for(M, 256), 256, 0, st>>>(pleaf, pint, left, right, M, size, arrive);
+  k_dfs_first<<<grid_for(ni, 256), 256, 0, st>>>(pint, left, size, ni, first);
+  k_leaf_pos<<<grid_for(M, 256), 256, 0, st>>>(pleaf, left, right, size, first, M, pos);
+  k_scatter_tri<<<grid_for(M, 256), 256, 0, st>>>(s->tri, pos, M, tri2);
+  k_ploc_finish<<<grid_for(ni, 256), 256, 0, st>>>(left, right, size, first, pos, ni, rf, rl);
+  note_launch(5);
+  UVD_CUDA_TRY(cudaMemcpyAsync(s->tri, tri2, 3 * M * sizeof(float4), cudaMemcpyDeviceToDevice, st));
+  UVD_CUDA_TRY(cudaGetLastError());
+  for (void* p : {(void*)cbA, (void*)cbB, (void*)idA, (void*)idB, (void*)nn, (void*)keep, (void*)lead,
+                  (void*)ctr, (void*)tri2})
+    al.put(p);
+  return UVD_OK;
+}
+
 // Morton-sort the triangles (tri_in, input order) and build the BVH over them.
 // On return s->tri is leaf-ordered and `order` (if non-null) receives the
 // sorted -> input permutation (caller frees).
@@ -445,6 +710,10 @@ int build_bvh(uvd_scene* s, float4* tri_in, uint32_t** order_out, cudaStream_t s
   UVD_TRY(sort_pairs_u64(keys, vals, M, al, st));
   k_gather_tri<<<grid_for(M, 256), 256, 0, st>>>(tri_in, vals, M, s->tri);
   note_launch();
+  if (s->kind == UVD_SCENE_TRIMESH) {  // row (patch) of the triangle at Morton position r is r
+    k_set_owner<<<grid_for(M, 256), 256, 0, st>>>(s->tri, M);
+    note_launch();
+  }
   if (M <= kLeafMax) {
     k_emit_small<<<1, 1, 0, st>>>(s->tri, M, s->nodes, cp);
     note_launch();
@@ -467,10 +736,19 @@ int build_bvh(uvd_scene* s, float4* tri_in, uint32_t** order_out, cudaStream_t s
       return UVD_ERR_NOMEM;
     }
     UVD_CUDA_TRY(cudaMemsetAsync(arrive, 0, ni * sizeof(int), st));
-    k_karras<<<grid_for(ni, 256), 256, 0, st>>>(keys, M, left, right, rf, rl, pint, pleaf);
-    note_launch();
-    k_refit<<<grid_for(M, 256), 256, 0, st>>>(s->tri, M, left, right, pint, pleaf, ibox, arrive);
-    note_launch();
+    static int use_karras = -1;
+    if (use_karras < 0) {
+      const char* e = getenv("UVD_BVH");
+      use_karras = e && std::string(e) == "karras";
+    }
+    if (use_karras) {  // Karras 2012 LBVH + bottom-up refit
+      k_karras<<<grid_for(ni, 256), 256, 0, st>>>(keys, M, left, right, rf, rl, pint, pleaf);
+      note_launch();
+      k_refit<<<grid_for(M, 256), 256, 0, st>>>(s->tri, M, left, right, pint, pleaf, ibox, arrive);
+      note_launch();
+    } else {  // PLOC (default): agglomerative clustering over the Morton order
+      UVD_TRY(build_ploc(s, M, left, right, rf, rl, pint, pleaf, ibox, arrive, st));
+    }
     k_emit<<<grid_for(ni, 256), 256, 0, st>>>(s->tri, M, left, right, rf, rl, ibox, s->nodes, cp);
     note_launch();
     s->root = 0;

@@ -154,7 +154,7 @@ __global__ void k_permute_patches(const uint32_t* __restrict__ order, int64_t N,
                                   const float* __restrict__ cen_in, const float* __restrict__ nrm_in,
                                   const double* __restrict__ area_in, float* __restrict__ cen,
                                   float* __restrict__ nrm, double* __restrict__ area,
-                                  int64_t* __restrict__ orig, float4* __restrict__ tri) {
+                                  int64_t* __restrict__ orig) {
   int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (r >= N) return;
   int64_t t = order[r];
@@ -164,7 +164,6 @@ __global__ void k_permute_patches(const uint32_t* __restrict__ order, int64_t N,
   }
   area[r] = area_in[t];
   orig[r] = t;
-  tri[3 * r].w = __int_as_float((int)r);
 }
 
 __global__ void k_iota64(int64_t* __restrict__ a, int64_t n) {
@@ -299,7 +298,7 @@ static int create_trimesh(uvd_scene* s, const uvd_scene_desc* d, cudaStream_t st
   }
   k_permute_patches<<<grid_for(M, 256), 256, 0, st>>>(order, M, cen_in, nrm_in, area_in,
                                                        s->centroid, s->normal, s->area,
-                                                       s->orig_id, s->tri);
+                                                       s->orig_id);
   note_launch();
   UVD_CUDA_TRY(cudaGetLastError());
   for (void* p : {(void*)dV, (void*)dF, (void*)tri_in, (void*)cen_in, (void*)nrm_in,

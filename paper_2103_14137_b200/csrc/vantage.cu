@@ -125,7 +125,9 @@ __device__ bool is_free(const Scene3& S, D3 p) {
         const float4* t = S.tri + 3 * (int64_t)(st + k);
         bool fr = false;
         double th = ray_tri_t(p, w, ww, t[0], t[1], t[2], &fr);
-        if (th > 0.0 && th < best) { best = th; best_front = fr; }
+        // nearest hit; at an exactly equal t (a shared edge) a front face wins,
+        // so the answer does not depend on the traversal order
+        if (th > 0.0 && (th < best || (th == best && fr && !best_front))) { best = th; best_front = fr; }
       }
     } else {
       Node nd = S.nodes[ref];
