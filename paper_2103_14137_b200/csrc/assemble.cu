@@ -440,14 +440,14 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmMinBlocks) k_assemble_lane(As
         }
       }
       const uint32_t vm = __ballot_sync(0xffffffffu, vis);
-      if (P.vis_bits && lane == 0 && tile < P.words) P.vis_bits[(c * P.L + l) * P.words + tile] = vm;
+      if (P.vis_bits && lane == 0 && tile < P.words) __stcs(P.vis_bits + (c * P.L + l) * P.words + tile, vm);
     }
     // entries with an undecided ray are re-traced exactly by k_fixup
     const uint32_t pm = __ballot_sync(0xffffffffu, pend);
-    if (lane == 0 && tile < P.words) P.pending[c * P.words + tile] = pm;
+    if (lane == 0 && tile < P.words) __stcs(P.pending + c * P.words + tile, pm);
     if (COUNT) cnt[4] += pend;
     const float a = (float)(acc * P.scale);
-    if (P.values) P.values[c * P.ld + r] = a;
+    if (P.values) __stcs(P.values + c * P.ld + r, a);  // streaming: keep the BVH in L2
   }
   if (COUNT)
     for (int k = 0; k < 6; ++k) {

@@ -324,7 +324,10 @@ __global__ void k_emit_small(const float4* __restrict__ tri, int64_t n, Node* no
 // internal node, and the surviving clusters are compacted in order.  Yields a
 // tree of markedly better SAH quality than the Karras LBVH (fewer node visits
 // per shadow ray), in the same (left, right, range, box) arrays.
-constexpr int kPlocRadius = 16;
+#ifndef UVD_PLOC_RADIUS
+#define UVD_PLOC_RADIUS 16
+#endif
+constexpr int kPlocRadius = UVD_PLOC_RADIUS;
 
 __device__ __forceinline__ float union_area(const float* __restrict__ a, const float* __restrict__ b) {
   float dx = fmaxf(a[3], b[3]) - fminf(a[0], b[0]);

@@ -41,7 +41,10 @@ constexpr double kSelfEps = 1e-4;     // Q6: open segment t in (1e-4/d, 1 - 1e-4
 constexpr double kMinDist = 1e-9;     // domain error below 1e-9 m
 constexpr double kEdgeTol = 1e-12;    // watertight acceptance of fp64 margins
 constexpr double kParallel = 1e-12;   // |det| <= 1e-12 |D||E1xE2| -> no crossing
-constexpr int kLeafMax = 4;           // triangles per BVH leaf (subtree collapse)
+#ifndef UVD_LEAF_MAX
+#define UVD_LEAF_MAX 2
+#endif
+constexpr int kLeafMax = UVD_LEAF_MAX;  // triangles per BVH leaf (subtree collapse), <= 8
 constexpr int kStackDepth = 128;      // per-warp traversal stack entries
 // Q20 free-space test direction (tilted off the axes).
 constexpr double kFreeDirX = 0.0123, kFreeDirY = 0.0371, kFreeDirZ = 1.0;
