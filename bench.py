@@ -53,6 +53,7 @@ def parse():
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-clocks", action="store_true", help="diagnostics: skip the nvidia-smi sampler")
     return ap.parse_args()
 
 
@@ -225,7 +226,7 @@ def main():
         __graft_entry__.build()
     if ws > 1:
         dist.barrier()
-    from paper_2103_14137_b200 import uvd
+    from paper_2103_14137_b200 import shard, uvd
     from synth import configs, vectors
 
     wl = workload(args.workload)
@@ -243,7 +244,7 @@ def main():
     lamps, _ = scene.vantage(wl["vantage"])
     N, K, L = scene.N, lamps.shape[0], lamps.shape[1]
     ld = scene.ld()
-    cols = [j for j in range(K) if (j // 32) % ws == rank]
+    cols = shard.block_cyclic(K, ws, rank, 32)
     n_loc = len(cols)
     A = torch.empty((n_loc, ld), dtype=torch.float32, device=dev)
     t_glob = vectors.sparse_plan(K, seed=0)
@@ -257,23 +258,36 @@ def main():
     ev_k0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ev_k1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
 
+    phase_names = ("scene", "vantage", "irradiance", "fluence", "coverage")
+    ev_ph = [[torch.cuda.Event(enable_timing=True) for _ in range(len(phase_names) + 1)]
+             for _ in range(args.steps)]
+
     def step(i=None):
+        ev = ev_ph[i] if i is not None else None
+        if ev:
+            ev[0].record(stream)
         sc = uvd.Scene(desc_dev)                              # a1, a2
+        if ev:
+            ev[1].record(stream)
         lam, _ = sc.vantage(wl["vantage"])                    # a3
-        if i is not None:
+        if ev:
+            ev[2].record(stream)
             ev_k0[i].record(stream)
         sc.irradiance(lam, cols=cols, out=A)                  # a4–a6
-        if i is not None:
+        if ev:
             ev_k1[i].record(stream)
+            ev[3].record(stream)
         mu = uvd.fluence(A, N, t_loc)                         # a7: μ = A·t
         rowsum = uvd.fluence(A, N, ones)                      #     A·𝟙 (ever-visible rows)
         g = uvd.fluence(A, N, y, transpose=True)              #     g = Aᵀ·y
-        if ws > 1:
-            dist.all_reduce(mu)
-            dist.all_reduce(rowsum)
+        shard.reduce_partials(mu, rowsum)                     # NCCL all_reduce (N > 1)
+        if ev:
+            ev[4].record(stream)
         cov = sc.coverage(mu, configs.MU_MIN, rowsum)         # a8
         sc.sync_status()
         sc.close()
+        if ev:
+            ev[5].record(stream)
         return cov, g
 
     for _ in range(max(3, args.warmup)):
@@ -282,7 +296,8 @@ def main():
     if ws > 1:
         dist.barrier()
     clocks = ClockSampler(local)
-    clocks.start()
+    if not args.no_clocks:
+        clocks.start()
     n_launch0 = uvd.launch_count()
     torch.cuda.synchronize()
     if ws > 1:
@@ -300,12 +315,11 @@ def main():
     n_launch = uvd.launch_count() - n_launch0
     clk = clocks.stop()
     k_ms = float(np.mean([a.elapsed_time(b) for a, b in zip(ev_k0, ev_k1)]))
-    if ws > 1:
-        tt = torch.tensor([ms_total, k_ms], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        ms_total, k_ms = float(tt[0]), float(tt[1])
+    ms_total, k_ms = shard.max_over_ranks([ms_total, k_ms], device=dev)
     ms_step = ms_total / args.steps
     value = N * K / (ms_step / 1e3)
+    phases = {nm: float(np.mean([e[k].elapsed_time(e[k + 1]) for e in ev_ph]))
+              for k, nm in enumerate(phase_names)}
 
     # roofline of the dominant kernel: algorithmic work from one instrumented launch
     sc = uvd.Scene(desc_dev)
@@ -313,10 +327,7 @@ def main():
     r = sc.irradiance(lam, cols=cols, out=A, counters=True)
     cnt = r["counters"].cpu().numpy().astype(np.float64)
     sc.close()
-    if ws > 1:
-        ct = torch.from_numpy(cnt).to(dev)
-        dist.all_reduce(ct)
-        cnt = ct.cpu().numpy()
+    cnt = shard.sum_over_ranks(cnt, device=dev).cpu().numpy()
     pairs = float(N) * K * L
     flops = FLOP_PER_PAIR * pairs + FLOP_PER_RAY * cnt[0] + FLOP_PER_BOX * cnt[1] + FLOP_PER_TRI * cnt[2]
     achieved = flops / ws / (k_ms / 1e3) / 1e12
@@ -332,7 +343,7 @@ def main():
     # end to end through the public API from pinned host buffers
     e2e = None
     if not args.no_e2e:
-        e2e = run_e2e(uvd, configs, wl, sc_np, is_mesh, cols, n_loc, ld, N, K, t_glob, ws, dev,
+        e2e = run_e2e(uvd, shard, configs, wl, sc_np, is_mesh, cols, n_loc, ld, N, K, t_glob, dev,
                       dist if ws > 1 else None, max(1, min(args.steps, 3)))
 
     cpu = None
@@ -355,7 +366,7 @@ def main():
                                  f"{K * ld * 4 / 1e9:.1f} GB dense A",
                            "precision": "fp32 conservative box tests; fp64 triangle tests and Eq. 7; A stored fp32",
                            "step": "scene_create+vantage+irradiance+fluence(A·t, A·1, Aᵀy)+coverage"},
-                "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "phases_ms": phases, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(n_launch), "clocks": clk}
         print(json.dumps(line), flush=True)
     if ws > 1:
@@ -364,7 +375,7 @@ def main():
     return 0
 
 
-def run_e2e(uvd, configs, wl, sc_np, is_mesh, cols, n_loc, ld, N, K, t_glob, ws, dev, dist, steps):
+def run_e2e(uvd, shard, configs, wl, sc_np, is_mesh, cols, n_loc, ld, N, K, t_glob, dev, dist, steps):
     """Same metric through the public API with HOST inputs: the triangle soup
     and t are copied from pinned host memory and μ + coverage are read back
     inside the timed region (wall clock, max over ranks)."""
@@ -387,8 +398,7 @@ def run_e2e(uvd, configs, wl, sc_np, is_mesh, cols, n_loc, ld, N, K, t_glob, ws,
         sc.irradiance(lam, cols=cols, out=A)
         t = th.to(dev, non_blocking=True)
         mu = uvd.fluence(A, N, t)
-        if dist is not None:
-            dist.all_reduce(mu)
+        shard.reduce_partials(mu)
         cov = sc.coverage(mu, configs.MU_MIN)
         mu_h.copy_(mu, non_blocking=True)
         torch.cuda.synchronize()
@@ -403,10 +413,7 @@ def run_e2e(uvd, configs, wl, sc_np, is_mesh, cols, n_loc, ld, N, K, t_glob, ws,
     for _ in range(steps):
         one()
     el = time.perf_counter() - t0
-    if dist is not None:
-        tt = torch.tensor([el], dtype=torch.float64, device=dev)
-        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        el = float(tt[0])
+    el = shard.max_over_ranks([el], device=dev)[0]
     return {"value": N * K / (el / steps), "unit": UNIT, "steps": steps,
             "h2d_bytes_per_step": int(h2d_scene + th.numel() * 8),
             "d2h_bytes_per_step": int(N * 8 + 3 * 8 + 8)}

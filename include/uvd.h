@@ -176,8 +176,10 @@ enum { UVD_DENSE_COLMAJOR = 0, UVD_CSC = 1 };
  *                  ld >= N and ld % 32 == 0 (torch shape (n_cols, ld)).
  *  CSC:            colptr[n_cols+1] int64, rowidx[nnz_cap] int32, values[nnz_cap]
  *                  fp32, rows ascending within a column; entries are the nonzero
- *                  A[i,j].  Two-phase: if nnz > nnz_cap the call returns
- *                  UVD_ERR_CAPACITY after writing colptr (colptr[n_cols] = nnz).
+ *                  A[i,j] (a patch seen by at least one lamp sample).  Two-phase:
+ *                  if nnz > nnz_cap the call returns UVD_ERR_CAPACITY after
+ *                  writing colptr (colptr[n_cols] = nnz); call with nnz_cap = 0
+ *                  to size.  The CSC path synchronises `stream` (to read nnz).
  *  vis_bits  (optional): [n_cols][L][ceil(N/32)] uint32, bit (i%32) of word i/32 =
  *            patch i front-facing and unoccluded from lamp sample l.
  *  col_sumsq (optional): [n_cols] fp64 Σ_i A[i,c]² (for ‖A‖_F).
@@ -221,8 +223,10 @@ UVD_API int uvd_sync_status(const uvd_scene* scene, void* stream);
  *  transpose = 1:  out[k] = Aᵀ · x     (x = y[n]; out = g)
  * A is a uvd_matrix_out previously filled by uvd_irradiance_matrix (dense or CSC),
  * n = number of patches, k = number of local columns.  x, out DEVICE fp64.
- * For A·t, columns with t_k == 0 are skipped.  Summation order is fixed
- * (deterministic).  Asynchronous. */
+ * For A·t, columns with t_k == 0 are skipped.  Dense: the summation order is
+ * fixed (deterministic).  CSC: A·t accumulates with fp64 atomics (order of the
+ * per-row additions not fixed: results may differ by a few fp64 ulps), Aᵀ·y is
+ * deterministic.  Asynchronous. */
 UVD_API int uvd_fluence(const uvd_matrix_out* A, int64_t n, int64_t k, int transpose, const double* x,
                 double* out, void* stream);
 

@@ -4,9 +4,12 @@
 //   k_morton    63-bit Morton code of each triangle centroid in the scene bbox
 //   radix sort  hand-written LSD sort of (u64 key, u32 value), 8-bit digits,
 //               stable block-local ranking with warp match/ballot
-//   k_karras    internal-node topology from longest common prefixes
-//               (Karras 2012; equal keys broken by index)
-//   k_refit     bottom-up AABBs with atomic arrival counters
+//   PLOC        (default) agglomerative clustering of the Morton-ordered
+//               triangles (Meister & Bittner 2018): nearest neighbours within
+//               a +-16 window merge when mutual; DFS leaf order afterwards
+//   k_karras    (UVD_BVH=karras) internal-node topology from longest common
+//               prefixes (Karras 2012; equal keys broken by index) + k_refit,
+//               bottom-up AABBs with atomic arrival counters
 //   k_emit      BVH2 nodes holding both child boxes (64 B), subtrees of
 //               <= kLeafMax triangles collapsed into leaf ranges, boxes padded
 //               outward so fp32 slab tests are conservative for the fp64 ray.
@@ -522,98 +525,6 @@ __global__ void k_set_owner(float4* __restrict__ tri, int64_t n) {
   if (r < n) tri[3 * r].w = __int_as_float((int)r);
 }
 
-// ------------------------------------------------------------ BVH4 collapse --
-// Top-down, one frontier level per launch: BVH4 node n takes BVH2 node b's two
-// children and repeatedly opens the internal child of largest surface area
-// (never a subtree of <= kLeafMax triangles, which becomes a leaf range) until
-// it has 4 children.  Internal children get new BVH4 nodes (atomic counter)
-// and join the next frontier.
-struct Frontier { int32_t b2; int32_t n4; };
-
-__device__ __forceinline__ float box_area(Box x) {
-  float dx = x.hx - x.lx, dy = x.hy - x.ly, dz = x.hz - x.lz;
-  return dx * dy + dy * dz + dz * dx;
-}
-
-__global__ void k_collapse4(const float4* __restrict__ tri, const int32_t* __restrict__ left,
-                            const int32_t* __restrict__ right, const int32_t* __restrict__ rfirst,
-                            const int32_t* __restrict__ rlast, const float* __restrict__ ibox,
-                            const Frontier* __restrict__ cur, const int* __restrict__ cur_n,
-                            Frontier* __restrict__ nxt, int* __restrict__ nxt_n,
-                            int* __restrict__ n4_count, Node4* __restrict__ nodes4, float cp) {
-  int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= *cur_n) return;
-  Frontier f = cur[i];
-  int32_t ch[4] = {left[f.b2], right[f.b2], 0, 0};
-  int cnt = 2;
-  while (cnt < 4) {
-    int best = -1;
-    float ba = -1.f;
-    for (int k = 0; k < cnt; ++k) {
-      int32_t c = ch[k];
-      if (c >= 0 && rlast[c] - rfirst[c] + 1 > kLeafMax) {
-        float a = box_area(load_box(ibox, c));
-        if (a > ba) { ba = a; best = k; }
-      }
-    }
-    if (best < 0) break;
-    int32_t c = ch[best];
-    ch[best] = left[c];
-    ch[cnt++] = right[c];
-  }
-  float lo[3][4], hi[3][4];
-  uint32_t ref[4];
-  for (int k = 0; k < 4; ++k) {
-    if (k >= cnt) {
-      for (int a = 0; a < 3; ++a) { lo[a][k] = 1e30f; hi[a][k] = 1e30f; }
-      ref[k] = kEmptyRef;
-      continue;
-    }
-    Box bx;
-    child_info(tri, ibox, rfirst, rlast, ch[k], &bx, &ref[k]);
-    if (!ref_is_leaf(ref[k])) {
-      int m = atomicAdd(n4_count, 1);
-      int q = atomicAdd(nxt_n, 1);
-      nxt[q] = Frontier{ch[k], m};
-      ref[k] = (uint32_t)m;
-    }
-    lo[0][k] = pad_lo(bx.lx, cp); hi[0][k] = pad_hi(bx.hx, cp);
-    lo[1][k] = pad_lo(bx.ly, cp); hi[1][k] = pad_hi(bx.hy, cp);
-    lo[2][k] = pad_lo(bx.lz, cp); hi[2][k] = pad_hi(bx.hz, cp);
-  }
-  Node4 nd;
-  for (int k = 0; k < 4; ++k) {
-    nd.c[2 * k] = make_float4(lo[0][k], lo[1][k], lo[2][k], __uint_as_float(ref[k]));
-    nd.c[2 * k + 1] = make_float4(hi[0][k], hi[1][k], hi[2][k], 0.f);
-  }
-  nodes4[f.n4] = nd;
-}
-
-__global__ void k_collapse4_init(Frontier* fr, int* fr_n, int* n4_count) {
-  fr[0] = Frontier{0, 0};
-  *fr_n = 1;
-  *n4_count = 1;
-}
-
-__global__ void k_collapse4_swap(int* cur_n, int* nxt_n) {
-  *cur_n = *nxt_n;
-  *nxt_n = 0;
-}
-
-// single-leaf scene (M <= kLeafMax): root with one leaf child
-__global__ void k_emit4_small(const float4* __restrict__ tri, int64_t n, Node4* nodes4, float cp) {
-  Box b = tri_box(tri, 0);
-  for (int64_t r = 1; r < n; ++r) b = join(b, tri_box(tri, r));
-  Node4 nd;
-  nd.c[0] = make_float4(pad_lo(b.lx, cp), pad_lo(b.ly, cp), pad_lo(b.lz, cp), __uint_as_float(make_leaf(0u, (uint32_t)n)));
-  nd.c[1] = make_float4(pad_hi(b.hx, cp), pad_hi(b.hy, cp), pad_hi(b.hz, cp), 0.f);
-  for (int k = 1; k < 4; ++k) {
-    nd.c[2 * k] = make_float4(1e30f, 1e30f, 1e30f, __uint_as_float(kEmptyRef));
-    nd.c[2 * k + 1] = make_float4(1e30f, 1e30f, 1e30f, 0.f);
-  }
-  nodes4[0] = nd;
-}
-
 // gather input-order triangles into sorted (leaf) order
 __global__ void k_gather_tri(const float4* __restrict__ tri_in, const uint32_t* __restrict__ order,
                              int64_t M, float4* __restrict__ tri) {
@@ -697,8 +608,7 @@ int build_bvh(uvd_scene* s, float4* tri_in, uint32_t** order_out, cudaStream_t s
   uint32_t* vals = (uint32_t*)al.get(M * sizeof(uint32_t));
   s->tri = (float4*)al.get(3 * M * sizeof(float4));
   s->nodes = (Node*)al.get(std::max<int64_t>(M - 1, 1) * sizeof(Node));
-  s->nodes4 = (Node4*)al.get(std::max<int64_t>(M - 1, 1) * sizeof(Node4));
-  if (!keys || !vals || !s->tri || !s->nodes || !s->nodes4) {
+  if (!keys || !vals || !s->tri || !s->nodes) {
     set_error("scene: out of device memory building the BVH (M=%lld)", (long long)M);
     return UVD_ERR_NOMEM;
   }
@@ -720,10 +630,7 @@ int build_bvh(uvd_scene* s, float4* tri_in, uint32_t** order_out, cudaStream_t s
   if (M <= kLeafMax) {
     k_emit_small<<<1, 1, 0, st>>>(s->tri, M, s->nodes, cp);
     note_launch();
-    k_emit4_small<<<1, 1, 0, st>>>(s->tri, M, s->nodes4, cp);
-    note_launch();
     s->root = 0;
-    s->n_nodes4 = 1;
   } else {
     int64_t ni = M - 1;
     int32_t* left = (int32_t*)al.get(ni * 4);
@@ -755,34 +662,6 @@ int build_bvh(uvd_scene* s, float4* tri_in, uint32_t** order_out, cudaStream_t s
     k_emit<<<grid_for(ni, 256), 256, 0, st>>>(s->tri, M, left, right, rf, rl, ibox, s->nodes, cp);
     note_launch();
     s->root = 0;
-    // BVH4: frontier capacity = number of BVH2 internal nodes (upper bound)
-    Frontier* fa = (Frontier*)al.get(ni * sizeof(Frontier));
-    Frontier* fb = (Frontier*)al.get(ni * sizeof(Frontier));
-    int* ctr = (int*)al.get(4 * sizeof(int));
-    if (!fa || !fb || !ctr) { set_error("scene: out of device memory (BVH4 frontier)"); return UVD_ERR_NOMEM; }
-    k_collapse4_init<<<1, 1, 0, st>>>(fa, ctr + 0, ctr + 2);
-    note_launch();
-    UVD_CUDA_TRY(cudaMemsetAsync(ctr + 1, 0, sizeof(int), st));
-    int h_ctr[4] = {1, 0, 1, 0};
-    for (int level = 0; level < 4096 && h_ctr[0] > 0; ++level) {
-      // frontier sizes at most double per level; size the grid from the host copy
-      int64_t cap = std::min<int64_t>((int64_t)h_ctr[0], ni);
-      for (int sub = 0; sub < 6; ++sub) {  // 6 levels per host round trip
-        k_collapse4<<<grid_for(std::max<int64_t>(cap, 1), 128), 128, 0, st>>>(
-            s->tri, left, right, rf, rl, ibox, fa, ctr + 0, fb, ctr + 1, ctr + 2, s->nodes4, cp);
-        note_launch();
-        k_collapse4_swap<<<1, 1, 0, st>>>(ctr + 0, ctr + 1);
-        note_launch();
-        std::swap(fa, fb);
-        cap = std::min<int64_t>(cap * 4, ni);
-      }
-      UVD_CUDA_TRY(cudaMemcpyAsync(h_ctr, ctr, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
-      UVD_CUDA_TRY(cudaStreamSynchronize(st));
-    }
-    s->n_nodes4 = h_ctr[2];
-    al.put(fa);
-    al.put(fb);
-    al.put(ctr);
     for (void* p : {(void*)left, (void*)right, (void*)rf, (void*)rl, (void*)pint, (void*)pleaf,
                     (void*)ibox, (void*)arrive})
       al.put(p);

@@ -13,6 +13,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <mutex>
+#include <vector>
 
 #include "uvd_internal.cuh"
 
@@ -119,6 +121,41 @@ __global__ void __launch_bounds__(kGemvThreads) k_gemv_t(const float* __restrict
   }
 }
 
+// CSC: μ += A[:,c]·t_c for the nonzero columns (one block per column, fp64
+// atomics: the order of the per-row additions is not fixed, so results may
+// differ from the dense kernel by a few fp64 ulps); g_c = Σ_e vals·y[row]
+// (one block per column, fixed tree reduction)
+__global__ void k_csc_n(const int64_t* __restrict__ colptr, const int32_t* __restrict__ rowidx,
+                        const float* __restrict__ vals, const int32_t* __restrict__ idx,
+                        const double* __restrict__ val, const int32_t* __restrict__ cnt,
+                        double* __restrict__ out) {
+  for (int32_t q = blockIdx.x; q < *cnt; q += gridDim.x) {
+    const int64_t c = idx[q];
+    const double t = val[q];
+    for (int64_t e = colptr[c] + threadIdx.x; e < colptr[c + 1]; e += blockDim.x)
+      atomicAdd(out + rowidx[e], (double)vals[e] * t);
+  }
+}
+
+__global__ void __launch_bounds__(kGemvThreads) k_csc_t(const int64_t* __restrict__ colptr,
+                                                        const int32_t* __restrict__ rowidx,
+                                                        const float* __restrict__ vals,
+                                                        const double* __restrict__ y,
+                                                        double* __restrict__ out) {
+  const int64_t c = blockIdx.x;
+  double s = 0.0;
+  for (int64_t e = colptr[c] + threadIdx.x; e < colptr[c + 1]; e += kGemvThreads)
+    s += (double)vals[e] * y[rowidx[e]];
+  __shared__ double red[kGemvThreads];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = kGemvThreads / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) out[c] = red[0];
+}
+
 // coverage: per-block partials, then one block combines them in fixed order
 constexpr int kCovThreads = 256;
 __global__ void __launch_bounds__(kCovThreads) k_coverage_part(const double* __restrict__ mu,
@@ -157,12 +194,55 @@ __global__ void k_coverage_final(const double* __restrict__ part, int nb, double
 
 using namespace uvd;
 
+// Grow-only scratch for the nonzero-column list, one buffer per (device,
+// stream) so calls on different streams never share it (a stream-ordered pool
+// allocation at every call stalled up to hundreds of ms on B200).
+struct FluScratch {
+  int dev = -1;
+  cudaStream_t stream = nullptr;
+  size_t bytes = 0;
+  void* p = nullptr;
+};
+static std::mutex g_flu_mu;
+static std::vector<FluScratch> g_flu;
+
+static void* flu_scratch(size_t bytes, cudaStream_t st) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_flu_mu);
+  for (FluScratch& e : g_flu) {
+    if (e.dev != dev || e.stream != st) continue;
+    if (e.bytes >= bytes) return e.p;
+    cudaStreamSynchronize(st);  // the old buffer may still be read by this stream
+    cudaFree(e.p);
+    size_t b = std::max<size_t>(bytes, (size_t)2 * e.bytes);
+    if (cudaMalloc(&e.p, b) != cudaSuccess) { cudaGetLastError(); e.p = nullptr; e.bytes = 0; return nullptr; }
+    e.bytes = b;
+    return e.p;
+  }
+  FluScratch e;
+  e.dev = dev;
+  e.stream = st;
+  e.bytes = std::max<size_t>(bytes, 1 << 20);
+  if (cudaMalloc(&e.p, e.bytes) != cudaSuccess) { cudaGetLastError(); return nullptr; }
+  g_flu.push_back(e);
+  return e.p;
+}
+
 extern "C" int uvd_fluence(const uvd_matrix_out* A, int64_t n, int64_t k, int transpose,
                            const double* x, double* out, void* stream) {
   clear_error();
   if (!A || !x || !out || n < 0 || k < 0) { set_error("uvd_fluence: bad argument"); return UVD_ERR_INVALID; }
-  if (A->format != UVD_DENSE_COLMAJOR) { set_error("uvd_fluence: format %d not supported yet", A->format); return UVD_ERR_INVALID; }
-  if (!A->values || A->ld < n || A->ld % 4 != 0 || ((uintptr_t)A->values & 15)) {
+  const bool csc = A->format == UVD_CSC;
+  if (csc) {
+    if (!A->colptr || !A->rowidx || !A->values) {
+      set_error("uvd_fluence: CSC A needs colptr, rowidx and values");
+      return UVD_ERR_INVALID;
+    }
+  } else if (A->format != UVD_DENSE_COLMAJOR) {
+    set_error("uvd_fluence: unknown format %d", A->format);
+    return UVD_ERR_INVALID;
+  } else if (!A->values || A->ld < n || A->ld % 4 != 0 || ((uintptr_t)A->values & 15)) {
     set_error("uvd_fluence: dense A needs 16-B aligned values and ld >= n, ld %% 4 == 0");
     return UVD_ERR_INVALID;
   }
@@ -170,26 +250,31 @@ extern "C" int uvd_fluence(const uvd_matrix_out* A, int64_t n, int64_t k, int tr
   if (n == 0) return UVD_OK;
   if (!transpose) {
     if (k == 0) { UVD_CUDA_TRY(cudaMemsetAsync(out, 0, n * sizeof(double), st)); return UVD_OK; }
-    int32_t* idx = nullptr;
-    double* val = nullptr;
-    int32_t* cnt = nullptr;
-    UVD_CUDA_TRY(cudaMallocAsync((void**)&idx, k * sizeof(int32_t), st));
-    UVD_CUDA_TRY(cudaMallocAsync((void**)&val, k * sizeof(double), st));
-    UVD_CUDA_TRY(cudaMallocAsync((void**)&cnt, sizeof(int32_t), st));
+    char* sp = (char*)flu_scratch((size_t)k * 16 + 256, st);
+    if (!sp) { set_error("uvd_fluence: out of device memory"); return UVD_ERR_NOMEM; }
+    double* val = (double*)sp;
+    int32_t* idx = (int32_t*)(sp + (size_t)k * 8);
+    int32_t* cnt = (int32_t*)(sp + (size_t)k * 12 + 128);
     k_nonzero<<<1, 1024, 0, st>>>(x, k, idx, val, cnt);
     note_launch();
-    int64_t quads = (n + 3) / 4;
-    k_gemv_n<<<(unsigned)((quads + kGemvThreads - 1) / kGemvThreads), kGemvThreads, 0, st>>>(
-        A->values, A->ld, n, idx, val, cnt, out);
+    if (csc) {
+      UVD_CUDA_TRY(cudaMemsetAsync(out, 0, n * sizeof(double), st));
+      k_csc_n<<<(unsigned)std::min<int64_t>(k, 4096), kGemvThreads, 0, st>>>(A->colptr, A->rowidx, A->values,
+                                                                              idx, val, cnt, out);
+    } else {
+      int64_t quads = (n + 3) / 4;
+      k_gemv_n<<<(unsigned)((quads + kGemvThreads - 1) / kGemvThreads), kGemvThreads, 0, st>>>(
+          A->values, A->ld, n, idx, val, cnt, out);
+    }
     note_launch();
     UVD_CUDA_TRY(cudaGetLastError());
-    cudaFreeAsync(idx, st);
-    cudaFreeAsync(val, st);
-    cudaFreeAsync(cnt, st);
   } else {
     if (k == 0) return UVD_OK;
-    k_gemv_t<<<(unsigned)((k + kGemvTCols - 1) / kGemvTCols), kGemvThreads, 0, st>>>(
-        A->values, A->ld, n, k, x, out);
+    if (csc)
+      k_csc_t<<<(unsigned)k, kGemvThreads, 0, st>>>(A->colptr, A->rowidx, A->values, x, out);
+    else
+      k_gemv_t<<<(unsigned)((k + kGemvTCols - 1) / kGemvTCols), kGemvThreads, 0, st>>>(
+          A->values, A->ld, n, k, x, out);
     note_launch();
     UVD_CUDA_TRY(cudaGetLastError());
   }
@@ -204,20 +289,19 @@ extern "C" int uvd_coverage(const uvd_scene* s, const double* mu, double mu_min,
   int dev = 0, sms = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int nb = (int)std::min<int64_t>((s->N + kCovThreads - 1) / kCovThreads, 2 * sms);
+  int nb = (int)std::min<int64_t>((s->N + kCovThreads - 1) / kCovThreads, std::min(2 * sms, kCovBlocksMax));
   nb = std::max(nb, 1);
-  double* part = nullptr;
-  double* dout = nullptr;
-  UVD_CUDA_TRY(cudaMallocAsync((void**)&part, 3 * nb * sizeof(double), st));
-  UVD_CUDA_TRY(cudaMallocAsync((void**)&dout, 3 * sizeof(double), st));
+  double* part = s->cov_part;
+  double* dout = s->cov_part + 3 * kCovBlocksMax;
   k_coverage_part<<<nb, kCovThreads, 0, st>>>(mu, s->area, a_rowsum, s->N, mu_min, part);
   note_launch();
   k_coverage_final<<<1, 32, 0, st>>>(part, nb, dout);
   note_launch();
-  UVD_CUDA_TRY(cudaMemcpyAsync(out, dout, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
-  cudaFreeAsync(part, st);
-  cudaFreeAsync(dout, st);
+  double* h = (double*)host_stage();
+  if (!h) { set_error("uvd_coverage: out of pinned host memory"); return UVD_ERR_NOMEM; }
+  UVD_CUDA_TRY(cudaMemcpyAsync(h, dout, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
   UVD_CUDA_TRY(cudaStreamSynchronize(st));
   UVD_CUDA_TRY(cudaGetLastError());
+  out[0] = h[0]; out[1] = h[1]; out[2] = h[2];
   return UVD_OK;
 }

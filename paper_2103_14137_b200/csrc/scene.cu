@@ -31,6 +31,15 @@ void set_error(const char* fmt, ...) {
 void clear_error() { g_err[0] = 0; }
 
 static std::atomic<unsigned long long> g_launches{0};
+
+void* host_stage() {
+  static thread_local void* p = nullptr;
+  if (!p && cudaMallocHost(&p, 64) != cudaSuccess) {
+    cudaGetLastError();
+    p = nullptr;
+  }
+  return p;
+}
 void note_launch(int n) { g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
 
 void* Alloc::get(size_t bytes) {
@@ -402,8 +411,8 @@ static void free_scene(uvd_scene* s) {
   if (!s) return;
   Alloc& al = s->alloc;
   for (void* p : {(void*)s->centroid, (void*)s->normal, (void*)s->area, (void*)s->orig_id,
-                  (void*)s->tri, (void*)s->nodes, (void*)s->nodes4, (void*)s->walls, (void*)s->poly_xy,
-                  (void*)s->poly_off, (void*)s->err_flag})
+                  (void*)s->tri, (void*)s->nodes, (void*)s->walls, (void*)s->poly_xy,
+                  (void*)s->poly_off, (void*)s->err_flag, (void*)s->cov_part})
     al.put(p);
   cudaStreamSynchronize(al.stream);
   delete s;
@@ -433,6 +442,13 @@ extern "C" int uvd_scene_create(const uvd_scene_desc* desc, int device, void* st
   }
   cudaStream_t st = (cudaStream_t)stream;
   int rc = desc->kind == UVD_SCENE_TRIMESH ? create_trimesh(s, desc, st) : create_extruded(s, desc, st);
+  if (rc == UVD_OK) {
+    s->cov_part = (double*)s->alloc.get((3 * kCovBlocksMax + 3) * sizeof(double));
+    if (!s->cov_part || !host_stage()) {
+      set_error("scene: out of memory (scratch)");
+      rc = UVD_ERR_NOMEM;
+    }
+  }
   if (rc == UVD_OK) {
     s->err_flag = (int*)s->alloc.get(sizeof(int));
     double* dsum = (double*)s->alloc.get(sizeof(double));
@@ -487,10 +503,11 @@ extern "C" int uvd_sync_status(const uvd_scene* s, void* stream) {
   clear_error();
   if (!s) { set_error("uvd_sync_status: null scene"); return UVD_ERR_INVALID; }
   cudaStream_t st = (cudaStream_t)stream;
-  int flag = 0;
-  UVD_CUDA_TRY(cudaMemcpyAsync(&flag, s->err_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  int* hflag = (int*)host_stage();
+  UVD_CUDA_TRY(cudaMemcpyAsync(hflag, s->err_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
   UVD_CUDA_TRY(cudaStreamSynchronize(st));
   UVD_CUDA_TRY(cudaGetLastError());
+  const int flag = *hflag;
   if (flag) {
     UVD_CUDA_TRY(cudaMemsetAsync(s->err_flag, 0, sizeof(int), st));
     set_error("lamp–centroid distance below 1e-9 m (S:160)");

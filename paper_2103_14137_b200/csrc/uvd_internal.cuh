@@ -45,7 +45,7 @@ constexpr double kParallel = 1e-12;   // |det| <= 1e-12 |D||E1xE2| -> no crossin
 #define UVD_LEAF_MAX 2
 #endif
 constexpr int kLeafMax = UVD_LEAF_MAX;  // triangles per BVH leaf (subtree collapse), <= 8
-constexpr int kStackDepth = 128;      // per-warp traversal stack entries
+constexpr int kCovBlocksMax = 1024;   // coverage partial sums (fixed, deterministic order)
 // Q20 free-space test direction (tilted off the axes).
 constexpr double kFreeDirX = 0.0123, kFreeDirY = 0.0371, kFreeDirZ = 1.0;
 
@@ -63,16 +63,6 @@ struct __align__(16) Node {
   float4 b;  // child1 lo.x hi.x lo.y hi.y
   float4 c;  // child0 lo.z hi.z, child1 lo.z hi.z
   uint4 d;   // child0 ref, child1 ref, (unused), (unused)
-};
-
-// BVH4 node (128 B = one L2 line), child-major: child k occupies c[2k] =
-// (lo.x, lo.y, lo.z, ref bits) and c[2k+1] = (hi.x, hi.y, hi.z, 0), so lane
-// (·, k) of a warp loads exactly its child's 32 B.  An unused slot has
-// ref = kEmptyRef and a point box at +1e30 that no segment with t in [0,1]
-// can reach.
-constexpr uint32_t kEmptyRef = 0xffffffffu;
-struct __align__(16) Node4 {
-  float4 c[8];
 };
 
 // ------------------------------------------------------------------ memory --
@@ -109,10 +99,8 @@ struct uvd_scene {
   int64_t* orig_id = nullptr; // N
   // BVH (device)
   float4* tri = nullptr;      // M*3: (v0, owner patch), (v1, orig tri), (v2, 0)  leaf order
-  uvd::Node* nodes = nullptr; // max(M-1, 1)   BVH2 (vantage queries)
+  uvd::Node* nodes = nullptr; // max(M-1, 1) BVH2 nodes
   uint32_t root = 0;          // root ref
-  uvd::Node4* nodes4 = nullptr;  // BVH4 collapsed from the BVH2 (assembly)
-  int64_t n_nodes4 = 0;
   // 2.5D description (device + host copies) for the floorplan vantage test
   uvd::Wall* walls = nullptr;  // device
   int64_t n_walls = 0;
@@ -124,9 +112,14 @@ struct uvd_scene {
   float wall_height = 0.f;
   // in-kernel error flag (device int)
   int* err_flag = nullptr;
+  // small preallocated scratch: coverage partials (device)
+  double* cov_part = nullptr;  // 3 * kCovBlocksMax + 3 doubles
 };
 
 namespace uvd {
+// per-thread pinned staging buffer (64 B, allocated once, never freed) for the
+// scalars synchronising calls return: no allocation on the critical path
+void* host_stage();
 // launchers implemented in the .cu files
 int build_bvh(uvd_scene* s, float4* tri_in, uint32_t** order_out, cudaStream_t st);
 int sort_pairs_u64(uint64_t* keys, uint32_t* vals, int64_t n, Alloc& al, cudaStream_t st);

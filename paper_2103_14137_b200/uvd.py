@@ -296,6 +296,52 @@ class Scene:
         res["_desc"] = m
         return res
 
+    def irradiance_csc(self, lamps: torch.Tensor, cols=None, power_w: float = 80.0,
+                       nnz_cap: int | None = None, vis_bits: bool = False, col_sumsq: bool = False,
+                       stream=None) -> dict:
+        """uvd_irradiance_matrix with CSC output (nonzero entries only).  With
+        nnz_cap=None the call is made twice (size, then fill).  Returns
+        dict(colptr (n_cols+1,) int64, rowidx (nnz,) int32, values (nnz,) fp32, nnz, ...)."""
+        assert lamps.is_cuda and lamps.dtype == torch.float32 and lamps.is_contiguous()
+        K, L = lamps.shape[0], lamps.shape[1]
+        ccols = None if cols is None else np.ascontiguousarray(cols, np.int64)
+        n_cols = K if ccols is None else len(ccols)
+        dev = lamps.device
+        colptr = torch.empty(n_cols + 1, dtype=torch.int64, device=dev)
+        res = dict(colptr=colptr)
+        m = _MatrixOut()
+        m.format = CSC
+        m.colptr = colptr.data_ptr()
+        if vis_bits:
+            vb = torch.empty((n_cols, L, (self.N + 31) // 32), dtype=torch.int32, device=dev)
+            m.vis_bits = vb.data_ptr()
+            res["vis_bits"] = vb
+        lamp = _Lamp(float(power_w), int(L))
+        cptr = ccols.ctypes.data_as(C.c_void_p) if ccols is not None else None
+        cap = 0 if nnz_cap is None else int(nnz_cap)
+        for _attempt in range(2 if nnz_cap is None else 1):
+            rowidx = torch.empty(max(cap, 1), dtype=torch.int32, device=dev)
+            values = torch.empty(max(cap, 1), dtype=torch.float32, device=dev)
+            m.nnz_cap = cap
+            m.rowidx = rowidx.data_ptr() if cap else 0
+            m.values = values.data_ptr() if cap else 0
+            cs = None
+            if col_sumsq and cap:
+                cs = torch.empty(n_cols, dtype=torch.float64, device=dev)
+                m.col_sumsq = cs.data_ptr()
+            rc = lib().uvd_irradiance_matrix(self.handle, _ptr(lamps), K, cptr, n_cols, C.byref(lamp),
+                                             C.byref(m), _stream(stream))
+            if rc == UVD_ERR_CAPACITY and nnz_cap is None:
+                cap = int(colptr[-1].item())
+                continue
+            _check(rc)
+            nnz = int(colptr[-1].item())
+            res.update(rowidx=rowidx[:nnz], values=values[:nnz], nnz=nnz, _desc=m)
+            if cs is not None:
+                res["col_sumsq"] = cs
+            return res
+        raise UvdError(UVD_ERR_CAPACITY, "CSC capacity negotiation failed")
+
     def sync_status(self, stream=None):
         _check(lib().uvd_sync_status(self.handle, _stream(stream)))
 
@@ -323,6 +369,23 @@ def fluence(A: torch.Tensor, n: int, x: torch.Tensor, transpose: bool = False,
     if out is None:
         out = torch.empty(k if transpose else n, dtype=torch.float64, device=A.device)
     m = _dense_desc(A)
+    _check(lib().uvd_fluence(C.byref(m), n, k, int(bool(transpose)), _ptr(x), _ptr(out), _stream(stream)))
+    return out
+
+
+def fluence_csc(csc: dict, n: int, x: torch.Tensor, transpose: bool = False,
+                out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """uvd_fluence on a CSC matrix from Scene.irradiance_csc."""
+    k = csc["colptr"].shape[0] - 1
+    assert x.dtype == torch.float64 and x.is_cuda and x.is_contiguous()
+    if out is None:
+        out = torch.empty(k if transpose else n, dtype=torch.float64, device=x.device)
+    m = _MatrixOut()
+    m.format = CSC
+    m.colptr = csc["colptr"].data_ptr()
+    m.rowidx = csc["rowidx"].data_ptr() if csc["nnz"] else csc["colptr"].data_ptr()
+    m.values = csc["values"].data_ptr() if csc["nnz"] else csc["colptr"].data_ptr()
+    m.nnz_cap = csc["nnz"]
     _check(lib().uvd_fluence(C.byref(m), n, k, int(bool(transpose)), _ptr(x), _ptr(out), _stream(stream)))
     return out
 

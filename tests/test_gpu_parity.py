@@ -157,6 +157,16 @@ def test_vantage_c4_sampled(uvd):
     _vantage_parity(uvd, sc, configs.FLOAT_OPTS, idx=np.sort(rng.choice(n, 300, replace=False)))
 
 
+@pytest.mark.slow
+def test_vantage_c5_arm_sampled(uvd):
+    """Full-size C5 Armbot sampling (bench workload) on 200 sampled candidates,
+    the reach proxy evaluated against every oracle base."""
+    sc = configs.c5_scene()
+    rng = np.random.default_rng(9)
+    n = len(O.vantage_candidates(sc, configs.ARM_OPTS)["points"])
+    _vantage_parity(uvd, sc, configs.ARM_OPTS, idx=np.sort(rng.choice(n, 200, replace=False)))
+
+
 def test_vantage_empty_and_capacity(uvd):
     sc = uvd.Scene(rooms.empty_room(1.0, 2.0, 0.25))
     with pytest.raises(uvd.UvdError) as e:
@@ -344,6 +354,47 @@ def test_tiny_scenes(uvd):
     orig = p["orig_id"].cpu().numpy()
     A = r2["A"][0, :2].cpu().numpy()
     assert A[list(orig).index(0)] == 0.0      # blocked by the cover 1 mm above
+
+
+# ------------------------------------------------------------------- CSC ---
+@pytest.mark.parametrize("case", ["c2", "ward", "tower"])
+def test_csc_matches_dense(uvd, case):
+    """a6 "dense or CSC by visibility": identical nonzero pattern and values,
+    col_sumsq (‖A‖_F) consistent, CSC fluence = dense fluence."""
+    if case == "c2":
+        desc, opts = configs.c2(6)["scene"], configs.DISC_OPTS
+    elif case == "ward":
+        desc, opts = ward.ward(seed=4, n_bays=1, e=0.15), configs.vopts(configs.FLOAT3D, 0.5, 0.05)
+    else:
+        desc, opts = ward.ward(seed=6, n_bays=1, e=0.2), dict(configs.TOWER_OPTS, spacing=0.5)
+    sc = uvd.Scene(desc)
+    lamps, _ = sc.vantage(opts)
+    K = lamps.shape[0]
+    cols = list(range(0, K, 3))
+    dense = sc.irradiance(lamps, cols=cols, vis_bits=True, col_sumsq=True)
+    csc = sc.irradiance_csc(lamps, cols=cols, vis_bits=True, col_sumsq=True)
+    assert torch.equal(dense["vis_bits"], csc["vis_bits"])
+    D = dense["A"][:, :sc.N].cpu().numpy()
+    colptr = csc["colptr"].cpu().numpy()
+    rows = csc["rowidx"].cpu().numpy()
+    vals = csc["values"].cpu().numpy()
+    assert colptr[-1] == csc["nnz"] == np.count_nonzero(D)
+    for c in range(len(cols)):
+        r = rows[colptr[c]:colptr[c + 1]]
+        assert np.array_equal(r, np.nonzero(D[c])[0])
+        assert np.allclose(vals[colptr[c]:colptr[c + 1]], D[c, r], rtol=1e-7, atol=0)
+    assert np.allclose(csc["col_sumsq"].cpu().numpy(), dense["col_sumsq"].cpu().numpy(), rtol=1e-6)
+    assert np.allclose(dense["col_sumsq"].cpu().numpy(), (D.astype(np.float64) ** 2).sum(1), rtol=1e-12)
+    t = torch.from_numpy(vectors.dense_iterate(len(cols), 3)).cuda()
+    y = torch.from_numpy(vectors.row_weights(sc.N, 2)).cuda()
+    assert np.allclose(uvd.fluence_csc(csc, sc.N, t).cpu().numpy(), uvd.fluence(dense["A"], sc.N, t).cpu().numpy(),
+                       rtol=1e-6, atol=1e-12)
+    assert np.allclose(uvd.fluence_csc(csc, sc.N, y, transpose=True).cpu().numpy(),
+                       uvd.fluence(dense["A"], sc.N, y, transpose=True).cpu().numpy(), rtol=1e-6)
+    # two-phase capacity protocol
+    with pytest.raises(uvd.UvdError) as e:
+        sc.irradiance_csc(lamps, cols=cols, nnz_cap=max(1, csc["nnz"] - 1))
+    assert e.value.code == uvd.UVD_ERR_CAPACITY
 
 
 # ------------------------------------------------------------------ a7/a8 ---
