@@ -296,31 +296,51 @@ __global__ void __launch_bounds__(kCscThreads) k_csc_fill(const AsmParams P, con
   }
 }
 
-// Exact (fp64 triangle tests) any-hit walk for one ray, used by k_fixup.
+// Exact any-hit walk for one ray, used by k_fixup: the same fp32 boxes and
+// fp32 triangle filter as the hot kernel, with every undecided triangle
+// re-tested at once in fp64 (no register pressure concern in this kernel).
 __device__ bool lane_clear_exact(const AsmParams& P, float ox, float oy, float oz, float cx, float cy,
                                  float cz, int owner) {
   uint32_t stk[kLaneStack];
   int sp = 0;
+  const float dx = cx - ox, dy = cy - oy, dz = cz - oz;
+  const float ix = safe_inv(dx), iy = safe_inv(dy), iz = safe_inv(dz);
+  const float oix = ox * ix, oiy = oy * iy, oiz = oz * iz;
+  const float nD = fabsf(dx) + fabsf(dy) + fabsf(dz);
+  const float tlo = (float)kSelfEps * rsqrtf(dx * dx + dy * dy + dz * dz);
+  const float thi = 1.0f - tlo;
   const D3 O = d3(ox, oy, oz);
   const D3 D = d3((double)cx - O.x, (double)cy - O.y, (double)cz - O.z);
   const double dd = ddot3(D, D);
   const double t_lo = kSelfEps / sqrt(dd);
-  const Ray32 r32 = make_ray32(ox, oy, oz, (float)D.x, (float)D.y, (float)D.z);
   uint32_t ref = P.root;
   for (;;) {
     if (ref_is_leaf(ref)) {
       const uint32_t st = ref_start(ref), nt = ref_count(ref);
       for (uint32_t k = 0; k < nt; ++k) {
         const float4* t = P.tri + 3 * (int64_t)(st + k);
-        if (__float_as_int(t[0].w) == owner) continue;
-        if (seg_hits_tri(O, D, dd, t_lo, 1.0 - t_lo, t[0], t[1], t[2])) return false;
+        const float4 a = t[0], b = t[1], c = t[2];
+        if (__float_as_int(a.w) == owner) continue;
+        int cls = seg_tri_filter32(ox, oy, oz, dx, dy, dz, nD, tlo, thi, a, b, c);
+        if (cls == 2) cls = seg_hits_tri(O, D, dd, t_lo, 1.0 - t_lo, a, b, c) ? 1 : 0;
+        if (cls == 1) return false;
       }
       if (!sp) return true;
       ref = stk[--sp];
     } else {
       const Node nd = P.nodes[ref];
-      const bool h0 = slab(r32, nd.a.x, nd.a.y, nd.a.z, nd.a.w, nd.c.x, nd.c.y, 1.0f);
-      const bool h1 = slab(r32, nd.b.x, nd.b.y, nd.b.z, nd.b.w, nd.c.z, nd.c.w, 1.0f);
+      const float ax0 = fmaf(nd.a.x, ix, -oix), ax1 = fmaf(nd.a.y, ix, -oix);
+      const float ay0 = fmaf(nd.a.z, iy, -oiy), ay1 = fmaf(nd.a.w, iy, -oiy);
+      const float az0 = fmaf(nd.c.x, iz, -oiz), az1 = fmaf(nd.c.y, iz, -oiz);
+      const float bx0 = fmaf(nd.b.x, ix, -oix), bx1 = fmaf(nd.b.y, ix, -oix);
+      const float by0 = fmaf(nd.b.z, iy, -oiy), by1 = fmaf(nd.b.w, iy, -oiy);
+      const float bz0 = fmaf(nd.c.z, iz, -oiz), bz1 = fmaf(nd.c.w, iz, -oiz);
+      const float an = fmaxf(fmaxf(fminf(ax0, ax1), fminf(ay0, ay1)), fmaxf(fminf(az0, az1), 0.0f));
+      const float af = fminf(fminf(fmaxf(ax0, ax1), fmaxf(ay0, ay1)), fminf(fmaxf(az0, az1), thi));
+      const float bn = fmaxf(fmaxf(fminf(bx0, bx1), fminf(by0, by1)), fmaxf(fminf(bz0, bz1), 0.0f));
+      const float bf = fminf(fminf(fmaxf(bx0, bx1), fmaxf(by0, by1)), fminf(fmaxf(bz0, bz1), thi));
+      const bool h0 = an <= fmaf(af, 1.000002f, 1e-7f);
+      const bool h1 = bn <= fmaf(bf, 1.000002f, 1e-7f);
       if (h0 && h1) {
         ref = nd.d.x;
         if (sp < kLaneStack) stk[sp++] = nd.d.y;

@@ -81,15 +81,18 @@ __device__ __forceinline__ bool seg_hits_tri(D3 O, D3 D, double dd /* D·D */, d
 
 // fp32 filtered segment/triangle test.  Same division-free Möller–Trumbore in
 // fp32 from the exact fp32 vertices and lamp origin, with the fp32-rounded
-// direction; every quantity carries a forward error bound (32 ulp × the 1-norm
-// product of its factors — the rounding of D, T, E1, E2 and of the products
-// are all below that), so each margin is classified as a certain miss (< -err),
-// a certain hit (> +err) or ambiguous.  Returns 0 miss, 1 hit, 2 ambiguous
-// (the caller re-tests those in fp64 with seg_hits_tri).
+// direction.  Forward error bound (u = 2^-24): the inputs D, T = O - V0,
+// E1, E2 carry relative error <= u per component; a cross product component
+// then errs by <= 4u x the sum of its |products|, and a dot product of such a
+// vector with a u-perturbed vector by <= (4u + u + 3u) x the 1-norm product of
+// the three factors, i.e. <= 8u |X|_1 |Y|_1 |Z|_1 for det, U, V and W alike.
+// Each margin is therefore classified with K_ERR = 16u (2x the first-order
+// bound) as a certain miss (< -err), a certain hit (> +err) or undecided.
+// Returns 0 miss, 1 hit, 2 undecided (resolved in fp64 by the caller).
 __device__ __forceinline__ int seg_tri_filter32(float ox, float oy, float oz, float dx, float dy,
                                                 float dz, float nD, float t_lo, float t_hi,
                                                 float4 a, float4 b, float4 c) {
-  const float k = 32.0f * 5.9604645e-08f;
+  const float k = 16.0f * 5.9604645e-08f;
   float e1x = b.x - a.x, e1y = b.y - a.y, e1z = b.z - a.z;
   float e2x = c.x - a.x, e2y = c.y - a.y, e2z = c.z - a.z;
   float tx = ox - a.x, ty = oy - a.y, tz = oz - a.z;
