@@ -33,4 +33,4 @@ for r in range(reps):
           f"= {len(cols) * sc.N / e0.elapsed_time(e1) / 1e6:.3f} G entries/s")
 sc.sync_status()
 r = sc.irradiance(lamps, cols=cols, out=A, counters=True)
-print("counters (rays, box tests, tri tests, node fetches, fp64 fixups, -):", r["counters"].tolist())
+print("counters (rays, box tests, tri tests, node fetches, fp64 fixups, cache hits):", r["counters"].tolist())
