@@ -331,8 +331,15 @@ def main():
     pairs = float(N) * K * L
     flops = FLOP_PER_PAIR * pairs + FLOP_PER_RAY * cnt[0] + FLOP_PER_BOX * cnt[1] + FLOP_PER_TRI * cnt[2]
     achieved = flops / ws / (k_ms / 1e3) / 1e12
+    traffic, traffic_note = None, None
+    tfile = os.path.join(ROOT, "profiles", "ncu_traffic_r01.json")
+    if os.path.exists(tfile) and args.workload == "C5":
+        tr = json.load(open(tfile))
+        traffic = tr["bytes_per_col"] * K  # per launch: all columns of the step
+        traffic_note = (f"DRAM read+write of {tr['capture']} ({tr['cols']}-column launch), scaled per column "
+                        f"to this {K}-column launch")
     roofline = {"bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
-                "frac": achieved / FP32_PEAK_TFLOPS, "traffic": None,
+                "frac": achieved / FP32_PEAK_TFLOPS, "traffic": traffic, "traffic_note": traffic_note,
                 "kernel": "k_assemble", "kernel_ms": k_ms,
                 "kernel_share": k_ms / ms_step,
                 "rays_per_s": cnt[0] / (k_ms / 1e3),
