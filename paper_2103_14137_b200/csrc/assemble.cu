@@ -455,6 +455,10 @@ extern "C" int uvd_irradiance_matrix(const uvd_scene* s, const float* lamp_xyz, 
     set_error("uvd_irradiance_matrix: unknown format %d", out->format);
     return UVD_ERR_INVALID;
   }
+  if (n_cols == 0) {
+    if (csc && out->colptr) UVD_CUDA_TRY(cudaMemsetAsync(out->colptr, 0, sizeof(int64_t), (cudaStream_t)stream));
+    return UVD_OK;
+  }
   if (!csc && (!out->values || out->ld < s->N || out->ld % 32 != 0)) {
     set_error("uvd_irradiance_matrix: dense output needs values and ld >= N, ld %% 32 == 0");
     return UVD_ERR_INVALID;
@@ -462,10 +466,6 @@ extern "C" int uvd_irradiance_matrix(const uvd_scene* s, const float* lamp_xyz, 
   if (csc && (!out->colptr || out->nnz_cap < 0 || (out->nnz_cap > 0 && (!out->rowidx || !out->values)))) {
     set_error("uvd_irradiance_matrix: CSC output needs colptr (and rowidx/values when nnz_cap > 0)");
     return UVD_ERR_INVALID;
-  }
-  if (n_cols == 0) {
-    if (csc) UVD_CUDA_TRY(cudaMemsetAsync(out->colptr, 0, sizeof(int64_t), (cudaStream_t)stream));
-    return UVD_OK;
   }
   cudaStream_t st = (cudaStream_t)stream;
   Alloc al = s->alloc;

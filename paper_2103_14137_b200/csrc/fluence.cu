@@ -232,7 +232,14 @@ static void* flu_scratch(size_t bytes, cudaStream_t st) {
 extern "C" int uvd_fluence(const uvd_matrix_out* A, int64_t n, int64_t k, int transpose,
                            const double* x, double* out, void* stream) {
   clear_error();
-  if (!A || !x || !out || n < 0 || k < 0) { set_error("uvd_fluence: bad argument"); return UVD_ERR_INVALID; }
+  if (!A || !out || n < 0 || k < 0) { set_error("uvd_fluence: bad argument"); return UVD_ERR_INVALID; }
+  cudaStream_t st0 = (cudaStream_t)stream;
+  if (n == 0) return UVD_OK;
+  if (k == 0) {  // empty shard: μ = 0, g is empty
+    if (!transpose) UVD_CUDA_TRY(cudaMemsetAsync(out, 0, n * sizeof(double), st0));
+    return UVD_OK;
+  }
+  if (!x) { set_error("uvd_fluence: null x"); return UVD_ERR_INVALID; }
   const bool csc = A->format == UVD_CSC;
   if (csc) {
     if (!A->colptr || !A->rowidx || !A->values) {
