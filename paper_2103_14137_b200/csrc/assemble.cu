@@ -356,39 +356,72 @@ __device__ bool lane_clear_exact(const AsmParams& P, float ox, float oy, float o
 }
 
 // Re-trace, with exact fp64 triangle tests, every entry flagged by
-// k_assemble_lane and rewrite its value and visibility bits.
-__global__ void k_fixup(AsmParams P) {
+// k_assemble_lane and rewrite its value and visibility bits.  The flagged
+// entries (~1e-3 of all) are first compacted into a list (warp-aggregated
+// atomics) so the re-trace runs with full warps; entries beyond the list's
+// capacity are re-traced in place by the collecting thread.
+__device__ void fixup_entry(const AsmParams& P, int64_t c, int r) {
+  const int64_t j = P.cols ? P.cols[c] : c;
+  const int64_t word = r >> 5;
+  const int b = r & 31;
+  const float cx = P.centroid[3 * r], cy = P.centroid[3 * r + 1], cz = P.centroid[3 * r + 2];
+  const float nx = P.normal[3 * r], ny = P.normal[3 * r + 1], nz = P.normal[3 * r + 2];
+  double acc = 0.0;
+  for (int l = 0; l < P.L; ++l) {
+    const float* pl = P.lamps + 3 * (j * P.L + l);
+    const float ox = pl[0], oy = pl[1], oz = pl[2];
+    const D3 D = d3((double)cx - (double)ox, (double)cy - (double)oy, (double)cz - (double)oz);
+    const double dd = ddot3(D, D);
+    const double d = sqrt(dd);
+    const double cosd = -(D.x * (double)nx + D.y * (double)ny + D.z * (double)nz);
+    const bool vis = cosd > 0.0 && d >= kMinDist && lane_clear_exact(P, ox, oy, oz, cx, cy, cz, r);
+    if (vis) acc += cosd / (dd * d);
+    if (P.vis_bits) {
+      uint32_t* vw = P.vis_bits + (c * P.L + l) * P.words + word;
+      if (vis) atomicOr(vw, 1u << b);
+      else atomicAnd(vw, ~(1u << b));
+    }
+  }
+  if (P.values) P.values[c * P.ld + r] = (float)(acc * P.scale);
+}
+
+__global__ void k_fixup_collect(AsmParams P, uint64_t* __restrict__ list, int64_t cap,
+                                unsigned long long* __restrict__ count) {
   const int64_t nwords = P.n_cols * P.words;
-  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nwords;
-       w += (int64_t)gridDim.x * blockDim.x) {
-    uint32_t bits = P.pending[w];
+  const int lane = threadIdx.x & 31;
+  for (int64_t w0 = blockIdx.x * (int64_t)blockDim.x; w0 < nwords; w0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t w = w0 + threadIdx.x;
+    uint32_t bits = w < nwords ? P.pending[w] : 0u;
+    const int n = __popc(bits);
+    int incl = n;  // warp inclusive scan of the counts
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    const int total = __shfl_sync(0xffffffffu, incl, 31);
+    unsigned long long base = 0;
+    if (lane == 31 && total) base = atomicAdd(count, (unsigned long long)total);
+    base = __shfl_sync(0xffffffffu, base, 31);
+    int64_t slot = (int64_t)base + incl - n;
     if (!bits) continue;
     const int64_t c = w / P.words, word = w - c * P.words;
-    const int64_t j = P.cols ? P.cols[c] : c;
     while (bits) {
       const int b = __ffs(bits) - 1;
       bits &= bits - 1;
       const int r = (int)(word * 32 + b);
-      const float cx = P.centroid[3 * r], cy = P.centroid[3 * r + 1], cz = P.centroid[3 * r + 2];
-      const float nx = P.normal[3 * r], ny = P.normal[3 * r + 1], nz = P.normal[3 * r + 2];
-      double acc = 0.0;
-      for (int l = 0; l < P.L; ++l) {
-        const float* pl = P.lamps + 3 * (j * P.L + l);
-        const float ox = pl[0], oy = pl[1], oz = pl[2];
-        const D3 D = d3((double)cx - (double)ox, (double)cy - (double)oy, (double)cz - (double)oz);
-        const double dd = ddot3(D, D);
-        const double d = sqrt(dd);
-        const double cosd = -(D.x * (double)nx + D.y * (double)ny + D.z * (double)nz);
-        const bool vis = cosd > 0.0 && d >= kMinDist && lane_clear_exact(P, ox, oy, oz, cx, cy, cz, r);
-        if (vis) acc += cosd / (dd * d);
-        if (P.vis_bits) {
-          uint32_t* vw = P.vis_bits + (c * P.L + l) * P.words + word;
-          if (vis) atomicOr(vw, 1u << b);
-          else atomicAnd(vw, ~(1u << b));
-        }
-      }
-      if (P.values) P.values[c * P.ld + r] = (float)(acc * P.scale);
+      if (slot < cap) list[slot] = ((uint64_t)c << 32) | (uint32_t)r;
+      else fixup_entry(P, c, r);  // list full: re-trace here
+      ++slot;
     }
+  }
+}
+
+__global__ void k_fixup_run(AsmParams P, const uint64_t* __restrict__ list, int64_t cap,
+                            const unsigned long long* __restrict__ count) {
+  const int64_t n = min((int64_t)*count, cap);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t e = list[i];
+    fixup_entry(P, (int64_t)(e >> 32), (int)(uint32_t)e);
   }
 }
 
@@ -520,9 +553,16 @@ extern "C" int uvd_irradiance_matrix(const uvd_scene* s, const float* lamp_xyz, 
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t nwords = n_cols * P.words;
-    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nwords + 255) / 256, 4 * sms));
-    k_fixup<<<g, 256, 0, st>>>(P);
-    note_launch();
+    const int64_t cap = std::min<int64_t>(nwords * 32, (int64_t)1 << 22);
+    uint64_t* list = (uint64_t*)al.get((size_t)cap * sizeof(uint64_t) + 256);
+    if (!list) { set_error("uvd_irradiance_matrix: out of device memory"); return UVD_ERR_NOMEM; }
+    unsigned long long* count = (unsigned long long*)((char*)list + (size_t)cap * sizeof(uint64_t));
+    UVD_CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(unsigned long long), st));
+    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nwords + 255) / 256, 8 * sms));
+    k_fixup_collect<<<g, 256, 0, st>>>(P, list, cap, count);
+    k_fixup_run<<<4 * sms, 128, 0, st>>>(P, list, cap, count);
+    note_launch(2);
+    al.put(list);
   }
   int rc = UVD_OK;
   if (csc) {
