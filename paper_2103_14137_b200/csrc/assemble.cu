@@ -30,12 +30,18 @@
 
 namespace uvd {
 
-constexpr int kAsmWarps = 8;
+#ifndef UVD_ITEM_ORDER
+#define UVD_ITEM_ORDER 0
+#endif
+#ifndef UVD_ASM_WARPS
+#define UVD_ASM_WARPS 32
+#endif
+constexpr int kAsmWarps = UVD_ASM_WARPS;
 constexpr int kAsmThreads = kAsmWarps * 32;
 #ifndef UVD_ASM_MINB
-#define UVD_ASM_MINB 4
+#define UVD_ASM_MINB 1
 #endif
-constexpr int kAsmMinBlocks = UVD_ASM_MINB;  // <= 64 registers: 32 warps per SM hide node-fetch latency
+constexpr int kAsmMinBlocks = UVD_ASM_MINB;  // 1024-thread blocks x 1 per SM: <= 64 registers, 32 warps per SM
 
 struct AsmParams {
   const float4* __restrict__ tri;
@@ -152,7 +158,13 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmMinBlocks) k_assemble_lane(As
   const int64_t total = P.n_cols * P.tiles;
   for (int64_t item = (int64_t)blockIdx.x * kAsmWarps + warp; item < total;
        item += (int64_t)gridDim.x * kAsmWarps) {
+#if UVD_ITEM_ORDER
+    // column fastest: concurrent warps trace the same 32 patches from adjacent lamps
+    const int64_t tile = item / P.n_cols, c = item - tile * P.n_cols;
+#else
+    // tile fastest: concurrent warps trace adjacent patches from the same lamp
     const int64_t c = item / P.tiles, tile = item - c * P.tiles;
+#endif
     const int64_t j = P.cols ? P.cols[c] : c;
     const int r = (int)(tile * 32 + lane);
     const bool valid = r < P.N;

@@ -20,8 +20,12 @@ wl = bench.workload(name)
 sc = uvd.Scene(wl["scene"])
 lamps, _ = sc.vantage(wl["vantage"])
 K = lamps.shape[0]
-step = max(1, K // n_cols)
-cols = list(range(0, K, step))[:n_cols]
+if os.environ.get("CONTIG"):
+    s0 = K // 3
+    cols = list(range(s0, min(K, s0 + n_cols)))
+else:
+    step = max(1, K // n_cols)
+    cols = list(range(0, K, step))[:n_cols]
 A = torch.empty((len(cols), sc.ld()), dtype=torch.float32, device="cuda")
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 for r in range(reps):
