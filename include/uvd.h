@@ -105,8 +105,9 @@ typedef struct {
  *   2.5D: q_s = fl32(e0 + ((e1-e0)*s)/n_seg) (q_nseg = e1), c = fl32((q_s+q_{s+1})/2, h/2),
  *         n = (-dy,dx)/len for boundary walls (into the room), (dy,-dx)/len for
  *         obstacle walls (out of the obstacle), area = len*h.
- * Patch (row) order: 2.5D = wall order; 3D = LBVH leaf (Morton) order, with
- * orig_id mapping back to the input triangle index.
+ * Patch (row) order: 2.5D = wall order; 3D = BVH leaf (depth-first) order, so
+ * adjacent rows are adjacent leaves, with orig_id mapping back to the input
+ * triangle index.
  * Errors: INVALID (non-finite vertex, index out of range, zero-area triangle,
  * polygon outside bounds / n<3, res<=0, h<=0), NOMEM, CUDA. */
 UVD_API int uvd_scene_create(const uvd_scene_desc* desc, int device, void* stream,

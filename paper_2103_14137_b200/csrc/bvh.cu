@@ -327,6 +327,9 @@ __global__ void k_emit_small(const float4* __restrict__ tri, int64_t n, Node* no
 // internal node, and the surviving clusters are compacted in order.  Yields a
 // tree of markedly better SAH quality than the Karras LBVH (fewer node visits
 // per shadow ray), in the same (left, right, range, box) arrays.
+#ifndef UVD_ROWS_DFS
+#define UVD_ROWS_DFS 1
+#endif
 #ifndef UVD_PLOC_RADIUS
 #define UVD_PLOC_RADIUS 16
 #endif
@@ -519,6 +522,12 @@ __global__ void k_scatter_tri(const float4* __restrict__ in, const int32_t* __re
   out[3 * d + 2] = in[3 * r + 2];
 }
 
+__global__ void k_scatter_u32(const uint32_t* __restrict__ in, const int32_t* __restrict__ pos, int64_t n,
+                              uint32_t* __restrict__ out) {
+  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r < n) out[pos[r]] = in[r];
+}
+
 // 3D scenes: the owner (row) of the triangle at Morton position r is r
 __global__ void k_set_owner(float4* __restrict__ tri, int64_t n) {
   int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -541,7 +550,8 @@ static inline unsigned grid_for(int64_t n, int t) { return (unsigned)((n + t - 1
 // PLOC driver: clusters -> binary tree (left/right/ibox/parents), then DFS
 // leaf order (triangles reordered so every subtree is a contiguous range).
 static int build_ploc(uvd_scene* s, int64_t M, int32_t* left, int32_t* right, int32_t* rf, int32_t* rl,
-                      int32_t* pint, int32_t* pleaf, float* ibox, int* arrive, cudaStream_t st) {
+                      int32_t* pint, int32_t* pleaf, float* ibox, int* arrive, uint32_t* order,
+                      cudaStream_t st) {
   Alloc& al = s->alloc;
   float* cbA = (float*)al.get(M * 6 * sizeof(float));
   float* cbB = (float*)al.get(M * 6 * sizeof(float));
@@ -591,6 +601,16 @@ static int build_ploc(uvd_scene* s, int64_t M, int32_t* left, int32_t* right, in
   k_ploc_finish<<<grid_for(ni, 256), 256, 0, st>>>(left, right, size, first, pos, ni, rf, rl);
   note_launch(5);
   UVD_CUDA_TRY(cudaMemcpyAsync(s->tri, tri2, 3 * M * sizeof(float4), cudaMemcpyDeviceToDevice, st));
+#if UVD_ROWS_DFS
+  if (s->kind == UVD_SCENE_TRIMESH) {
+    // 3D rows follow the BVH leaf (DFS) order: adjacent rows are adjacent leaves
+    uint32_t* ord2 = (uint32_t*)tri2;  // reuse the scratch (>= 4 B per triangle)
+    k_scatter_u32<<<grid_for(M, 256), 256, 0, st>>>(order, pos, M, ord2);
+    k_set_owner<<<grid_for(M, 256), 256, 0, st>>>(s->tri, M);
+    note_launch(2);
+    UVD_CUDA_TRY(cudaMemcpyAsync(order, ord2, M * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+  }
+#endif
   UVD_CUDA_TRY(cudaGetLastError());
   for (void* p : {(void*)cbA, (void*)cbB, (void*)idA, (void*)idB, (void*)nn, (void*)keep, (void*)lead,
                   (void*)ctr, (void*)tri2})
@@ -657,7 +677,7 @@ int build_bvh(uvd_scene* s, float4* tri_in, uint32_t** order_out, cudaStream_t s
       k_refit<<<grid_for(M, 256), 256, 0, st>>>(s->tri, M, left, right, pint, pleaf, ibox, arrive);
       note_launch();
     } else {  // PLOC (default): agglomerative clustering over the Morton order
-      UVD_TRY(build_ploc(s, M, left, right, rf, rl, pint, pleaf, ibox, arrive, st));
+      UVD_TRY(build_ploc(s, M, left, right, rf, rl, pint, pleaf, ibox, arrive, vals, st));
     }
     k_emit<<<grid_for(ni, 256), 256, 0, st>>>(s->tri, M, left, right, rf, rl, ibox, s->nodes, cp);
     note_launch();
