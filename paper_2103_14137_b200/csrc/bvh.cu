@@ -288,22 +288,44 @@ __device__ __forceinline__ void child_info(const float4* __restrict__ tri, const
   }
 }
 
+// depth-first preorder position of every internal node (root 0, left child =
+// parent + 1, right child = parent + 1 + internal nodes of the left subtree), by
+// walking up from the node: a node and its first child share a 128-B line half
+// of the time, and subtrees are contiguous in memory
+__global__ void k_preorder(const int32_t* __restrict__ left, const int32_t* __restrict__ parent_int,
+                           const int32_t* __restrict__ rfirst, const int32_t* __restrict__ rlast,
+                           int64_t n_int, int32_t* __restrict__ pre) {
+  int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (v >= n_int) return;
+  int32_t acc = 0, c = (int32_t)v;
+  while (c != 0) {
+    const int32_t p = parent_int[c];
+    const int32_t l = left[p];
+    acc += 1;
+    if (l != c && l >= 0) acc += rlast[l] - rfirst[l];  // internal nodes of the left subtree
+    c = p;
+  }
+  pre[v] = acc;
+}
+
 __global__ void k_emit(const float4* __restrict__ tri, int64_t n, const int32_t* __restrict__ left,
                        const int32_t* __restrict__ right, const int32_t* __restrict__ rfirst,
                        const int32_t* __restrict__ rlast, const float* __restrict__ ibox,
-                       Node* __restrict__ nodes, float cp) {
+                       const int32_t* __restrict__ pre, Node* __restrict__ nodes, float cp) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n - 1) return;
   Box b0, b1;
   uint32_t r0, r1;
   child_info(tri, ibox, rfirst, rlast, left[i], &b0, &r0);
   child_info(tri, ibox, rfirst, rlast, right[i], &b1, &r1);
+  if (!ref_is_leaf(r0)) r0 = (uint32_t)pre[r0];
+  if (!ref_is_leaf(r1)) r1 = (uint32_t)pre[r1];
   Node nd;
   nd.a = make_float4(pad_lo(b0.lx, cp), pad_hi(b0.hx, cp), pad_lo(b0.ly, cp), pad_hi(b0.hy, cp));
   nd.b = make_float4(pad_lo(b1.lx, cp), pad_hi(b1.hx, cp), pad_lo(b1.ly, cp), pad_hi(b1.hy, cp));
   nd.c = make_float4(pad_lo(b0.lz, cp), pad_hi(b0.hz, cp), pad_lo(b1.lz, cp), pad_hi(b1.hz, cp));
   nd.d = make_uint4(r0, r1, 0u, 0u);
-  nodes[i] = nd;
+  nodes[pre[i]] = nd;
 }
 
 // single-leaf scene (M <= kLeafMax): a root node with one leaf child and an
@@ -679,7 +701,10 @@ int build_bvh(uvd_scene* s, float4* tri_in, uint32_t** order_out, cudaStream_t s
     } else {  // PLOC (default): agglomerative clustering over the Morton order
       UVD_TRY(build_ploc(s, M, left, right, rf, rl, pint, pleaf, ibox, arrive, vals, st));
     }
-    k_emit<<<grid_for(ni, 256), 256, 0, st>>>(s->tri, M, left, right, rf, rl, ibox, s->nodes, cp);
+    int32_t* pre = (int32_t*)arrive;  // arrival counters are free again
+    k_preorder<<<grid_for(ni, 256), 256, 0, st>>>(left, pint, rf, rl, ni, pre);
+    note_launch();
+    k_emit<<<grid_for(ni, 256), 256, 0, st>>>(s->tri, M, left, right, rf, rl, ibox, pre, s->nodes, cp);
     note_launch();
     s->root = 0;
     for (void* p : {(void*)left, (void*)right, (void*)rf, (void*)rl, (void*)pint, (void*)pleaf,
