@@ -218,9 +218,16 @@ def main():
     import torch.distributed as dist
 
     ws, rank, local = dist_env()
+    # one process per GPU; BENCH_BACKEND=gloo + fewer GPUs than ranks is only a
+    # functional dry run of the multi-rank path (ranks then share a device)
+    backend = os.environ.get("BENCH_BACKEND", "nccl")
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     if ws > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     import __graft_entry__
     if rank == 0:
         __graft_entry__.build()
