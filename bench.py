@@ -321,8 +321,12 @@ def main():
     ms_total = e0.elapsed_time(e1)
     n_launch = uvd.launch_count() - n_launch0
     clk = clocks.stop()
-    k_ms = float(np.mean([a.elapsed_time(b) for a, b in zip(ev_k0, ev_k1)]))
-    ms_total, k_ms = shard.max_over_ranks([ms_total, k_ms], device=dev)
+    k_each = [a.elapsed_time(b) for a, b in zip(ev_k0, ev_k1)]
+    k_ms = float(np.mean(k_each))
+    k_sum = float(shard.sum_over_ranks([k_ms], device=dev)[0])
+    ms_total, k_ms, k_med, k_best = shard.max_over_ranks(
+        [ms_total, k_ms, float(np.median(k_each)), float(np.min(k_each))], device=dev)
+    imbalance = k_ms / (k_sum / ws)  # slowest rank's assembly time over the mean
     ms_step = ms_total / args.steps
     value = N * K / (ms_step / 1e3)
     phases = {nm: float(np.mean([e[k].elapsed_time(e[k + 1]) for e in ev_ph]))
@@ -347,7 +351,8 @@ def main():
                         f"to this {K}-column launch")
     roofline = {"bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": achieved / FP32_PEAK_TFLOPS, "traffic": traffic, "traffic_note": traffic_note,
-                "kernel": "k_assemble", "kernel_ms": k_ms,
+                "kernel": "k_assemble", "kernel_ms": k_ms, "kernel_ms_median": k_med,
+                "kernel_ms_best": k_best, "imbalance": imbalance,
                 "kernel_share": k_ms / ms_step,
                 "rays_per_s": cnt[0] / (k_ms / 1e3),
                 "per_launch": {"rays": cnt[0], "box_tests": cnt[1], "tri_tests": cnt[2],
