@@ -67,6 +67,23 @@ class _MatrixOut(C.Structure):
                 ("vis_bits", C.c_void_p), ("col_sumsq", C.c_void_p), ("counters", C.c_void_p)]
 
 
+_ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p)
+
+
+class _LpOpts(C.Structure):
+    _fields_ = [("mu_min", C.c_double), ("t_max", C.c_double), ("penalty", C.c_void_p),
+                ("penalty_scalar", C.c_double), ("eps", C.c_double), ("max_iter", C.c_int64),
+                ("check_every", C.c_int32), ("use_graph", C.c_int32), ("primal_weight", C.c_double),
+                ("allreduce", _ALLREDUCE_FN), ("allreduce_ctx", C.c_void_p)]
+
+
+class _LpResult(C.Structure):
+    _fields_ = [("status", C.c_int32), ("restarts", C.c_int32), ("iterations", C.c_int64),
+                ("primal_obj", C.c_double), ("dual_obj", C.c_double), ("rel_primal_res", C.c_double),
+                ("rel_dual_res", C.c_double), ("rel_gap", C.c_double), ("sum_t", C.c_double),
+                ("primal_weight", C.c_double), ("averaged", C.c_int32)]
+
+
 _lib = None
 
 
@@ -94,6 +111,8 @@ def lib():
                                   C.c_void_p, C.c_void_p]
         L.uvd_coverage.argtypes = [C.c_void_p, C.c_void_p, C.c_double, C.c_void_p,
                                    C.POINTER(C.c_double), C.c_void_p]
+        L.uvd_lp_solve.argtypes = [C.POINTER(_MatrixOut), C.c_int64, C.c_int64, C.POINTER(_LpOpts),
+                                   C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(_LpResult), C.c_void_p]
         L.uvd_last_error.restype = C.c_char_p
         L.uvd_version.restype = C.c_int
         L.uvd_launch_count.restype = C.c_ulonglong
@@ -103,7 +122,7 @@ def lib():
 
 EXPORTS = ("uvd_scene_create", "uvd_scene_query", "uvd_scene_patches", "uvd_scene_destroy",
            "uvd_vantage_sample", "uvd_irradiance_matrix", "uvd_sync_status", "uvd_fluence",
-           "uvd_coverage", "uvd_last_error", "uvd_version", "uvd_launch_count")
+           "uvd_coverage", "uvd_lp_solve", "uvd_last_error", "uvd_version", "uvd_launch_count")
 
 
 def _check(rc):
@@ -397,3 +416,72 @@ def version() -> int:
 def launch_count() -> int:
     """Kernels libuvd has launched in this process (uvd_launch_count)."""
     return int(lib().uvd_launch_count())
+
+
+class _DevView:
+    """Zero-copy view of a device fp64 buffer (for the allreduce callback)."""
+
+    def __init__(self, ptr, count):
+        self.__cuda_array_interface__ = {"shape": (int(count),), "typestr": "<f8", "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+def lp_solve(A, n: int, mu_min: float = 280.0, t_max: float = 1800.0, penalty=None, t0=None,
+             eps: float = 1e-6, max_iter: int = 200000, check_every: int = 64, use_graph: bool = True,
+             primal_weight: float = 0.0, distributed: bool = False, stream=None) -> dict:
+    """uvd_lp_solve: the relaxed dwell-time LP of Eq. 9 on this
+    process's column shard of A (dense (k, ld) tensor, or a CSC dict from
+    Scene.irradiance_csc).  penalty: float (every patch) or (n,) fp64 CUDA
+    tensor; None = 10·‖A‖_F is the caller's job (pass it).  distributed: sum the
+    per-iteration partials across torch.distributed ranks (columns sharded)."""
+    if isinstance(A, dict):
+        m = _MatrixOut()
+        m.format = CSC
+        m.colptr = A["colptr"].data_ptr()
+        m.rowidx = A["rowidx"].data_ptr() if A["nnz"] else A["colptr"].data_ptr()
+        m.values = A["values"].data_ptr() if A["nnz"] else A["colptr"].data_ptr()
+        m.nnz_cap = A["nnz"]
+        k = A["colptr"].shape[0] - 1
+        dev = A["colptr"].device
+    else:
+        m = _dense_desc(A)
+        k = A.shape[0]
+        dev = A.device
+    if penalty is None:
+        raise ValueError("lp_solve: pass the penalty (the paper: p_i > ||A||_F, P:274)")
+    o = _LpOpts()
+    o.mu_min, o.t_max, o.eps = float(mu_min), float(t_max), float(eps)
+    if isinstance(penalty, torch.Tensor):
+        assert penalty.dtype == torch.float64 and penalty.is_cuda and penalty.numel() == n
+        o.penalty = penalty.data_ptr()
+    else:
+        o.penalty_scalar = float(penalty)
+    o.max_iter, o.check_every, o.use_graph = int(max_iter), int(check_every), int(bool(use_graph))
+    o.primal_weight = float(primal_weight)
+    cb = None
+    if distributed:
+        import torch.distributed as dist
+
+        def _allreduce(buf, count, strm, ctx):
+            try:
+                s = torch.cuda.ExternalStream(strm) if strm else torch.cuda.current_stream()
+                with torch.cuda.stream(s):
+                    t = torch.as_tensor(_DevView(buf, count), device=dev)
+                    dist.all_reduce(t)
+                return 0
+            except Exception:  # noqa: BLE001 — reported to the C side as a failure code
+                return 1
+        cb = _ALLREDUCE_FN(_allreduce)
+        o.allreduce = cb
+    t = torch.zeros(k, dtype=torch.float64, device=dev) if t0 is None else t0.clone()
+    sigma = torch.empty(n, dtype=torch.float64, device=dev)
+    y = torch.empty(n + 1, dtype=torch.float64, device=dev)
+    r = _LpResult()
+    _check(lib().uvd_lp_solve(C.byref(m), int(n), int(k), C.byref(o), _ptr(t) if k else C.c_void_p(0),
+                              _ptr(sigma), _ptr(y), C.byref(r), _stream(stream)))
+    del cb
+    return {"t": t, "sigma": sigma, "y": y[:n], "y_budget": y[n:], "status": int(r.status),
+            "iterations": int(r.iterations), "restarts": int(r.restarts), "primal_obj": r.primal_obj,
+            "dual_obj": r.dual_obj, "rel_primal_res": r.rel_primal_res, "rel_dual_res": r.rel_dual_res,
+            "rel_gap": r.rel_gap, "sum_t": r.sum_t, "primal_weight": r.primal_weight,
+            "averaged": bool(r.averaged)}

@@ -97,7 +97,7 @@ def test_penalty_above_frobenius_gives_zero_slack(lp, orc):
     c = configs.c1()
     pat = orc.extruded_patches(c["scene"])
     v = orc.vantage(c["scene"], c["vantage"])
-    A = orc.irradiance_matrix(pat, v["samples"][v["feasible"]])["A"].T  # (N, K)
+    A = orc.irradiance_matrix(pat, v["samples"][v["feasible"]])["A"]  # (N, K)
     p = 10.0 * np.linalg.norm(A)
     r = lp.solve(A, 280.0, p, t_max=1e6)
     assert not r["sigma"].any()
