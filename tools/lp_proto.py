@@ -10,7 +10,7 @@ import numpy as np
 
 
 def pdhg(A, mu_min, p, t_max, eps=1e-8, max_iter=200000, M=64, omega=None, eta=0.999, verbose=False,
-         scaled=True):
+         scaled=True, presolve=False):
     n, k = A.shape
     p = np.full(n, p) if np.ndim(p) == 0 else p
     tau = eta / (A.sum(0) + 1.0)
@@ -25,11 +25,16 @@ def pdhg(A, mu_min, p, t_max, eps=1e-8, max_iter=200000, M=64, omega=None, eta=0
         omega = cs / qs if scaled else 1.0
     cn = np.sqrt(k + (p ** 2).sum())
     t = np.zeros(k); s = np.zeros(n); y = np.zeros(n); yb = 0.0
+    if presolve:  # rows no vantage sees: σ_i = μ_min, y_i = p_i are optimal and fixed points
+        z = A.sum(1) == 0
+        s[z] = mu_min
+        y[z] = p[z]
     mu = A @ t; S = t.sum()
     gT = A.T @ y
     avg = None
     m = 0
     t_last, s_last, y_last, yb_last = t.copy(), s.copy(), y.copy(), yb
+    hist = []
 
     def score(t_, s_, y_, yb_, mu_, S_, gT_):
         rp = np.sqrt((np.maximum(0, mu_min - mu_ - s_) ** 2).sum() + max(0, S_ - t_max) ** 2)
@@ -66,13 +71,14 @@ def pdhg(A, mu_min, p, t_max, eps=1e-8, max_iter=200000, M=64, omega=None, eta=0
         it += M
         kc, relc, poc = score(t, s, y, yb, mu, S, gT)
         ka, rela, poa = score(avg[0], avg[2], avg[4], avg[5], avg[3], avg[6], avg[1])
+        hist.append((it, max(relc), max(rela)))
         if verbose and it % (M * 50) == 0:
             print(it, f"omega={omega:.3g}", "cur", ["%.2e" % x for x in relc], "avg", ["%.2e" % x for x in rela],
                   poc, poa)
         if max(relc) <= eps:
-            return dict(t=t, obj=poc, it=it, restarts=restarts, omega=omega)
+            return dict(t=t, obj=poc, it=it, restarts=restarts, omega=omega, hist=hist)
         if max(rela) <= eps:
-            return dict(t=avg[0], obj=poa, it=it, restarts=restarts, omega=omega)
+            return dict(t=avg[0], obj=poa, it=it, restarts=restarts, omega=omega, hist=hist)
         avg_better = ka < kc
         cand = min(ka, kc)
         do = cand <= 0.2 * kkt_restart or (cand <= 0.8 * kkt_restart and cand > prev) or (it - it_r) >= 0.36 * it
@@ -93,7 +99,7 @@ def pdhg(A, mu_min, p, t_max, eps=1e-8, max_iter=200000, M=64, omega=None, eta=0
             m = 0
             avg = None
             restarts += 1
-    return dict(t=t, obj=None, it=it, restarts=restarts, omega=omega)
+    return dict(t=t, obj=None, it=it, restarts=restarts, omega=omega, hist=hist)
 
 
 if __name__ == "__main__":
