@@ -246,13 +246,14 @@ UVD_API int uvd_coverage(const uvd_scene* scene, const double* mu, double mu_min
  *   minimise Σ_k t_k + Σ_i p_i σ_i
  *   s.t.     (A·t)_i + σ_i ≥ μ_min  (every patch i),   Σ_k t_k ≤ T_max,   t, σ ≥ 0
  * and its dual  maximise μ_min Σ_i y_i − T_max y_b  s.t.  (Aᵀy)_k − y_b ≤ 1,
- * y_i ≤ p_i, y ≥ 0.  Solved by PDHG (primal–dual hybrid gradient, Chambolle &
- * Pock 2011) with their diagonal preconditioning (α = 1), PDLP-style adaptive
- * restarts to the iterate average and primal-weight updates; every iteration
- * is one Aᵀ·y and one A·t (uvd_fluence kernels, zero-t columns skipped) plus
- * two fused fp64 vector kernels.  The paper used Gurobi's interior-point
- * method; any optimal (t, σ) is acceptable (the optimum need not be
- * unique, Q17): the solver's contract is the KKT tolerance below.
+ * y_i ≤ p_i, y ≥ 0.  Solved by reflected restarted Halpern PDHG (Lu & Yang
+ * 2024) with Chambolle–Pock diagonal preconditioning (α = 1): the coverage
+ * rows are dualised, the budget is kept as a set (exact weighted projection
+ * onto {t ≥ 0, Σt ≤ T_max}); every iteration is one A·t and one Aᵀ·y
+ * (uvd_fluence kernels, zero-t columns skipped) plus fused fp64 vector
+ * kernels.  The paper used Gurobi's interior-point method; any optimal
+ * (t, σ) is acceptable (the optimum need not be unique, Q17): the solver's
+ * contract is the KKT tolerance below.
  *
  * A: this process's column shard (dense or CSC, as filled by
  *    uvd_irradiance_matrix), n patches, k local columns.  A ≥ 0 is assumed
@@ -260,15 +261,16 @@ UVD_API int uvd_coverage(const uvd_scene* scene, const double* mu, double mu_min
  * t: DEVICE [k] fp64, in: initial dwell times (zeros are fine), out: solution.
  * sigma: DEVICE [n] fp64 out (slacks σ).  y: DEVICE [n+1] fp64 out (duals of
  *    the n coverage rows, then of the budget row).
- * Multi-GPU (columns sharded): set `allreduce` to a function that sums
- *    `count` fp64 values at the DEVICE pointer `buf` in place across ranks
- *    (enqueued on or synchronised with `stream`); the library calls it once per
- *    iteration (N+1 values: partial A·t and Σt) and at convergence checks.
+ * Multi-GPU (columns sharded): set `allreduce` to a function that
+ *    reduces `count` fp64 values at the DEVICE pointer `buf` in place across
+ *    ranks (op 0 = sum, 1 = max), enqueued on or synchronised with `stream`;
+ *    the library calls it once per iteration for the partial A·t (n values), a
+ *    few times per iteration for the budget projection's sums, and at checks.
  *    No CUDA graph is used in that mode.  NULL: single process.
  * Termination (relative KKT, as in PDLP): ‖primal residual‖₂ ≤ eps(1+‖q‖₂),
  *    ‖dual residual‖₂ ≤ eps(1+‖c‖₂), |primal − dual objective| ≤
  *    eps(1+|primal|+|dual|), q = (μ_min 𝟙, −T_max), c = (𝟙, p); checked every
- *    `check_every` iterations on the current iterate and on the average.
+ *    `check_every` iterations on the operator output T(z).
  * Synchronises `stream` at every check.  Deterministic for a given launch
  * sequence (fixed reduction orders; CSC A·t uses fp64 atomics). */
 typedef struct {
@@ -280,8 +282,8 @@ typedef struct {
   int64_t max_iter;       /* 0 → 200000 */
   int32_t check_every;    /* 0 → 64 */
   int32_t use_graph;      /* capture check_every iterations in one CUDA graph (single process, non-NULL stream) */
-  double primal_weight;   /* initial ω; 0 → 1 */
-  int (*allreduce)(double* buf, int64_t count, void* stream, void* ctx);
+  double primal_weight;   /* initial ω; 0 → ‖T^½c‖/‖Σ^½q‖ (PDLP's rule in the preconditioned space) */
+  int (*allreduce)(double* buf, int64_t count, int op, void* stream, void* ctx);
   void* allreduce_ctx;
 } uvd_lp_opts;
 
@@ -294,7 +296,7 @@ typedef struct {
   double rel_primal_res, rel_dual_res, rel_gap;
   double sum_t;           /* Σ_k t_k over all ranks */
   double primal_weight;   /* final ω */
-  int32_t averaged;       /* 1 if the returned point is the restart average */
+  int32_t averaged;       /* reserved (0) */
 } uvd_lp_result;
 
 UVD_API int uvd_lp_solve(const uvd_matrix_out* A, int64_t n, int64_t k, const uvd_lp_opts* opts, double* t,

@@ -1,29 +1,33 @@
 // lp.cu — NEXT-1: the relaxed dwell-time LP of Eq. 9
 // (P:262–272), the first stage of the paper's two-stage planner (§IV-D), solved
-// on the GPU by the primal–dual hybrid gradient method instead of the paper's
-// Gurobi interior point.
+// on the GPU by a first-order primal–dual method instead of the paper's Gurobi
+// interior point.
 //
-//   primal  min cᵀx  s.t. Kx ≥ q, x ≥ 0      x = (t ∈ R^k, σ ∈ R^n)
-//   dual    max qᵀy  s.t. Kᵀy ≤ c, y ≥ 0      y = (y ∈ R^n, y_b)
-//   K = [[A, I], [−𝟙ᵀ, 0]],  c = (𝟙, p),  q = (μ_min 𝟙, −T_max)
+//   minimise Σ_k t_k + Σ_i p_i σ_i  s.t.  A t + σ ≥ μ_min 𝟙,  t ∈ Δ = {t ≥ 0, Σ t ≤ T_max},  σ ≥ 0
 //
-// PDHG (Chambolle & Pock 2011), with their diagonal preconditioners for
-// α = 1 — T_j = η / Σ_i |K_ij|, Σ_i = η / Σ_j |K_ij|, which bound
-// ‖Σ^½ K T^½‖ ≤ η < 1 — and a primal weight ω (steps T/ω, Σω):
-//   x⁺ = max(0, x − (T/ω)(c − Kᵀy))
-//   y⁺ = max(0, y + (Σω)(q − K(2x⁺ − x)))
-// plus PDLP-style adaptive restarts (Applegate et al. 2021): every
-// `check_every` iterations the current iterate and the running average are
-// scored by their ω-weighted KKT error; the better one becomes the restart
-// point on sufficient (×0.2) or stalled necessary (×0.8) decay or after 36 % of
-// the iterations; ω is then updated from the primal and dual movement.
+// Operator: PDHG (Chambolle & Pock 2011) on the saddle problem with the
+// coverage rows dualised (y ≥ 0) and the budget kept as the simple set Δ:
+//   t̂ = Π_Δ^T (t − (T/ω)(𝟙 − Aᵀy))          weighted projection onto Δ
+//   σ̂ = max(0, σ − (η/ω)(p − y))
+//   ŷ = max(0, y + (Σω)(μ_min − 2(A t̂ + σ̂) + (A t + σ)))
+// with Chambolle–Pock's diagonal preconditioners for α = 1 (T_k = η/Σ_i A_ik,
+// Σ_i = η/(Σ_k A_ik + 1), η = 0.999: ‖Σ^½ K T^½‖ < 1) and a primal weight ω.
+// Π_Δ^T is the T⁻¹-weighted projection: t̂_k = max(0, v_k − λ T_k) with λ ≥ 0
+// the root of Σ_k max(0, v_k − λT_k) = T_max (or λ = 0 if the cap is slack),
+// found exactly by Newton's method from the left on this convex piecewise-
+// linear function (finite; Michelot's simplex projection, weighted); ωλ is the
+// budget's dual multiplier y_b.
 //
-// One iteration = Aᵀ·y (k_gemv_t) + A·t⁺ (k_nonzero + k_gemv_n, zero-t columns
-// skipped) + two fused fp64 vector kernels (k_lp_primal: t-update, Σt and the
-// running averages; k_lp_dual: σ- and y-updates, K(2x⁺−x) formed from the
-// stored A·t, and the averages).  Bandwidth: one pass over A for Aᵀ·y plus the
-// nonzero-t columns for A·t; single-process solves replay `check_every`
-// iterations as one CUDA graph.
+// Outer method: reflected restarted Halpern iteration (Lu & Yang 2024):
+//   z⁺ = w ((1+ρ) T(z) − ρ z) + (1 − w) z₀,   w = (k+1)/(k+2),  ρ = 1,
+// restarted (z₀ ← T(z), k ← 0) when the fixed-point residual ‖z − T(z)‖_ω has
+// decayed ×0.2 (sufficient), or ×0.8 and stalled (necessary), or after 36 % of
+// the iterations (artificial); ω is then re-balanced from the primal and dual
+// movement between restart points (PDLP's smoothed rule).  Because A·t and
+// Aᵀ·y are linear, the mixed iterate's products are mixed the same way: every
+// iteration costs one A·t̂ (k_nonzero + k_gemv_n: zero columns of the sparse t̂
+// skipped) and one Aᵀ·ŷ (k_gemv_t) plus three fused fp64 vector kernels.
+// Single-process solves replay `check_every` iterations as one CUDA graph.
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -34,27 +38,31 @@
 
 namespace uvd {
 
-struct LpScal {  // device-resident scalars of the iteration
-  double y2, S, y2_avg, S_avg, y2_last;  // budget dual y_b, Σt (global), their averages, restart anchor
-  double omega;                         // primal weight ω
-  double w;                             // averaging weight of the current iteration, 1/(m+1)
-  double m;                             // iterates averaged since the last restart
+struct HpScal {   // device-resident scalars
+  double omega;   // primal weight ω
+  double w;       // Halpern weight of the current iteration
+  double kc;      // iterations since the last restart
+  double first;   // 1 in the first iteration after a restart
+  double lam;     // budget multiplier λ of the last projection
+  double pad[3];
 };
 
-struct LpVec {
-  double *t, *gT, *t_avg, *gT_avg, *t_last, *tau;                          // [k]
-  double *sig, *y1, *mu, *buf, *sig_avg, *mu_avg, *y_avg, *sig_last, *y_last, *sig1, *pen;  // [n] (buf n+1)
-  LpScal* sc;
-  double* part;      // [kLpBlocks][8] row partials
+struct HpVec {
+  double *t, *gT, *t0, *gT0, *tT, *gTT, *tau;                             // [k]
+  double *sig, *y, *mu, *sig0, *y0, *mu0, *sigT, *yT, *buf, *sig1, *pen;  // [n] (buf: A t̂, n+1)
+  HpScal* sc;
+  double* part;      // [kHpBlocks][8] row partials
+  double* res;       // [kHpBlocks][4] row residual partials: last iteration (0,1), first after restart (2,3)
+  double* cres;      // [8] column residual (0 last, 1 first), projection sums (2..4)
   double* rows_out;  // [8]
-  double* cols_out;  // [4] (summed across ranks)
+  double* cols_out;  // [8]
 };
 
-constexpr int kLpBlocks = 296;  // 2 x 148 SMs: fixed grid -> fixed reduction order
-constexpr int kLpThreads = 256;
+constexpr int kHpBlocks = 296;  // 2 x 148 SMs: fixed grid -> fixed reduction order
+constexpr int kHpThreads = 256;
 
 __device__ __forceinline__ double block_sum(double v, double* sh) {
-  // fixed-order block reduction (blockDim.x a multiple of 32, <= 1024)
+  // fixed-order block reduction (blockDim.x a multiple of 32, <= 1024); result in thread 0
   for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
   __syncthreads();
@@ -63,101 +71,212 @@ __device__ __forceinline__ double block_sum(double v, double* sh) {
   double s = 0.0;
   if (threadIdx.x == 0)
     for (int i = 0; i < nw; ++i) s += sh[i];
-  return s;  // valid in thread 0
+  return s;
 }
 
-// x-update of the t block, running averages of t and of Kᵀy's A-part, Σt⁺.
-__global__ void __launch_bounds__(1024) k_lp_primal(LpVec v, int64_t k, int64_t n) {
-  __shared__ double sh[32];
-  LpScal* s = v.sc;
-  const double m = s->m, w = 1.0 / (m + 1.0), om = s->omega, y2 = s->y2;
-  double acc = 0.0;
+__device__ __forceinline__ double block_max(double v, double* sh) {
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (lane == 0) sh[warp] = v;
+  __syncthreads();
+  double s = -INFINITY;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < nw; ++i) s = fmax(s, sh[i]);
+  return s;
+}
+
+// t̂ = max(0, v − λT) (v stored in t̂), residual Σ(t̂ − t)²/T, Σ t̂, Halpern weight
+__device__ void primal_finish(HpVec& v, int64_t k, int64_t n, double lam, double* sh, HpScal* s, double kc) {
+  double r = 0.0, acc = 0.0;
   for (int64_t j = threadIdx.x; j < k; j += blockDim.x) {
-    const double g = v.gT[j];
-    const double tn = fmax(0.0, v.t[j] - v.tau[j] / om * (1.0 - g + y2));  // c_t − (Kᵀy)_t = 1 − (Aᵀy)_k + y_b
-    v.t_avg[j] += w * (tn - v.t_avg[j]);
-    v.gT_avg[j] += w * (g - v.gT_avg[j]);
-    v.t[j] = tn;
+    const double tn = fmax(0.0, v.tT[j] - lam * v.tau[j]);
+    const double d = tn - v.t[j];
+    r += d * d / v.tau[j];
     acc += tn;
+    v.tT[j] = tn;
   }
+  const double rs = block_sum(r, sh);
   const double tot = block_sum(acc, sh);
   if (threadIdx.x == 0) {
-    v.buf[n] = tot;  // this rank's Σt⁺ (summed across ranks with A·t⁺)
-    s->y2_avg += w * (y2 - s->y2_avg);
-    s->w = w;
-    s->m = m + 1.0;
+    v.cres[0] = rs;
+    if (kc == 0.0) v.cres[1] = rs;
+    v.buf[n] = tot;
+    s->w = (kc + 1.0) / (kc + 2.0);
+    s->first = kc == 0.0 ? 1.0 : 0.0;
+    s->kc = kc + 1.0;
+    s->lam = lam;
   }
 }
 
-// σ-update, y-update from K(2x⁺ − x) = 2(A t⁺ + σ⁺) − (A t + σ), averages.
-__global__ void __launch_bounds__(kLpThreads) k_lp_dual(LpVec v, int64_t n, double mu_min, double t_max,
-                                                       double sig2, double eta) {
-  const LpScal* s = v.sc;
-  const double w = s->w, om = s->omega;
-  for (int64_t i = blockIdx.x * (int64_t)kLpThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kLpThreads) {
-    const double mun = v.buf[i], so = v.sig[i], yo = v.y1[i];
-    const double sn = fmax(0.0, so - eta / om * (v.pen[i] - yo));  // c_σ − (Kᵀy)_σ = p − y
-    const double kxo = v.mu[i] + so, kxn = mun + sn;
-    const double yn = fmax(0.0, yo + om * v.sig1[i] * (mu_min - 2.0 * kxn + kxo));
-    v.sig_avg[i] += w * (sn - v.sig_avg[i]);
-    v.mu_avg[i] += w * (mun - v.mu_avg[i]);
-    v.y_avg[i] += w * (yo - v.y_avg[i]);
-    v.mu[i] = mun;
-    v.sig[i] = sn;
-    v.y1[i] = yn;
-  }
-  if (blockIdx.x == 0 && threadIdx.x == 0) {
-    LpScal* sw = v.sc;
-    const double Sn = v.buf[n];
-    const double y2n = fmax(0.0, sw->y2 + om * sig2 * (2.0 * Sn - sw->S - t_max));  // row −Σt ≥ −T_max
-    sw->S_avg += w * (Sn - sw->S_avg);
-    sw->S = Sn;
-    sw->y2 = y2n;
-  }
-}
-
-// KKT pieces over the rows for the current iterate and the average:
-// Σ max(0, μ_min − μ − σ)², Σ max(0, y − p)², Σ p σ, Σ y.
-__global__ void __launch_bounds__(kLpThreads) k_lp_kkt_rows(LpVec v, int64_t n, double mu_min) {
+// t-part of T(z), single process: v = t − (T/ω)(1 − Aᵀy), projection onto Δ
+// inside the block (Newton from the left), then primal_finish
+__global__ void __launch_bounds__(1024) k_hp_primal(HpVec v, int64_t k, int64_t n, double cap) {
   __shared__ double sh[32];
-  double a[8] = {0, 0, 0, 0, 0, 0, 0, 0};
-  for (int64_t i = blockIdx.x * (int64_t)kLpThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kLpThreads) {
-    const double p = v.pen[i];
-    double r = fmax(0.0, mu_min - v.mu[i] - v.sig[i]);
-    double d = fmax(0.0, v.y1[i] - p);
-    a[0] += r * r; a[1] += d * d; a[2] += p * v.sig[i]; a[3] += v.y1[i];
-    r = fmax(0.0, mu_min - v.mu_avg[i] - v.sig_avg[i]);
-    d = fmax(0.0, v.y_avg[i] - p);
-    a[4] += r * r; a[5] += d * d; a[6] += p * v.sig_avg[i]; a[7] += v.y_avg[i];
+  __shared__ double bc[2];
+  HpScal* s = v.sc;
+  const double om = s->omega, kc = s->kc;
+  double pos = 0.0;
+  for (int64_t j = threadIdx.x; j < k; j += blockDim.x) {
+    const double val = v.t[j] - v.tau[j] / om * (1.0 - v.gT[j]);
+    v.tT[j] = val;
+    pos += fmax(0.0, val);
   }
-  for (int q = 0; q < 8; ++q) {
+  const double p0 = block_sum(pos, sh);
+  if (threadIdx.x == 0) bc[0] = p0;
+  __syncthreads();
+  double lam = 0.0;
+  if (bc[0] > cap) {
+    double prev = -1.0;  // (meaningful in thread 0 only)
+    for (int it = 0; it < 200; ++it) {  // finite and monotone
+      double sv = 0.0, st = 0.0, cn = 0.0;
+      for (int64_t j = threadIdx.x; j < k; j += blockDim.x) {
+        const double val = v.tT[j], tj = v.tau[j];
+        if (val > lam * tj) { sv += val; st += tj; cn += 1.0; }
+      }
+      const double SV = block_sum(sv, sh);
+      const double ST = block_sum(st, sh);
+      const double CN = block_sum(cn, sh);
+      if (threadIdx.x == 0) { bc[0] = (SV - cap) / ST; bc[1] = CN == prev ? 1.0 : 0.0; prev = CN; }
+      __syncthreads();
+      lam = fmax(lam, bc[0]);
+      const bool stop = bc[1] != 0.0;
+      __syncthreads();
+      if (stop) break;
+    }
+  }
+  primal_finish(v, k, n, lam, sh, s, kc);
+}
+
+// multi-process projection: v and Σmax(0, v) (k_hp_primal_v), host-driven
+// Newton steps over the ranks' summed (Σ v, Σ T, count) (k_hp_proj_sums), then
+// k_hp_primal_fin
+__global__ void __launch_bounds__(1024) k_hp_primal_v(HpVec v, int64_t k) {
+  __shared__ double sh[32];
+  const double om = v.sc->omega;
+  double pos = 0.0;
+  for (int64_t j = threadIdx.x; j < k; j += blockDim.x) {
+    const double val = v.t[j] - v.tau[j] / om * (1.0 - v.gT[j]);
+    v.tT[j] = val;
+    pos += fmax(0.0, val);
+  }
+  const double p0 = block_sum(pos, sh);
+  if (threadIdx.x == 0) { v.cres[2] = p0; v.cres[3] = 0.0; v.cres[4] = 0.0; }
+}
+
+__global__ void __launch_bounds__(1024) k_hp_proj_sums(HpVec v, int64_t k, double lam) {
+  __shared__ double sh[32];
+  double sv = 0.0, st = 0.0, cn = 0.0;
+  for (int64_t j = threadIdx.x; j < k; j += blockDim.x) {
+    const double val = v.tT[j], tj = v.tau[j];
+    if (val > lam * tj) { sv += val; st += tj; cn += 1.0; }
+  }
+  const double SV = block_sum(sv, sh);
+  const double ST = block_sum(st, sh);
+  const double CN = block_sum(cn, sh);
+  if (threadIdx.x == 0) { v.cres[2] = SV; v.cres[3] = ST; v.cres[4] = CN; }
+}
+
+__global__ void __launch_bounds__(1024) k_hp_primal_fin(HpVec v, int64_t k, int64_t n, double lam) {
+  __shared__ double sh[32];
+  primal_finish(v, k, n, lam, sh, v.sc, v.sc->kc);
+}
+
+// σ̂, ŷ of T(z), row residuals, then the Halpern mix of σ, y and A t
+__global__ void __launch_bounds__(kHpThreads) k_hp_dual(HpVec v, int64_t n, double mu_min, double eta) {
+  __shared__ double sh[32];
+  const HpScal* s = v.sc;
+  const double w = s->w, om = s->omega;
+  const bool first = s->first != 0.0;
+  double r0 = 0.0, r1 = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)kHpThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kHpThreads) {
+    const double so = v.sig[i], yo = v.y[i], muo = v.mu[i], muh = v.buf[i];
+    const double sn = fmax(0.0, so - eta / om * (v.pen[i] - yo));
+    const double yh = fmax(0.0, yo + om * v.sig1[i] * (mu_min - 2.0 * (muh + sn) + (muo + so)));
+    const double ds = sn - so, dy = yh - yo;
+    r0 += ds * ds / eta;
+    r1 += dy * dy / v.sig1[i];
+    v.sigT[i] = sn;
+    v.yT[i] = yh;
+    v.sig[i] = w * (2.0 * sn - so) + (1.0 - w) * v.sig0[i];
+    v.y[i] = w * (2.0 * yh - yo) + (1.0 - w) * v.y0[i];
+    v.mu[i] = w * (2.0 * muh - muo) + (1.0 - w) * v.mu0[i];
+  }
+  const double a = block_sum(r0, sh);
+  const double b = block_sum(r1, sh);
+  if (threadIdx.x == 0) {
+    v.res[blockIdx.x * 4 + 0] = a;
+    v.res[blockIdx.x * 4 + 1] = b;
+    if (first) { v.res[blockIdx.x * 4 + 2] = a; v.res[blockIdx.x * 4 + 3] = b; }
+  }
+}
+
+// Halpern mix of t and Aᵀy
+__global__ void k_hp_mix_cols(HpVec v, int64_t k) {
+  const double w = v.sc->w;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < k; j += (int64_t)gridDim.x * blockDim.x) {
+    v.t[j] = w * (2.0 * v.tT[j] - v.t[j]) + (1.0 - w) * v.t0[j];
+    v.gT[j] = w * (2.0 * v.gTT[j] - v.gT[j]) + (1.0 - w) * v.gT0[j];
+  }
+}
+
+// KKT pieces of T(z) over the rows: Σmax(0, μ_min − A t̂ − σ̂)², Σmax(0, ŷ − p)², Σ p σ̂, Σ ŷ
+__global__ void __launch_bounds__(kHpThreads) k_hp_kkt_rows(HpVec v, int64_t n, double mu_min) {
+  __shared__ double sh[32];
+  double a[4] = {0, 0, 0, 0};
+  for (int64_t i = blockIdx.x * (int64_t)kHpThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kHpThreads) {
+    const double p = v.pen[i];
+    const double r = fmax(0.0, mu_min - v.buf[i] - v.sigT[i]);
+    const double d = fmax(0.0, v.yT[i] - p);
+    a[0] += r * r; a[1] += d * d; a[2] += p * v.sigT[i]; a[3] += v.yT[i];
+  }
+  for (int q = 0; q < 4; ++q) {
     const double s = block_sum(a[q], sh);
     if (threadIdx.x == 0) v.part[blockIdx.x * 8 + q] = s;
   }
 }
 
-// KKT pieces over this rank's columns: Σ max(0, (Aᵀy)_k − y_b − 1)² (current, average)
-__global__ void __launch_bounds__(1024) k_lp_kkt_cols(LpVec v, int64_t k) {
+// rows_out[0..nq) = row partial sums; [4..8) = residual partials (last, first after restart)
+__global__ void k_hp_rows_final(HpVec v, int nq) {
+  const int q = threadIdx.x;
+  double s = 0.0;
+  if (q < nq) {
+    for (int b = 0; b < kHpBlocks; ++b) s += v.part[b * 8 + q];
+    v.rows_out[q] = s;
+  } else if (q >= 4 && q < 8) {
+    for (int b = 0; b < kHpBlocks; ++b) s += v.res[b * 4 + (q - 4)];
+    v.rows_out[q] = s;
+  }
+}
+
+// cols_out = [Σmax(0, (Aᵀŷ)_k − ωλ − 1)², Σ t̂, col residual last, first | max_k (Aᵀŷ)_k, ωλ]
+__global__ void __launch_bounds__(1024) k_hp_kkt_cols(HpVec v, int64_t k) {
   __shared__ double sh[32];
-  const double y2 = v.sc->y2, y2a = v.sc->y2_avg;
-  double a0 = 0.0, a1 = 0.0;
+  const double yb = v.sc->omega * v.sc->lam;
+  double a0 = 0.0, a1 = 0.0, mx = -INFINITY;
   for (int64_t j = threadIdx.x; j < k; j += blockDim.x) {
-    const double d0 = fmax(0.0, v.gT[j] - y2 - 1.0), d1 = fmax(0.0, v.gT_avg[j] - y2a - 1.0);
-    a0 += d0 * d0;
-    a1 += d1 * d1;
+    const double g = v.gTT[j];
+    const double d = fmax(0.0, g - yb - 1.0);
+    a0 += d * d;
+    a1 += v.tT[j];
+    mx = fmax(mx, g);
   }
   const double s0 = block_sum(a0, sh);
   const double s1 = block_sum(a1, sh);
-  if (threadIdx.x == 0) { v.cols_out[0] = s0; v.cols_out[1] = s1; }
+  const double m = block_max(mx, sh);
+  if (threadIdx.x == 0) {
+    v.cols_out[0] = s0; v.cols_out[1] = s1; v.cols_out[2] = v.cres[0]; v.cols_out[3] = v.cres[1];
+    v.cols_out[4] = m; v.cols_out[5] = yb;
+  }
 }
 
-// restart movement: Σ(σ − σ_last)², Σ(y − y_last)² (rows) and Σ(t − t_last)² (cols)
-__global__ void __launch_bounds__(kLpThreads) k_lp_move_rows(LpVec v, int64_t n, double eta) {
+// movement between restart points (T(z) vs the anchor z₀), in the preconditioned norms
+__global__ void __launch_bounds__(kHpThreads) k_hp_move_rows(HpVec v, int64_t n, double eta) {
   __shared__ double sh[32];
   double a0 = 0.0, a1 = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)kLpThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kLpThreads) {
-    const double d0 = v.sig[i] - v.sig_last[i], d1 = v.y1[i] - v.y_last[i];
-    a0 += d0 * d0 / eta;  // movement in the preconditioned space: ‖T^-½ Δx‖, ‖Σ^-½ Δy‖
+  for (int64_t i = blockIdx.x * (int64_t)kHpThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kHpThreads) {
+    const double d0 = v.sigT[i] - v.sig0[i], d1 = v.yT[i] - v.y0[i];
+    a0 += d0 * d0 / eta;
     a1 += d1 * d1 / v.sig1[i];
   }
   const double s0 = block_sum(a0, sh);
@@ -165,90 +284,75 @@ __global__ void __launch_bounds__(kLpThreads) k_lp_move_rows(LpVec v, int64_t n,
   if (threadIdx.x == 0) { v.part[blockIdx.x * 8] = s0; v.part[blockIdx.x * 8 + 1] = s1; }
 }
 
-__global__ void __launch_bounds__(1024) k_lp_move_cols(LpVec v, int64_t k) {
+__global__ void __launch_bounds__(1024) k_hp_move_cols(HpVec v, int64_t k) {
   __shared__ double sh[32];
   double a = 0.0;
   for (int64_t j = threadIdx.x; j < k; j += blockDim.x) {
-    const double d = v.t[j] - v.t_last[j];
+    const double d = v.tT[j] - v.t0[j];
     a += d * d / v.tau[j];
   }
   const double s = block_sum(a, sh);
-  if (threadIdx.x == 0) v.cols_out[2] = s;
+  if (threadIdx.x == 0) v.cols_out[6] = s;
 }
 
-// Σ_i Σ1_i (rows) and Σ_k T_k (cols): the initial primal weight in the preconditioned space
-__global__ void __launch_bounds__(kLpThreads) k_lp_wsum_rows(LpVec v, int64_t n) {
-  __shared__ double sh[32];
-  double a = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)kLpThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kLpThreads)
-    a += v.sig1[i];
-  const double s = block_sum(a, sh);
-  if (threadIdx.x == 0) v.part[blockIdx.x * 8] = s;
-}
-
-__global__ void __launch_bounds__(1024) k_lp_wsum_cols(LpVec v, int64_t k) {
-  __shared__ double sh[32];
-  double a = 0.0;
-  for (int64_t j = threadIdx.x; j < k; j += blockDim.x) a += v.tau[j];
-  const double s = block_sum(a, sh);
-  if (threadIdx.x == 0) v.cols_out[3] = s;
-}
-
-// sum the per-block row partials in block order (q < nq quantities)
-__global__ void k_lp_rows_final(LpVec v, int nq) {
-  const int q = threadIdx.x;
-  if (q >= nq) return;
-  double s = 0.0;
-  for (int b = 0; b < kLpBlocks; ++b) s += v.part[b * 8 + q];
-  v.rows_out[q] = s;
-}
-
-// restart: optionally replace the iterate by the average; reset the average;
-// set the anchors for the next movement measurement; set ω
-__global__ void k_lp_restart_rows(LpVec v, int64_t n, int to_avg, int anchor) {
+// (re)start: z = z₀ = T(z) (from_T) or z₀ = z; products follow; ω set, k = 0
+__global__ void k_hp_anchor_rows(HpVec v, int64_t n, int from_T) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    if (to_avg) { v.sig[i] = v.sig_avg[i]; v.y1[i] = v.y_avg[i]; v.mu[i] = v.mu_avg[i]; }
-    if (anchor) { v.sig_last[i] = v.sig[i]; v.y_last[i] = v.y1[i]; }
+    if (from_T) { v.sig[i] = v.sigT[i]; v.y[i] = v.yT[i]; v.mu[i] = v.buf[i]; }
+    v.sig0[i] = v.sig[i]; v.y0[i] = v.y[i]; v.mu0[i] = v.mu[i];
   }
 }
 
-__global__ void k_lp_restart_cols(LpVec v, int64_t k, int to_avg, int anchor, double omega) {
+__global__ void k_hp_anchor_cols(HpVec v, int64_t k, int from_T, double omega) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < k; j += (int64_t)gridDim.x * blockDim.x) {
-    if (to_avg) v.t[j] = v.t_avg[j];
-    if (anchor) v.t_last[j] = v.t[j];
+    if (from_T) { v.t[j] = v.tT[j]; v.gT[j] = v.gTT[j]; }
+    v.t0[j] = v.t[j]; v.gT0[j] = v.gT[j];
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
-    LpScal* s = v.sc;
-    if (to_avg) { s->y2 = s->y2_avg; s->S = s->S_avg; }
-    if (anchor) s->y2_last = s->y2;
-    s->omega = omega;
-    s->m = 0.0;
+    v.sc->omega = omega;
+    v.sc->kc = 0.0;
+    v.sc->w = 0.5;
+    v.sc->first = 1.0;
   }
 }
 
-// setup: preconditioners from the row/column sums of A (A ≥ 0), penalties, zero state
-__global__ void k_lp_setup_rows(LpVec v, int64_t n, const double* __restrict__ rowsum, const double* pen_in,
+// setup: preconditioners from the row/column sums of A (A ≥ 0), penalties, state
+__global__ void k_hp_setup_rows(HpVec v, int64_t n, const double* __restrict__ rowsum, const double* pen_in,
                                 double pen_scalar, double eta) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    v.sig1[i] = eta / (rowsum[i] + 1.0);  // row i of K: Σ_k A_ik + 1 (σ_i)
+    v.sig1[i] = eta / (rowsum[i] + 1.0);  // row i of [A I]: Σ_k A_ik + 1
     v.pen[i] = pen_in ? pen_in[i] : pen_scalar;
-    v.sig[i] = 0.0; v.y1[i] = 0.0;
-    v.sig_avg[i] = 0.0; v.mu_avg[i] = 0.0; v.y_avg[i] = 0.0;
+    v.sig[i] = 0.0;
+    v.y[i] = 0.0;
   }
 }
 
-__global__ void k_lp_setup_cols(LpVec v, int64_t k, double eta) {
+__global__ void k_hp_setup_cols(HpVec v, int64_t k, double eta) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < k; j += (int64_t)gridDim.x * blockDim.x) {
-    v.tau[j] = eta / (v.gT[j] + 1.0);  // column k of K: Σ_i A_ik + 1 (budget row)
-    v.t_avg[j] = 0.0; v.gT_avg[j] = 0.0;
+    v.tau[j] = eta / fmax(v.gT[j], 1e-6);  // column k of A: Σ_i A_ik (a dark column gets a large step)
     v.t[j] = fmax(0.0, v.t[j]);
   }
 }
 
-__global__ void k_lp_init_scalars(LpVec v, int64_t n, double omega) {
-  LpScal* s = v.sc;
-  s->S = v.buf[n]; s->S_avg = 0.0; s->y2 = 0.0; s->y2_avg = 0.0; s->y2_last = 0.0;
-  s->omega = omega; s->w = 1.0; s->m = 0.0;
+// Σ_i Σ1_i, Σ p_i² (rows) -> part; Σ_k T_k (cols) -> cols_out[7]
+__global__ void __launch_bounds__(kHpThreads) k_hp_wsum_rows(HpVec v, int64_t n) {
+  __shared__ double sh[32];
+  double a = 0.0, b = 0.0;
+  for (int64_t i = blockIdx.x * (int64_t)kHpThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kHpThreads) {
+    a += v.sig1[i];
+    b += v.pen[i] * v.pen[i];
+  }
+  const double s0 = block_sum(a, sh);
+  const double s1 = block_sum(b, sh);
+  if (threadIdx.x == 0) { v.part[blockIdx.x * 8] = s0; v.part[blockIdx.x * 8 + 1] = s1; }
+}
+
+__global__ void __launch_bounds__(1024) k_hp_wsum_cols(HpVec v, int64_t k) {
+  __shared__ double sh[32];
+  double a = 0.0;
+  for (int64_t j = threadIdx.x; j < k; j += blockDim.x) a += v.tau[j];
+  const double s = block_sum(a, sh);
+  if (threadIdx.x == 0) v.cols_out[7] = s;
 }
 
 __global__ void k_fill(double* x, int64_t n, double val) {
@@ -256,60 +360,14 @@ __global__ void k_fill(double* x, int64_t n, double val) {
     x[i] = val;
 }
 
-__global__ void k_sumsq_final(const double* __restrict__ x, int64_t n, double* out) {
-  __shared__ double sh[32];
-  double a = 0.0;
-  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) a += x[i] * x[i];
-  const double s = block_sum(a, sh);
-  if (threadIdx.x == 0) *out = s;
-}
-
-__global__ void __launch_bounds__(1024) k_lp_sum_t(LpVec v, int64_t k, int64_t n) {
-  __shared__ double sh[32];
-  double a = 0.0;
-  for (int64_t j = threadIdx.x; j < k; j += blockDim.x) a += v.t[j];
-  const double s = block_sum(a, sh);
-  if (threadIdx.x == 0) v.buf[n] = s;
-}
-
-__global__ void k_lp_copy_mu(LpVec v, int64_t n) {
+__global__ void k_copy(double* dst, const double* src, int64_t n) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    v.mu[i] = v.buf[i];
-}
-
-// S, y_b, S_avg, y_b avg, m, y_b anchor -> out[0..5]
-__global__ void k_lp_scalars_out(LpVec v, double* out) {
-  const LpScal* s = v.sc;
-  out[0] = s->S; out[1] = s->y2; out[2] = s->S_avg; out[3] = s->y2_avg; out[4] = s->m; out[5] = s->y2_last;
+    dst[i] = src[i];
 }
 
 }  // namespace uvd
 
 using namespace uvd;
-
-namespace {
-
-struct HostKkt {
-  double rp, rd, pobj, dobj, gap, rel_p, rel_d, rel_g, kkt_w;
-};
-
-HostKkt score(double rp2_rows, double rd2_rows, double psig, double sumy, double rd2_cols, double S, double y2,
-              double mu_min, double t_max, double qn, double cn, double omega) {
-  HostKkt h;
-  const double over = std::max(0.0, S - t_max);
-  h.rp = std::sqrt(rp2_rows + over * over);
-  h.rd = std::sqrt(rd2_rows + rd2_cols);
-  h.pobj = S + psig;
-  h.dobj = mu_min * sumy - t_max * y2;
-  h.gap = std::fabs(h.pobj - h.dobj);
-  h.rel_p = h.rp / (1.0 + qn);
-  h.rel_d = h.rd / (1.0 + cn);
-  h.rel_g = h.gap / (1.0 + std::fabs(h.pobj) + std::fabs(h.dobj));
-  h.kkt_w = std::sqrt(omega * h.rp * h.rp + h.rd * h.rd / omega + h.gap * h.gap);
-  return h;
-}
-
-}  // namespace
 
 extern "C" int uvd_lp_solve(const uvd_matrix_out* A, int64_t n, int64_t k, const uvd_lp_opts* o, double* t,
                             double* sigma, double* y, uvd_lp_result* res, void* stream) {
@@ -326,51 +384,57 @@ extern "C" int uvd_lp_solve(const uvd_matrix_out* A, int64_t n, int64_t k, const
   const double eps = o->eps > 0.0 ? o->eps : 1e-6;
   const int64_t max_iter = o->max_iter > 0 ? o->max_iter : 200000;
   const int M = o->check_every > 0 ? o->check_every : 64;
-  const double eta = 0.999;  // strict: ‖Σ^½ K T^½‖ ≤ η < 1
+  const double eta = 0.999;
+  const double mu_min = o->mu_min, t_max = o->t_max;
   const bool multi = o->allreduce != nullptr;
-  auto allreduce = [&](double* buf, int64_t cnt) -> int {
-    if (!multi) return UVD_OK;
-    const int rc = o->allreduce(buf, cnt, stream, o->allreduce_ctx);
+  auto allreduce = [&](double* buf, int64_t cnt, int op) -> int {
+    if (!multi || cnt == 0) return UVD_OK;
+    const int rc = o->allreduce(buf, cnt, op, stream, o->allreduce_ctx);
     if (rc != 0) { set_error("uvd_lp_solve: allreduce callback failed (%d)", rc); return UVD_ERR_INVALID; }
     return UVD_OK;
   };
 
-  // ---- workspace (one allocation; freed at the end) ----
+  // ---- workspace ----
   const int64_t kk = std::max<int64_t>(k, 1);
-  const size_t nd = (size_t)5 * kk + (size_t)10 * n + 1 + (size_t)kLpBlocks * 8 + 8 + 4 + 2 * (size_t)n + 8;
+  const size_t nd = (size_t)6 * kk + (size_t)9 * n + 1 + std::max<size_t>(n, kk) + (size_t)kHpBlocks * 12 + 32;
   double* ws = nullptr;
-  UVD_CUDA_TRY(cudaMalloc(&ws, nd * sizeof(double) + sizeof(LpScal) + 64));
-  double* h = nullptr;  // pinned host mirror of the check results
-  UVD_CUDA_TRY(cudaMallocHost(&h, 32 * sizeof(double)));
-  LpVec v;
+  UVD_CUDA_TRY(cudaMalloc(&ws, nd * sizeof(double) + sizeof(HpScal) + 64));
+  double* h = nullptr;  // pinned host mirror of check results
+  if (cudaMallocHost(&h, 64 * sizeof(double)) != cudaSuccess) {
+    cudaFree(ws);
+    set_error("uvd_lp_solve: pinned allocation failed");
+    return UVD_ERR_NOMEM;
+  }
+  HpVec v;
   double* p = ws;
   v.t = t;
   v.gT = p; p += kk;
-  v.t_avg = p; p += kk;
-  v.gT_avg = p; p += kk;
-  v.t_last = p; p += kk;
+  v.t0 = p; p += kk;
+  v.gT0 = p; p += kk;
+  v.tT = p; p += kk;
+  v.gTT = p; p += kk;
   v.tau = p; p += kk;
   v.sig = sigma;
-  v.y1 = y;
+  v.y = y;
   v.mu = p; p += n;
+  v.sig0 = p; p += n;
+  v.y0 = p; p += n;
+  v.mu0 = p; p += n;
+  v.sigT = p; p += n;
+  v.yT = p; p += n;
   v.buf = p; p += n + 1;
-  v.sig_avg = p; p += n;
-  v.mu_avg = p; p += n;
-  v.y_avg = p; p += n;
-  v.sig_last = p; p += n;
-  v.y_last = p; p += n;
   v.sig1 = p; p += n;
   v.pen = p; p += n;
-  double* ones = p; p += std::max(n, kk);  // all-ones vector (setup only)
-  v.part = p; p += kLpBlocks * 8;
+  double* ones = p; p += std::max(n, kk);
+  v.part = p; p += (size_t)kHpBlocks * 8;
+  v.res = p; p += (size_t)kHpBlocks * 4;
+  v.cres = p; p += 8;
   v.rows_out = p; p += 8;
-  v.cols_out = p; p += 4;
-  double* misc = p; p += 8;
-  v.sc = reinterpret_cast<LpScal*>(p);
+  v.cols_out = p; p += 8;
+  v.sc = reinterpret_cast<HpScal*>(p);
 
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t exec = nullptr;
-  int rc = UVD_OK;
   auto finish = [&](int code) {
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
@@ -379,204 +443,215 @@ extern "C" int uvd_lp_solve(const uvd_matrix_out* A, int64_t n, int64_t k, const
     cudaFreeHost(h);
     return code;
   };
-#define LP_TRY(expr)                 \
-  do {                               \
-    const int _r = (expr);           \
-    if (_r != UVD_OK) return finish(_r); \
+#define LP_TRY(expr)                       \
+  do {                                     \
+    const int _r = (expr);                 \
+    if (_r != UVD_OK) return finish(_r);   \
   } while (0)
-#define LP_CUDA(expr)                                                                          \
-  do {                                                                                         \
-    const cudaError_t _e = (expr);                                                             \
-    if (_e != cudaSuccess) {                                                                   \
-      set_error("uvd_lp_solve: %s: %s", #expr, cudaGetErrorString(_e));                       \
-      return finish(UVD_ERR_CUDA);                                                             \
-    }                                                                                          \
+#define LP_CUDA(expr)                                                        \
+  do {                                                                       \
+    const cudaError_t _e = (expr);                                           \
+    if (_e != cudaSuccess) {                                                 \
+      set_error("uvd_lp_solve: %s: %s", #expr, cudaGetErrorString(_e));     \
+      return finish(UVD_ERR_CUDA);                                           \
+    }                                                                        \
   } while (0)
+  auto fetch = [&](double* dst, const double* src, int cnt) -> int {
+    UVD_CUDA_TRY(cudaMemcpyAsync(dst, src, cnt * sizeof(double), cudaMemcpyDeviceToHost, st));
+    return UVD_OK;
+  };
 
-  const int nb_rows = (int)std::min<int64_t>((n + kLpThreads - 1) / kLpThreads, kLpBlocks);
-  // ---- setup: preconditioners, ‖c‖, ‖q‖ ----
-  k_fill<<<kLpBlocks, kLpThreads, 0, st>>>(ones, std::max(n, kk), 1.0);
+  const int nb_rows = (int)std::min<int64_t>((n + kHpThreads - 1) / kHpThreads, kHpBlocks);
+  LP_CUDA(cudaMemsetAsync(v.res, 0, (size_t)kHpBlocks * 4 * sizeof(double), st));  // blocks >= nb_rows stay 0
+  // ---- setup: preconditioners, norms, ω₀ ----
+  k_fill<<<kHpBlocks, kHpThreads, 0, st>>>(ones, std::max(n, kk), 1.0);
   note_launch();
-  LP_TRY(uvd_fluence(A, n, k, 1, ones, v.gT, stream));       // column sums Σ_i A_ik
-  LP_TRY(uvd_fluence(A, n, k, 0, ones, v.buf, stream));      // partial row sums Σ_k A_ik
-  LP_TRY(allreduce(v.buf, n));
-  k_lp_setup_rows<<<kLpBlocks, kLpThreads, 0, st>>>(v, n, v.buf, o->penalty, o->penalty_scalar, eta);
-  k_lp_setup_cols<<<kLpBlocks, kLpThreads, 0, st>>>(v, k, eta);
-  k_sumsq_final<<<1, 1024, 0, st>>>(v.pen, n, misc);  // Σ p²
-  note_launch(3);
-  LP_CUDA(cudaMemcpyAsync(h, misc, sizeof(double), cudaMemcpyDeviceToHost, st));
-  h[1] = (double)k;
+  LP_TRY(uvd_fluence(A, n, k, 1, ones, v.gT, stream));   // column sums Σ_i A_ik (local columns)
+  LP_TRY(uvd_fluence(A, n, k, 0, ones, v.buf, stream));  // row sums Σ_k A_ik (partial over ranks)
+  LP_TRY(allreduce(v.buf, n, 0));
+  k_hp_setup_rows<<<kHpBlocks, kHpThreads, 0, st>>>(v, n, v.buf, o->penalty, o->penalty_scalar, eta);
+  k_hp_setup_cols<<<kHpBlocks, kHpThreads, 0, st>>>(v, k, eta);
+  k_hp_wsum_rows<<<kHpBlocks, kHpThreads, 0, st>>>(v, n);
+  k_hp_rows_final<<<1, 32, 0, st>>>(v, 2);
+  k_hp_wsum_cols<<<1, 1024, 0, st>>>(v, k);
+  note_launch(5);
+  h[10] = (double)k;
+  LP_CUDA(cudaMemcpyAsync(v.cols_out + 6, &h[10], sizeof(double), cudaMemcpyHostToDevice, st));
+  LP_TRY(allreduce(v.cols_out + 6, 2, 0));  // [6] global column count, [7] Σ T_k
+  LP_TRY(fetch(h, v.rows_out, 2));
+  LP_TRY(fetch(h + 2, v.cols_out + 6, 2));
   LP_CUDA(cudaStreamSynchronize(st));
-  double sum_p2 = h[0];
-  double k_tot = (double)k;
-  if (multi) {  // global column count
-    LP_CUDA(cudaMemcpyAsync(misc + 2, &h[1], sizeof(double), cudaMemcpyHostToDevice, st));
-    LP_TRY(allreduce(misc + 2, 1));
-    LP_CUDA(cudaMemcpyAsync(&h[2], misc + 2, sizeof(double), cudaMemcpyDeviceToHost, st));
-    LP_CUDA(cudaStreamSynchronize(st));
-    k_tot = h[2];
-  }
-  const double qn = std::sqrt((double)n * o->mu_min * o->mu_min + o->t_max * o->t_max);
+  const double sum_sig1 = h[0], sum_p2 = h[1], k_tot = h[2], sum_tau = h[3];
+  const double qn = std::sqrt((double)n * mu_min * mu_min + t_max * t_max);
   const double cn = std::sqrt(k_tot + sum_p2);
-  const double sig2 = eta / std::max(k_tot, 1.0);  // budget row: Σ_k |−1| = K
   double omega = o->primal_weight;
   if (!(omega > 0.0)) {
-    // PDLP's ω₀ = ‖c‖/‖q‖ measured in the preconditioned space (x̃ = T^-½x, ỹ = Σ^-½y):
-    // ‖T^½ c‖² = Σ_k T_k + η Σ_i p_i²,  ‖Σ^½ q‖² = μ_min² Σ_i Σ1_i + Σ2 T_max²
-    k_lp_wsum_rows<<<kLpBlocks, kLpThreads, 0, st>>>(v, n);
-    k_lp_rows_final<<<1, 32, 0, st>>>(v, 1);
-    k_lp_wsum_cols<<<1, 1024, 0, st>>>(v, k);
-    note_launch(3);
-    LP_TRY(allreduce(v.cols_out + 3, 1));
-    LP_CUDA(cudaMemcpyAsync(h, v.rows_out, sizeof(double), cudaMemcpyDeviceToHost, st));
-    LP_CUDA(cudaMemcpyAsync(h + 1, v.cols_out + 3, sizeof(double), cudaMemcpyDeviceToHost, st));
-    LP_CUDA(cudaStreamSynchronize(st));
-    const double cs = std::sqrt(h[1] + eta * sum_p2);
-    const double qs = std::sqrt(o->mu_min * o->mu_min * h[0] + sig2 * o->t_max * o->t_max);
+    // PDLP's ω₀ = ‖c‖/‖q‖ in the preconditioned space: ‖T^½c‖² = Σ T_k + η Σ p², ‖Σ^½q‖² = μ_min² Σ Σ1_i
+    const double cs = std::sqrt(sum_tau + eta * sum_p2), qs = std::sqrt(mu_min * mu_min * sum_sig1);
     omega = cs > 0.0 && qs > 0.0 ? cs / qs : 1.0;
   }
 
-  // ---- initial point: μ = A t, S = Σ t, y = 0, σ = 0 ----
+  // ---- initial point z = (t, 0, 0): A t, Aᵀy ----
   LP_TRY(uvd_fluence(A, n, k, 0, t, v.buf, stream));
-  k_lp_sum_t<<<1, 1024, 0, st>>>(v, k, n);
+  LP_TRY(allreduce(v.buf, n, 0));
+  k_copy<<<kHpBlocks, kHpThreads, 0, st>>>(v.mu, v.buf, n);
   note_launch();
-  LP_TRY(allreduce(v.buf, n + 1));
-  k_lp_copy_mu<<<kLpBlocks, kLpThreads, 0, st>>>(v, n);
-  k_lp_init_scalars<<<1, 1, 0, st>>>(v, n, omega);
-  k_lp_restart_cols<<<kLpBlocks, kLpThreads, 0, st>>>(v, k, 0, 1, omega);  // anchors t_last = t
-  k_lp_restart_rows<<<kLpBlocks, kLpThreads, 0, st>>>(v, n, 0, 1);
-  note_launch(4);
-  LP_TRY(uvd_fluence(A, n, k, 1, v.y1, v.gT, stream));  // Aᵀy for the first iteration (y = 0)
+  LP_TRY(uvd_fluence(A, n, k, 1, v.y, v.gT, stream));
+  k_hp_anchor_rows<<<kHpBlocks, kHpThreads, 0, st>>>(v, n, 0);
+  k_hp_anchor_cols<<<kHpBlocks, kHpThreads, 0, st>>>(v, k, 0, omega);
+  note_launch(2);
 
-  // one PDHG iteration: x-update, A·t⁺ (+ Σt⁺), [allreduce], y-update, Aᵀy⁺
+  // one iteration: T(z) (projection, A t̂, σ̂, ŷ, Aᵀŷ) and the Halpern mix
+  auto project_multi = [&]() -> int {
+    k_hp_primal_v<<<1, 1024, 0, st>>>(v, k);
+    note_launch();
+    UVD_TRY(allreduce(v.cres + 2, 1, 0));
+    UVD_TRY(fetch(h + 20, v.cres + 2, 1));
+    UVD_CUDA_TRY(cudaStreamSynchronize(st));
+    double lam = 0.0;
+    if (h[20] > t_max) {
+      double prev = -1.0;
+      for (int it = 0; it < 200; ++it) {
+        k_hp_proj_sums<<<1, 1024, 0, st>>>(v, k, lam);
+        note_launch();
+        UVD_TRY(allreduce(v.cres + 2, 3, 0));
+        UVD_TRY(fetch(h + 20, v.cres + 2, 3));
+        UVD_CUDA_TRY(cudaStreamSynchronize(st));
+        lam = std::max(lam, (h[20] - t_max) / h[21]);
+        if (h[22] == prev) break;
+        prev = h[22];
+      }
+    }
+    k_hp_primal_fin<<<1, 1024, 0, st>>>(v, k, n, lam);
+    note_launch();
+    return UVD_OK;
+  };
   auto iteration = [&]() -> int {
-    k_lp_primal<<<1, 1024, 0, st>>>(v, k, n);
+    if (multi) {
+      UVD_TRY(project_multi());
+    } else {
+      k_hp_primal<<<1, 1024, 0, st>>>(v, k, n, t_max);
+      note_launch();
+    }
+    UVD_TRY(uvd_fluence(A, n, k, 0, v.tT, v.buf, stream));
+    UVD_TRY(allreduce(v.buf, n, 0));
+    k_hp_dual<<<nb_rows, kHpThreads, 0, st>>>(v, n, mu_min, eta);
     note_launch();
-    UVD_TRY(uvd_fluence(A, n, k, 0, v.t, v.buf, stream));
-    UVD_TRY(allreduce(v.buf, n + 1));
-    k_lp_dual<<<nb_rows, kLpThreads, 0, st>>>(v, n, o->mu_min, o->t_max, sig2, eta);
+    UVD_TRY(uvd_fluence(A, n, k, 1, v.yT, v.gTT, stream));
+    k_hp_mix_cols<<<kHpBlocks, kHpThreads, 0, st>>>(v, k);
     note_launch();
-    UVD_TRY(uvd_fluence(A, n, k, 1, v.y1, v.gT, stream));
     return UVD_OK;
   };
   const bool graph_ok = o->use_graph && !multi && st != nullptr;
   if (graph_ok) {
-    // warm the fluence scratch for this stream outside the capture
     LP_CUDA(cudaStreamSynchronize(st));
     LP_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
     int crc = UVD_OK;
-    for (int it = 0; it < M && crc == UVD_OK; ++it) crc = iteration();
+    for (int q = 0; q < M && crc == UVD_OK; ++q) crc = iteration();
     const cudaError_t ce = cudaStreamEndCapture(st, &graph);
     if (crc != UVD_OK) return finish(crc);
     LP_CUDA(ce);
     LP_CUDA(cudaGraphInstantiate(&exec, graph, 0));
   }
 
-  // evaluate the KKT pieces of the current iterate and of the average
-  auto evaluate = [&](HostKkt* cur, HostKkt* avg, double* S_out) -> int {
-    k_lp_kkt_rows<<<kLpBlocks, kLpThreads, 0, st>>>(v, n, o->mu_min);
-    k_lp_rows_final<<<1, 32, 0, st>>>(v, 8);
-    k_lp_kkt_cols<<<1, 1024, 0, st>>>(v, k);
+  struct Kkt { double rel_p, rel_d, rel_g, pobj, dobj, yb, S; };
+  double r_last = 0.0, r_first = 0.0;
+  // KKT of T(z) (the last iteration's operator output) and the fixed-point residuals
+  auto evaluate = [&](Kkt* out) -> int {
+    k_hp_kkt_rows<<<kHpBlocks, kHpThreads, 0, st>>>(v, n, mu_min);
+    k_hp_rows_final<<<1, 32, 0, st>>>(v, 4);
+    k_hp_kkt_cols<<<1, 1024, 0, st>>>(v, k);
     note_launch(3);
-    UVD_TRY(allreduce(v.cols_out, 2));
-    k_lp_scalars_out<<<1, 1, 0, st>>>(v, misc);
-    note_launch();
-    UVD_CUDA_TRY(cudaMemcpyAsync(h, v.rows_out, 8 * sizeof(double), cudaMemcpyDeviceToHost, st));
-    UVD_CUDA_TRY(cudaMemcpyAsync(h + 8, v.cols_out, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
-    UVD_CUDA_TRY(cudaMemcpyAsync(h + 10, misc, 5 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    UVD_TRY(allreduce(v.cols_out, 4, 0));
+    UVD_TRY(allreduce(v.cols_out + 4, 1, 1));
+    UVD_TRY(fetch(h, v.rows_out, 8));
+    UVD_TRY(fetch(h + 8, v.cols_out, 6));
     UVD_CUDA_TRY(cudaStreamSynchronize(st));
-    // misc: S, y2, S_avg, y2_avg, m
-    *cur = score(h[0], h[1], h[2], h[3], h[8], h[10], h[11], o->mu_min, o->t_max, qn, cn, omega);
-    *avg = score(h[4], h[5], h[6], h[7], h[9], h[12], h[13], o->mu_min, o->t_max, qn, cn, omega);
-    if (h[14] < 0.5) *avg = *cur;  // no averaged iterate yet
-    *S_out = h[10];
+    const double S = h[9];
+    const double over = std::max(0.0, S - t_max);
+    const double rp = std::sqrt(h[0] + over * over);
+    const double pobj = S + h[2];
+    Kkt best{};
+    double best_m = INFINITY;
+    // two budget multipliers: the projection's ωλ, and the least y_b making every column dual feasible
+    const double ybs[2] = {h[13], std::max(0.0, h[12] - 1.0)};
+    const double dres[2] = {h[8], 0.0};
+    for (int c = 0; c < 2; ++c) {
+      const double rd = std::sqrt(h[1] + dres[c]);
+      const double dobj = mu_min * h[3] - t_max * ybs[c];
+      Kkt q{rp / (1.0 + qn), rd / (1.0 + cn), std::fabs(pobj - dobj) / (1.0 + std::fabs(pobj) + std::fabs(dobj)),
+            pobj, dobj, ybs[c], S};
+      const double m = std::max(q.rel_p, std::max(q.rel_d, q.rel_g));
+      if (m < best_m) { best_m = m; best = q; }
+    }
+    *out = best;
+    r_last = std::sqrt(omega * (h[10] + h[4]) + h[5] / omega);
+    r_first = std::sqrt(omega * (h[11] + h[6]) + h[7] / omega);
     return UVD_OK;
   };
-  auto converged = [&](const HostKkt& c) { return c.rel_p <= eps && c.rel_d <= eps && c.rel_g <= eps; };
+  auto converged = [&](const Kkt& c) { return c.rel_p <= eps && c.rel_d <= eps && c.rel_g <= eps; };
 
-  HostKkt cur, avg;
-  double S = 0.0;
-  LP_TRY(evaluate(&cur, &avg, &S));
-  double kkt_restart = cur.kkt_w, kkt_prev_cand = INFINITY;
+  Kkt cur{};
   int64_t it = 0, it_restart = 0;
   int restarts = 0;
-  bool done = converged(cur), use_avg = false;
-  HostKkt fin = cur;
-  while (!done && it < max_iter) {
+  bool done = false;
+  double r_prev = INFINITY;
+  while (it < max_iter) {
     if (graph_ok) {
       LP_CUDA(cudaGraphLaunch(exec, st));
     } else {
       for (int q = 0; q < M; ++q) LP_TRY(iteration());
     }
     it += M;
-    LP_TRY(evaluate(&cur, &avg, &S));
-    if (converged(cur) || converged(avg)) {
-      use_avg = !converged(cur);
-      fin = use_avg ? avg : cur;
-      done = true;
-      break;
-    }
-    // restart decision (PDLP: β_sufficient 0.2, β_necessary 0.8, artificial 0.36)
-    const bool avg_better = avg.kkt_w < cur.kkt_w;
-    const double cand = avg_better ? avg.kkt_w : cur.kkt_w;
-    const bool do_restart = cand <= 0.2 * kkt_restart ||
-                            (cand <= 0.8 * kkt_restart && cand > kkt_prev_cand) ||
-                            (double)(it - it_restart) >= 0.36 * (double)it;
-    kkt_prev_cand = cand;
-    if (do_restart) {
-      if (avg_better) {  // the average becomes the iterate; its Aᵀy is recomputed
-        k_lp_restart_rows<<<kLpBlocks, kLpThreads, 0, st>>>(v, n, 1, 0);
-        k_lp_restart_cols<<<kLpBlocks, kLpThreads, 0, st>>>(v, k, 1, 0, omega);
-        note_launch(2);
-        LP_TRY(uvd_fluence(A, n, k, 1, v.y1, v.gT, stream));
-      }
-      // primal weight from the movement since the last restart (before the anchors move)
-      k_lp_move_rows<<<kLpBlocks, kLpThreads, 0, st>>>(v, n, eta);
-      k_lp_rows_final<<<1, 32, 0, st>>>(v, 2);
-      k_lp_move_cols<<<1, 1024, 0, st>>>(v, k);
-      k_lp_scalars_out<<<1, 1, 0, st>>>(v, misc);
-      note_launch(4);
-      LP_TRY(allreduce(v.cols_out + 2, 1));
-      LP_CUDA(cudaMemcpyAsync(h, v.rows_out, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
-      LP_CUDA(cudaMemcpyAsync(h + 2, v.cols_out + 2, sizeof(double), cudaMemcpyDeviceToHost, st));
-      LP_CUDA(cudaMemcpyAsync(h + 3, misc, 6 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    LP_TRY(evaluate(&cur));
+    if (converged(cur)) { done = true; break; }
+    const bool restart = r_last <= 0.2 * r_first || (r_last <= 0.8 * r_first && r_last > r_prev) ||
+                         (double)(it - it_restart) >= 0.36 * (double)it;
+    r_prev = r_last;
+    if (restart) {
+      // ω from the movement between restart points (before the anchors move)
+      k_hp_move_rows<<<kHpBlocks, kHpThreads, 0, st>>>(v, n, eta);
+      k_hp_rows_final<<<1, 32, 0, st>>>(v, 2);
+      k_hp_move_cols<<<1, 1024, 0, st>>>(v, k);
+      note_launch(3);
+      LP_TRY(allreduce(v.cols_out + 6, 1, 0));
+      LP_TRY(fetch(h, v.rows_out, 2));
+      LP_TRY(fetch(h + 2, v.cols_out + 6, 1));
       LP_CUDA(cudaStreamSynchronize(st));
-      const double dy2 = h[4] - h[8];  // y2 − y2_last
-      const double dx = std::sqrt(h[2] + h[0]), dy = std::sqrt(h[1] + dy2 * dy2 / sig2);
+      const double dx = std::sqrt(h[2] + h[0]), dy = std::sqrt(h[1]);
       if (dx > 1e-10 && dy > 1e-10) omega = std::exp(0.5 * std::log(dy / dx) + 0.5 * std::log(omega));
-      k_lp_restart_rows<<<kLpBlocks, kLpThreads, 0, st>>>(v, n, 0, 1);        // anchors = iterate
-      k_lp_restart_cols<<<kLpBlocks, kLpThreads, 0, st>>>(v, k, 0, 1, omega);  // ω, m = 0
+      k_hp_anchor_rows<<<kHpBlocks, kHpThreads, 0, st>>>(v, n, 1);
+      k_hp_anchor_cols<<<kHpBlocks, kHpThreads, 0, st>>>(v, k, 1, omega);
       note_launch(2);
-      kkt_restart = cand;
-      kkt_prev_cand = INFINITY;
       it_restart = it;
+      r_prev = INFINITY;
       ++restarts;
     }
   }
-  if (use_avg) {  // hand back the average
-    k_lp_restart_rows<<<kLpBlocks, kLpThreads, 0, st>>>(v, n, 1, 0);
-    k_lp_restart_cols<<<kLpBlocks, kLpThreads, 0, st>>>(v, k, 1, 0, omega);
-    note_launch(2);
+  // hand back T(z) of the last iteration: t̂, σ̂, ŷ and the chosen y_b
+  k_copy<<<kHpBlocks, kHpThreads, 0, st>>>(v.sig, v.sigT, n);
+  k_copy<<<kHpBlocks, kHpThreads, 0, st>>>(v.y, v.yT, n);
+  note_launch(2);
+  if (k > 0) {
+    k_copy<<<kHpBlocks, kHpThreads, 0, st>>>(v.t, v.tT, k);
+    note_launch();
   }
-  if (!done) fin = cur;
-  k_lp_scalars_out<<<1, 1, 0, st>>>(v, misc);
-  note_launch();
-  LP_CUDA(cudaMemcpyAsync(y + n, misc + 1, sizeof(double), cudaMemcpyDeviceToDevice, st));
-  LP_CUDA(cudaMemcpyAsync(h, misc, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  h[30] = cur.yb;
+  LP_CUDA(cudaMemcpyAsync(y + n, &h[30], sizeof(double), cudaMemcpyHostToDevice, st));
   LP_CUDA(cudaStreamSynchronize(st));
   LP_CUDA(cudaGetLastError());
   res->status = done ? 0 : 1;
   res->restarts = restarts;
   res->iterations = it;
-  res->primal_obj = fin.pobj;
-  res->dual_obj = fin.dobj;
-  res->rel_primal_res = fin.rel_p;
-  res->rel_dual_res = fin.rel_d;
-  res->rel_gap = fin.rel_g;
-  res->sum_t = h[0];
+  res->primal_obj = cur.pobj;
+  res->dual_obj = cur.dobj;
+  res->rel_primal_res = cur.rel_p;
+  res->rel_dual_res = cur.rel_d;
+  res->rel_gap = cur.rel_g;
+  res->sum_t = cur.S;
   res->primal_weight = omega;
-  res->averaged = use_avg ? 1 : 0;
-  return finish(rc);
+  res->averaged = 0;
+  return finish(UVD_OK);
 #undef LP_TRY
 #undef LP_CUDA
 }

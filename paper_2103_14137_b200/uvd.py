@@ -67,7 +67,7 @@ class _MatrixOut(C.Structure):
                 ("vis_bits", C.c_void_p), ("col_sumsq", C.c_void_p), ("counters", C.c_void_p)]
 
 
-_ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p)
+_ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_int, C.c_void_p, C.c_void_p)
 
 
 class _LpOpts(C.Structure):
@@ -462,12 +462,12 @@ def lp_solve(A, n: int, mu_min: float = 280.0, t_max: float = 1800.0, penalty=No
     if distributed:
         import torch.distributed as dist
 
-        def _allreduce(buf, count, strm, ctx):
+        def _allreduce(buf, count, op, strm, ctx):
             try:
                 s = torch.cuda.ExternalStream(strm) if strm else torch.cuda.current_stream()
                 with torch.cuda.stream(s):
                     t = torch.as_tensor(_DevView(buf, count), device=dev)
-                    dist.all_reduce(t)
+                    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == 1 else dist.ReduceOp.SUM)
                 return 0
             except Exception:  # noqa: BLE001 — reported to the C side as a failure code
                 return 1
