@@ -428,12 +428,14 @@ class _DevView:
 
 def lp_solve(A, n: int, mu_min: float = 280.0, t_max: float = 1800.0, penalty=None, t0=None,
              eps: float = 1e-6, max_iter: int = 200000, check_every: int = 64, use_graph: bool = True,
-             primal_weight: float = 0.0, distributed: bool = False, stream=None) -> dict:
+             primal_weight: float = 0.0, distributed: bool = False, allreduce=None, stream=None) -> dict:
     """uvd_lp_solve: the relaxed dwell-time LP of Eq. 9 on this
     process's column shard of A (dense (k, ld) tensor, or a CSC dict from
     Scene.irradiance_csc).  penalty: float (every patch) or (n,) fp64 CUDA
     tensor; None = 10·‖A‖_F is the caller's job (pass it).  distributed: sum the
-    per-iteration partials across torch.distributed ranks (columns sharded)."""
+    per-iteration partials across torch.distributed ranks (columns sharded);
+    allreduce: or any callable(tensor, op) reducing a CUDA fp64 tensor in place
+    across the column shards (op "sum" or "max")."""
     if isinstance(A, dict):
         m = _MatrixOut()
         m.format = CSC
@@ -459,15 +461,17 @@ def lp_solve(A, n: int, mu_min: float = 280.0, t_max: float = 1800.0, penalty=No
     o.max_iter, o.check_every, o.use_graph = int(max_iter), int(check_every), int(bool(use_graph))
     o.primal_weight = float(primal_weight)
     cb = None
-    if distributed:
+    if distributed and allreduce is None:
         import torch.distributed as dist
 
+        def allreduce(x, op):
+            dist.all_reduce(x, op=dist.ReduceOp.MAX if op == "max" else dist.ReduceOp.SUM)
+    if allreduce is not None:
         def _allreduce(buf, count, op, strm, ctx):
             try:
                 s = torch.cuda.ExternalStream(strm) if strm else torch.cuda.current_stream()
                 with torch.cuda.stream(s):
-                    t = torch.as_tensor(_DevView(buf, count), device=dev)
-                    dist.all_reduce(t, op=dist.ReduceOp.MAX if op == 1 else dist.ReduceOp.SUM)
+                    allreduce(torch.as_tensor(_DevView(buf, count), device=dev), "max" if op == 1 else "sum")
                 return 0
             except Exception:  # noqa: BLE001 — reported to the C side as a failure code
                 return 1

@@ -164,3 +164,56 @@ def test_lp_c3_end_to_end(uvd):
         t = res["t"].cpu().numpy()
         viol = np.maximum(0.0, configs.MU_MIN - An @ t - sig)
         assert viol.max() <= 1e-4 * configs.MU_MIN
+
+
+def test_lp_two_column_shards(uvd):
+    """Multi-process path of uvd_lp_solve (columns sharded) exercised by
+    two solver threads on two streams of this one GPU: the allreduce callback
+    sums the two shards' partials through host memory behind a host barrier (no
+    kernel ever waits on another).  The sharded solve reaches the single-process
+    objective; the union of the shards' dwell times is a feasible plan."""
+    import threading
+    n, k = 240, 36
+    A = synth_matrix(9, n, k, density=0.35, zero_rows=1)
+    p = 10.0 * float(np.linalg.norm(A.astype(np.float64)))
+    ref = OLP.solve(A.astype(np.float64), 280.0, p, 300.0)
+    shards = [[j for j in range(k) if (j // 4) % 2 == r] for r in range(2)]
+    bar = threading.Barrier(2)
+    slots = [None, None]
+    out = [None, None]
+
+    def reducer(rank):
+        def red(x, op):
+            torch.cuda.current_stream().synchronize()
+            slots[rank] = x.cpu()
+            bar.wait()
+            o = slots[1 - rank]
+            tot = torch.maximum(slots[rank], o) if op == "max" else (slots[0] + slots[1])  # same order on both
+            bar.wait()
+            x.copy_(tot.to(x.device))
+            torch.cuda.current_stream().synchronize()
+        return red
+
+    def run(rank):
+        s = torch.cuda.Stream()
+        with torch.cuda.stream(s):
+            g = dense_gpu(np.ascontiguousarray(A[:, shards[rank]]))
+            out[rank] = uvd.lp_solve(g, n, penalty=p, t_max=300.0, eps=1e-8, allreduce=reducer(rank), stream=s)
+            s.synchronize()
+
+    th = [threading.Thread(target=run, args=(r,)) for r in range(2)]
+    for x in th:
+        x.start()
+    for x in th:
+        x.join(timeout=600)
+    assert out[0] is not None and out[1] is not None
+    assert out[0]["status"] == 0 and out[0]["iterations"] == out[1]["iterations"]
+    assert abs(out[0]["primal_obj"] - ref["obj"]) <= REL_OBJ * (1 + ref["obj"])
+    assert out[0]["primal_obj"] == out[1]["primal_obj"]
+    t = np.zeros(k)
+    for r in range(2):
+        t[shards[r]] = out[r]["t"].cpu().numpy()
+    assert t.sum() <= 300.0 * (1 + 1e-6)
+    s = out[0]["sigma"].cpu().numpy()
+    viol = np.maximum(0.0, 280.0 - A.astype(np.float64) @ t - s)
+    assert viol.max() <= 1e-4 * 280.0
