@@ -71,6 +71,12 @@ def lib():
         L.orc_vantage_eval_2d.restype = None
         L.orc_vantage_eval_2d.argtypes = [_f32p, _f32p, _i32p, C.c_int, _f32p, C.c_int64,
                                           C.c_double, _u8p, _u8p]
+        L.orc_irradiance_area.restype = C.c_int
+        L.orc_irradiance_area.argtypes = [C.c_int, _f32p, _i32p, C.c_int64, _f32p, C.c_int64, _f32p, _i64p,
+                                          _i32p, _f32p, _f32p, _f64p, _f32p, C.c_int, C.c_double, C.c_int,
+                                          _i64p, _i64p, C.c_int64, _f64p, _u8p, _i32p, _i32p, C.c_int]
+        L.orc_solid_angle.restype = C.c_double
+        L.orc_solid_angle.argtypes = [_f64p, _f64p, _f64p, _f64p]
         _lib = L
     return _lib
 
@@ -174,6 +180,49 @@ def irradiance_matrix(patches: dict, lamps: np.ndarray, P: float = 80.0, mode: s
     r = irradiance_pairs(patches, lamps, ii.ravel(), jj.ravel(), P, mode, n_threads=n_threads)
     L = lamps.shape[1]
     return dict(A=r["A"].reshape(N, K), vis=r["vis"].reshape(N, K, L), deg=r["deg"].reshape(N, K, L))
+
+
+def solid_angle(p, a, b, c) -> float:
+    """Van Oosterom–Strackee solid angle of triangle abc seen from p (fp64)."""
+    f = [np.ascontiguousarray(v, np.float64) for v in (p, a, b, c)]
+    return float(lib().orc_solid_angle(*f))
+
+
+def irradiance_area_pairs(patches: dict, lamps: np.ndarray, pi, pj, m: int = 1, P: float = 80.0,
+                          mode: str = "3d", n_threads: int = 0) -> dict:
+    """NEXT-2, Eq. 4 as written (reading Q23): mean irradiance
+    over patch i from configuration j, each patch triangle split into 4^m
+    sub-triangles (edge midpoints), solid angle per sub-triangle (Van
+    Oosterom–Strackee), visibility of each sub-triangle's fp32 centroid."""
+    lamps = np.ascontiguousarray(lamps, np.float32)
+    K, L = lamps.shape[0], lamps.shape[1]
+    pi = np.ascontiguousarray(pi, np.int64)
+    pj = np.ascontiguousarray(pj, np.int64)
+    n, N = len(pi), patches["N"]
+    per = 2 if "seg" in patches else 1           # 2.5D: the wall quad's two triangles
+    pfirst = np.arange(N, dtype=np.int64) * per
+    pcount = np.full(N, per, np.int32)
+    A = np.zeros(n, np.float64)
+    deg = np.zeros(n, np.uint8)
+    nvis = np.zeros(n, np.int32)
+    nsub = np.zeros(n, np.int32)
+    seg = patches.get("seg", np.zeros((1, 4), np.float32))
+    rc = lib().orc_irradiance_area(0 if mode == "3d" else 1, patches["tri"], patches["tri_patch"],
+                                   len(patches["tri"]), np.ascontiguousarray(seg, np.float32), len(seg),
+                                   patches["tri"], pfirst, pcount, patches["centroid"], patches["normal"],
+                                   patches["area"], lamps.reshape(-1), L, P, int(m), pi, pj, n, A, deg,
+                                   nvis, nsub, n_threads)
+    if rc != 0:
+        raise ArithmeticError("lamp–surface distance < 1e-9 m (S:160)")
+    return dict(A=A, deg=deg.astype(bool), nvis=nvis, nsub=nsub)
+
+
+def irradiance_area_matrix(patches: dict, lamps: np.ndarray, m: int = 1, P: float = 80.0, mode: str = "3d",
+                           n_threads: int = 0) -> dict:
+    N, K = patches["N"], lamps.shape[0]
+    ii, jj = np.meshgrid(np.arange(N), np.arange(K), indexing="ij")
+    r = irradiance_area_pairs(patches, lamps, ii.ravel(), jj.ravel(), m, P, mode, n_threads)
+    return dict(A=r["A"].reshape(N, K), deg=r["deg"].reshape(N, K), nvis=r["nvis"].reshape(N, K))
 
 
 # --------------------------------------------------------------------------- #

@@ -592,3 +592,138 @@ void orc_vantage_eval_2d(const float* bounds, const float* poly_xy, const int* p
     ambiguous[q] = (uint8_t)amb;
   }
 }
+
+/* ======================================================================== */
+/* NEXT-2 — area-integrated irradiance (Eq. 4 as written)                    */
+/* ======================================================================== */
+/* Eq. 4 integrates the point-source irradiance over the patch and
+ * §IV-C divides the flux by the patch area ("mean irradiance
+ * I_i(x_k) = F[i]/|s_i|").  Reading Q23:
+ *   A[i,j] = (1/|s_i|) Σ_l (P/L)/(4π) Σ_s vis(p_l → c_s) · Ω(p_l, s)
+ * s ranges over the 4^m sub-triangles of each of patch i's triangles (edge
+ * midpoints, recursively, fp64); Ω = the solid angle of sub-triangle s seen
+ * from p_l (Van Oosterom & Strackee 1983, the closed form behind Mosher 1999);
+ * c_s = fl32 of the sub-triangle's centroid is the visibility target (the same
+ * open-segment test as a5, own triangles excluded); the front-facing test is the
+ * patch's (same as a4).  For an unoccluded patch Σ_s Ω_s = Ω of the patch
+ * exactly, so A is then exact; occlusion is resolved at 4^m samples per
+ * triangle. */
+static double solid_angle(v3 p, v3 a, v3 b, v3 c) {
+  v3 r1 = sub(a, p), r2 = sub(b, p), r3 = sub(c, p);
+  double l1 = norm(r1), l2 = norm(r2), l3 = norm(r3);
+  double num = fabs(dot(r1, cross(r2, r3)));
+  double den = l1 * l2 * l3 + dot(r1, r2) * l3 + dot(r1, r3) * l2 + dot(r2, r3) * l1;
+  return 2.0 * atan2(num, den);
+}
+
+typedef struct {
+  const float* tri; const int32_t* tri_patch; int64_t M;   /* 3D occluders */
+  const float* seg; int64_t n_seg;                           /* 2D occluders */
+  const float* ptri; const int64_t* pfirst; const int32_t* pcount;  /* patch triangles */
+  const float* centroid; const float* normal; const double* area;
+  const float* lamps; int L; double P; int m;
+  const int64_t* pi; const int64_t* pj;
+  int mode;
+  double* A; uint8_t* deg; int32_t* nvis; int32_t* nsub; int32_t* err;
+} area_ctx;
+
+/* max margin of the open segment p -> x against every occluder of patch i */
+static double max_margin(const area_ctx* c, int64_t i, v3 p, v3 x) {
+  v3 D = sub(x, p);
+  double d = norm(D);
+  double S = -INFINITY;
+  if (c->mode == 0) {
+    for (int64_t k = 0; k < c->M; ++k) {
+      if (c->tri_patch[k] == (int32_t)i) continue;
+      const float* t = c->tri + 9 * k;
+      double s = orc_tri_margin(p, D, d, ld3(t), ld3(t + 3), ld3(t + 6));
+      if (s > S) S = s;
+    }
+  } else {
+    for (int64_t k = 0; k < c->n_seg; ++k) {
+      if (k == i) continue;
+      const float* sg = c->seg + 4 * k;
+      double s = seg_margin_2d(p.x, p.y, D.x, D.y, d, sg[0], sg[1], sg[2], sg[3]);
+      if (s > S) S = s;
+    }
+  }
+  return S;
+}
+
+typedef struct { double acc; int nvis, nsub, deg, err; } area_acc;
+
+static void area_sub(const area_ctx* c, int64_t i, v3 p, v3 a, v3 b, v3 cc, int level, area_acc* r) {
+  if (level > 0) {
+    v3 ab = scl(add(a, b), 0.5), bc = scl(add(b, cc), 0.5), ca = scl(add(cc, a), 0.5);
+    area_sub(c, i, p, a, ab, ca, level - 1, r);
+    area_sub(c, i, p, ab, b, bc, level - 1, r);
+    area_sub(c, i, p, ca, bc, cc, level - 1, r);
+    area_sub(c, i, p, ab, bc, ca, level - 1, r);
+    return;
+  }
+  /* visibility target: the sub-triangle centroid rounded to fp32 */
+  float xf[3] = {(float)(((a.x + b.x) + cc.x) / 3.0), (float)(((a.y + b.y) + cc.y) / 3.0),
+                 (float)(((a.z + b.z) + cc.z) / 3.0)};
+  v3 x = ld3(xf);
+  r->nsub += 1;
+  if (norm(sub(x, p)) < ORC_DMIN) { r->err = 1; return; }
+  double S = max_margin(c, i, p, x);
+  if (fabs(S) < ORC_DEG) r->deg = 1;
+  if (S < 0.0) {
+    r->acc += solid_angle(p, a, b, cc);
+    r->nvis += 1;
+  }
+}
+
+static void area_pair(int64_t q, void* vctx) {
+  area_ctx* c = (area_ctx*)vctx;
+  int64_t i = c->pi[q], j = c->pj[q];
+  v3 C = ld3(c->centroid + 3 * i), n = ld3(c->normal + 3 * i);
+  double total = 0.0;
+  int deg = 0, nvis = 0, nsub = 0;
+  for (int l = 0; l < c->L; ++l) {
+    v3 p = ld3(c->lamps + 3 * (j * c->L + l));
+    v3 D = sub(C, p);
+    double d = norm(D);
+    if (d < ORC_DMIN) { c->err[0] = 1; deg = 1; continue; }
+    double cos_t = dot(sub(p, C), n) / d;
+    if (fabs(cos_t) < ORC_DEG) deg = 1;
+    if (!(cos_t > 0.0)) continue;           /* the patch faces away */
+    area_acc r = {0.0, 0, 0, 0, 0};
+    for (int32_t k = 0; k < c->pcount[i]; ++k) {
+      const float* t = c->ptri + 9 * (c->pfirst[i] + k);
+      area_sub(c, i, p, ld3(t), ld3(t + 3), ld3(t + 6), c->m, &r);
+    }
+    if (r.err) c->err[0] = 1;
+    deg |= r.deg;
+    nvis += r.nvis;
+    nsub += r.nsub;
+    total += (c->P / (double)c->L) / (4.0 * M_PI) * r.acc;
+  }
+  c->A[q] = total / c->area[i];
+  c->deg[q] = (uint8_t)deg;
+  c->nvis[q] = nvis;
+  c->nsub[q] = nsub;
+}
+
+/* mode 0: 3D occluders (tri, tri_patch, M); mode 1: 2D floorplan (seg, n_seg).
+ * Patch i's triangles: ptri[9 * (pfirst[i] + k)], k < pcount[i].  Per pair q:
+ * A[q], deg[q] (any sub-ray with |margin| < 1e-6 or |cosθ| < 1e-6), nvis[q] /
+ * nsub[q] visible / traced sub-rays (all lamp samples).  Returns 0 or -2. */
+int orc_irradiance_area(int mode, const float* tri, const int32_t* tri_patch, int64_t M,
+                        const float* seg, int64_t n_seg, const float* ptri, const int64_t* pfirst,
+                        const int32_t* pcount, const float* centroid, const float* normal,
+                        const double* area, const float* lamps, int L, double P, int m,
+                        const int64_t* pi, const int64_t* pj, int64_t n_pairs, double* A,
+                        uint8_t* deg, int32_t* nvis, int32_t* nsub, int n_threads) {
+  int32_t err = 0;
+  area_ctx c = {tri, tri_patch, M, seg, n_seg, ptri, pfirst, pcount, centroid, normal, area,
+                lamps, L, P, m, pi, pj, mode, A, deg, nvis, nsub, &err};
+  orc_parallel_for(n_pairs, n_threads, area_pair, &c);
+  return err ? -2 : 0;
+}
+
+/* Solid angle of triangle (a, b, c) seen from p (exported for the pins). */
+double orc_solid_angle(const double* p, const double* a, const double* b, const double* c) {
+  return solid_angle(mk(p[0], p[1], p[2]), mk(a[0], a[1], a[2]), mk(b[0], b[1], b[2]), mk(c[0], c[1], c[2]));
+}
