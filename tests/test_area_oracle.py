@@ -12,7 +12,7 @@ import math
 import numpy as np
 import pytest
 
-from synth import rooms, ward
+from synth import configs, rooms, ward
 
 
 def rect_solid_angle(a, b, h):
@@ -125,11 +125,12 @@ def test_small_patch_limit_is_the_point_model(orc):
 def test_2d_and_3d_area_oracles_agree(orc):
     """On an extruded world the floorplan visibility and the triangle
     visibility give the same area-model matrix on non-degenerate pairs."""
-    sc = rooms.random_room(2)
-    pat = orc.extruded_patches(dict(sc, patch_res=0.25))
-    lam = np.array([[[1.1, 2.3, 1.0]], [[3.2, 0.7, 1.0]]], np.float32)
+    sc = dict(rooms.random_room(2), patch_res=0.25)
+    pat = orc.extruded_patches(sc)
+    v = orc.vantage(sc, configs.DISC_OPTS)
+    lam = v["samples"][v["feasible"]][[3, 17, 40]]
     a2 = orc.irradiance_area_matrix(pat, lam, m=1, mode="2d")
     a3 = orc.irradiance_area_matrix(pat, lam, m=1, mode="3d")
     ok = ~(a2["deg"] | a3["deg"])
-    assert ok.mean() > 0.95 and (a2["A"][ok] > 0).mean() > 0.2
+    assert ok.mean() > 0.95 and (a2["A"][ok] > 0).mean() > 0.05
     assert np.allclose(a2["A"][ok], a3["A"][ok], rtol=1e-12, atol=0)
