@@ -163,10 +163,22 @@ UVD_API int uvd_vantage_sample(const uvd_scene* scene, const uvd_vantage_opts* o
 
 /* ------------------------------------------------------------------ a4–a6 */
 /* Lamp model: total radiant flux P split over L = samples_per_config
- * isotropic point samples of power P/L each. */
+ * isotropic point samples of power P/L each.
+ * Irradiance model (`model`):
+ *  UVD_MODEL_CENTROID (0, the hot path, BASELINE north_star): point source at
+ *    the patch centroid, all-or-nothing centroid visibility (Eq. 7, Q4/Q5).
+ *  UVD_MODEL_AREA (1, NEXT-2: Eq. 4 as written; Q23): mean
+ *    irradiance over the patch, A = (P/L)/(4π|s_i|) Σ_l Σ_s vis(p_l → c_s) Ω_s,
+ *    each patch triangle split `subdiv` times at edge midpoints (4^subdiv
+ *    sub-triangles), Ω_s the exact solid angle of sub-triangle s (Van Oosterom
+ *    & Strackee 1983), c_s = fl32 of its centroid the visibility target; the
+ *    front-facing test is the patch's.  Exact for unoccluded patches. */
+enum { UVD_MODEL_CENTROID = 0, UVD_MODEL_AREA = 1 };
 typedef struct {
   double power_w;
   int32_t samples_per_config;
+  int32_t model;    /* UVD_MODEL_CENTROID (default) or UVD_MODEL_AREA */
+  int32_t subdiv;   /* UVD_MODEL_AREA: subdivision level m, 0..6 */
 } uvd_lamp;
 
 enum { UVD_DENSE_COLMAJOR = 0, UVD_CSC = 1 };
@@ -209,7 +221,9 @@ typedef struct {
  * lamp_xyz: DEVICE [k_total * L * 3] (configuration j -> samples j*L .. j*L+L-1).
  * cols: HOST [n_cols] global configuration ids of this call's columns (local
  * column c <-> cols[c]); NULL means all, n_cols = k_total.  Asynchronous;
- * call uvd_sync_status to collect in-kernel DOMAIN errors. */
+ * call uvd_sync_status to collect in-kernel DOMAIN errors.
+ * UVD_MODEL_AREA (NEXT-2): dense output only (CSC returns INVALID); vis_bits
+ * bit = some sub-triangle of the patch seen from lamp sample l. */
 UVD_API int uvd_irradiance_matrix(const uvd_scene* scene, const float* lamp_xyz, int64_t k_total,
                           const int64_t* cols, int64_t n_cols, const uvd_lamp* lamp,
                           uvd_matrix_out* out, void* stream);

@@ -63,6 +63,11 @@ struct AsmParams {
   unsigned long long* __restrict__ counters;  // [6] or nullptr (instrumented kernel)
   uint32_t* __restrict__ pending;  // [n_cols][words] entries left undecided in fp32
   int* __restrict__ err;
+  // NEXT-2 area model (area_m >= 0): patch areas, patch-ordered wall triangles
+  // (extruded scenes; 3D patch r is the leaf-ordered triangle r), subdivision level
+  const double* __restrict__ area;
+  const float4* __restrict__ ptri;
+  int area_m;  // < 0: the centroid model (a4–a6)
 };
 
 // ---------------------------------------------------------------------------
@@ -205,6 +210,129 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmMinBlocks) k_assemble_lane(As
     if (COUNT) cnt[4] += pend;
     const float a = (float)(acc * P.scale);
     if (P.values) __stcs(P.values + c * P.ld + r, a);  // streaming: keep the BVH in L2
+  }
+  if (COUNT)
+    for (int k = 0; k < 6; ++k) {
+      unsigned long long v = cnt[k];
+      for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      if (lane == 0 && v) atomicAdd(P.counters + k, v);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// NEXT-2: area-integrated irradiance (Eq. 4 as written, P:159–162, P:248;
+// reading Q23).  Each triangle of patch r is split m times at its edge
+// midpoints (fp64, exact); sub-triangle s contributes its exact solid angle
+// (Van Oosterom & Strackee 1983) when the open segment from the lamp sample to
+// its centroid (rounded to fp32, the same target the oracle uses) is clear:
+//   A[r,j] = (P/L)/(4π|s_r|) Σ_l Σ_s vis_ls Ω_ls.
+// Same warp/tile mapping and traversal as k_assemble_lane; sub-rays of a lane
+// run back to back (the lanes of a warp trace the same sub-index of adjacent
+// patches, so they stay coherent).
+struct DTri { D3 a, b, c; };
+
+__device__ __forceinline__ D3 dmid(D3 u, D3 v) {  // exact midpoint of fp64 points from fp32 data
+  return d3(__dmul_rn(__dadd_rn(u.x, v.x), 0.5), __dmul_rn(__dadd_rn(u.y, v.y), 0.5),
+            __dmul_rn(__dadd_rn(u.z, v.z), 0.5));
+}
+
+// sub-triangle s of t after m midpoint subdivisions; base-4 digits of s, most
+// significant first, pick the child: 0 (a,ab,ca), 1 (ab,b,bc), 2 (ca,bc,c), 3 (ab,bc,ca)
+__device__ __forceinline__ DTri sub_tri(DTri t, uint32_t s, int m) {
+  for (int lv = m - 1; lv >= 0; --lv) {
+    const uint32_t dgt = (s >> (2 * lv)) & 3u;
+    const D3 ab = dmid(t.a, t.b), bc = dmid(t.b, t.c), ca = dmid(t.c, t.a);
+    DTri n;
+    if (dgt == 0) { n.a = t.a; n.b = ab; n.c = ca; }
+    else if (dgt == 1) { n.a = ab; n.b = t.b; n.c = bc; }
+    else if (dgt == 2) { n.a = ca; n.b = bc; n.c = t.c; }
+    else { n.a = ab; n.b = bc; n.c = ca; }
+    t = n;
+  }
+  return t;
+}
+
+__device__ __forceinline__ double tri_solid_angle(D3 p, const DTri& t) {
+  const D3 r1 = dsub3(t.a, p), r2 = dsub3(t.b, p), r3 = dsub3(t.c, p);
+  const double l1 = sqrt(ddot3(r1, r1)), l2 = sqrt(ddot3(r2, r2)), l3 = sqrt(ddot3(r3, r3));
+  const double num = fabs(ddot3(r1, dcross3(r2, r3)));
+  const double den = l1 * l2 * l3 + ddot3(r1, r2) * l3 + ddot3(r1, r3) * l2 + ddot3(r2, r3) * l1;
+  return 2.0 * atan2(num, den);
+}
+
+__device__ __forceinline__ float3 sub_target(const DTri& t) {  // fl32(((a+b)+c)/3), no contraction
+  return make_float3(__double2float_rn(__ddiv_rn(__dadd_rn(__dadd_rn(t.a.x, t.b.x), t.c.x), 3.0)),
+                     __double2float_rn(__ddiv_rn(__dadd_rn(__dadd_rn(t.a.y, t.b.y), t.c.y), 3.0)),
+                     __double2float_rn(__ddiv_rn(__dadd_rn(__dadd_rn(t.a.z, t.b.z), t.c.z), 3.0)));
+}
+
+__device__ __forceinline__ DTri patch_tri(const AsmParams& P, int r, int k) {
+  const float4* tv = P.ptri ? P.ptri + 3 * (2 * (int64_t)r + k) : P.tri + 3 * (int64_t)r;
+  DTri t;
+  t.a = f2d(tv[0]); t.b = f2d(tv[1]); t.c = f2d(tv[2]);
+  return t;
+}
+
+constexpr int kAreaThreads = 256;
+
+template <bool COUNT>
+__global__ void __launch_bounds__(kAreaThreads, 2) k_assemble_area(AsmParams P) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kAreaThreads / 32;
+  unsigned long long cnt[6] = {0, 0, 0, 0, 0, 0};
+  const int64_t total = P.n_cols * P.tiles;
+  const int ntri = P.ptri ? 2 : 1;
+  const uint32_t nsub = 1u << (2 * P.area_m);
+  for (int64_t item = (int64_t)blockIdx.x * nw + warp; item < total; item += (int64_t)gridDim.x * nw) {
+    const int64_t c = item / P.tiles, tile = item - c * P.tiles;
+    const int64_t j = P.cols ? P.cols[c] : c;
+    const int r = (int)(tile * 32 + lane);
+    const bool valid = r < P.N;
+    double acc = 0.0;
+    bool pend = false;
+    for (int l = 0; l < P.L; ++l) {
+      const float* pl = P.lamps + 3 * (j * P.L + l);
+      const float ox = pl[0], oy = pl[1], oz = pl[2];
+      bool anyvis = false;
+      if (valid) {
+        const float cx = P.centroid[3 * r], cy = P.centroid[3 * r + 1], cz = P.centroid[3 * r + 2];
+        const float nx = P.normal[3 * r], ny = P.normal[3 * r + 1], nz = P.normal[3 * r + 2];
+        const D3 D = d3((double)cx - (double)ox, (double)cy - (double)oy, (double)cz - (double)oz);
+        const double d = sqrt(ddot3(D, D));
+        const double cosd = -(D.x * (double)nx + D.y * (double)ny + D.z * (double)nz);
+        bool front = cosd > 0.0;  // P:242, the patch's facing (as a4)
+        if (d < kMinDist) { atomicExch(P.err, 1); front = false; }
+        if (front) {
+          const D3 po = d3(ox, oy, oz);
+          for (int k = 0; k < ntri; ++k) {
+            const DTri base = patch_tri(P, r, k);
+            for (uint32_t s = 0; s < nsub; ++s) {
+              const DTri t = sub_tri(base, s, P.area_m);
+              const float3 x = sub_target(t);
+              const float dx = x.x - ox, dy = x.y - oy, dz = x.z - oz;
+              if ((double)dx * dx + (double)dy * dy + (double)dz * dz < kMinDist * kMinDist) {
+                atomicExch(P.err, 1);
+                continue;
+              }
+              if (COUNT) cnt[0] += 1;
+              const int res = lane_walk32<COUNT>(P, ox, oy, oz, dx, dy, dz, r, cnt);
+              if (COUNT && res == kBlocked) cnt[5] += 1;
+              pend |= res == kUndecided;
+              if (res == kClear) {
+                acc += tri_solid_angle(po, t);
+                anyvis = true;
+              }
+            }
+          }
+        }
+      }
+      const uint32_t vm = __ballot_sync(0xffffffffu, anyvis);
+      if (P.vis_bits && lane == 0 && tile < P.words) __stcs(P.vis_bits + (c * P.L + l) * P.words + tile, vm);
+    }
+    const uint32_t pm = __ballot_sync(0xffffffffu, pend);
+    if (lane == 0 && tile < P.words) __stcs(P.pending + c * P.words + tile, pm);
+    if (COUNT) cnt[4] += pend;
+    const float a = valid ? (float)(acc * P.scale / P.area[r]) : 0.f;
+    if (P.values) __stcs(P.values + c * P.ld + r, a);
   }
   if (COUNT)
     for (int k = 0; k < 6; ++k) {
@@ -386,15 +514,37 @@ __device__ void fixup_entry(const AsmParams& P, int64_t c, int r) {
     const double dd = ddot3(D, D);
     const double d = sqrt(dd);
     const double cosd = -(D.x * (double)nx + D.y * (double)ny + D.z * (double)nz);
-    const bool vis = cosd > 0.0 && d >= kMinDist && lane_clear_exact(P, ox, oy, oz, cx, cy, cz, r);
-    if (vis) acc += cosd / (dd * d);
+    bool vis;
+    if (P.area_m >= 0) {  // NEXT-2: every sub-triangle re-traced exactly
+      vis = false;
+      if (cosd > 0.0 && d >= kMinDist) {
+        const D3 po = d3(ox, oy, oz);
+        const uint32_t nsub = 1u << (2 * P.area_m);
+        for (int k = 0; k < (P.ptri ? 2 : 1); ++k) {
+          const DTri base = patch_tri(P, r, k);
+          for (uint32_t s = 0; s < nsub; ++s) {
+            const DTri t = sub_tri(base, s, P.area_m);
+            const float3 x = sub_target(t);
+            const float ex = x.x - ox, ey = x.y - oy, ez = x.z - oz;
+            if ((double)ex * ex + (double)ey * ey + (double)ez * ez < kMinDist * kMinDist) continue;
+            if (lane_clear_exact(P, ox, oy, oz, x.x, x.y, x.z, r)) {
+              acc += tri_solid_angle(po, t);
+              vis = true;
+            }
+          }
+        }
+      }
+    } else {
+      vis = cosd > 0.0 && d >= kMinDist && lane_clear_exact(P, ox, oy, oz, cx, cy, cz, r);
+      if (vis) acc += cosd / (dd * d);
+    }
     if (P.vis_bits) {
       uint32_t* vw = P.vis_bits + (c * P.L + l) * P.words + word;
       if (vis) atomicOr(vw, 1u << b);
       else atomicAnd(vw, ~(1u << b));
     }
   }
-  if (P.values) P.values[c * P.ld + r] = (float)(acc * P.scale);
+  if (P.values) P.values[c * P.ld + r] = (float)(P.area_m >= 0 ? acc * P.scale / P.area[r] : acc * P.scale);
 }
 
 __global__ void k_fixup_collect(AsmParams P, uint64_t* __restrict__ list, int64_t cap,
@@ -487,6 +637,16 @@ extern "C" int uvd_irradiance_matrix(const uvd_scene* s, const float* lamp_xyz, 
     set_error("uvd_irradiance_matrix: need power_w > 0 and samples_per_config >= 1");
     return UVD_ERR_INVALID;
   }
+  const bool area_model = lamp->model == UVD_MODEL_AREA;
+  if ((lamp->model != UVD_MODEL_CENTROID && !area_model) ||
+      (area_model && (lamp->subdiv < 0 || lamp->subdiv > 6))) {
+    set_error("uvd_irradiance_matrix: model must be CENTROID or AREA with 0 <= subdiv <= 6");
+    return UVD_ERR_INVALID;
+  }
+  if (area_model && (out->format == UVD_CSC || (s->kind == UVD_SCENE_EXTRUDED && !s->ptri) || !UVD_ROWS_DFS)) {
+    set_error("uvd_irradiance_matrix: the AREA model needs dense output");
+    return UVD_ERR_INVALID;
+  }
   if (!cols) n_cols = k_total;
   if (n_cols < 0 || k_total < 0) { set_error("uvd_irradiance_matrix: negative size"); return UVD_ERR_INVALID; }
   if (cols)
@@ -532,6 +692,9 @@ extern "C" int uvd_irradiance_matrix(const uvd_scene* s, const float* lamp_xyz, 
   P.ld = csc ? P.words * 32 : out->ld;
   P.counters = out->counters;
   P.err = s->err_flag;
+  P.area = s->area;
+  P.ptri = s->kind == UVD_SCENE_EXTRUDED ? s->ptri : nullptr;
+  P.area_m = area_model ? lamp->subdiv : -1;
   // scratch: column ids, undecided-entry bits, visibility bits for CSC
   int64_t* dcols = nullptr;
   uint32_t* vis_scratch = nullptr;
@@ -557,8 +720,22 @@ extern "C" int uvd_irradiance_matrix(const uvd_scene* s, const float* lamp_xyz, 
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_assemble_lane<true>, kAsmThreads, 0);
     grid_c = std::max(1, sms * std::max(per, 1));
   }
-  if (P.counters) k_assemble_lane<true><<<grid_c, kAsmThreads, 0, st>>>(P);
-  else k_assemble_lane<false><<<grid, kAsmThreads, 0, st>>>(P);
+  if (area_model) {
+    static int grid_a = 0;
+    if (!grid_a) {
+      int dev = 0, sms = 0, per = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_assemble_area<false>, kAreaThreads, 0);
+      grid_a = std::max(1, sms * std::max(per, 1));
+    }
+    if (P.counters) k_assemble_area<true><<<grid_a, kAreaThreads, 0, st>>>(P);
+    else k_assemble_area<false><<<grid_a, kAreaThreads, 0, st>>>(P);
+  } else if (P.counters) {
+    k_assemble_lane<true><<<grid_c, kAsmThreads, 0, st>>>(P);
+  } else {
+    k_assemble_lane<false><<<grid, kAsmThreads, 0, st>>>(P);
+  }
   note_launch();
   {  // exact fp64 re-trace of the (rare) entries the fp32 pass left undecided
     int dev = 0, sms = 148;

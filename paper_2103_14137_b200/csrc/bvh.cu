@@ -349,9 +349,7 @@ __global__ void k_emit_small(const float4* __restrict__ tri, int64_t n, Node* no
 // internal node, and the surviving clusters are compacted in order.  Yields a
 // tree of markedly better SAH quality than the Karras LBVH (fewer node visits
 // per shadow ray), in the same (left, right, range, box) arrays.
-#ifndef UVD_ROWS_DFS
-#define UVD_ROWS_DFS 1
-#endif
+
 #ifndef UVD_PLOC_RADIUS
 #define UVD_PLOC_RADIUS 16
 #endif

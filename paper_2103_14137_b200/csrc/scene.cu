@@ -403,7 +403,7 @@ static int create_extruded(uvd_scene* s, const uvd_scene_desc* d, cudaStream_t s
   UVD_TRY(build_bvh(s, tri_in, nullptr, st));
   // pageable H2D copies above may still read the host vectors: finish first
   UVD_CUDA_TRY(cudaStreamSynchronize(st));
-  al.put(tri_in);
+  s->ptri = tri_in;  // patch-ordered wall triangles (2 per patch) for the area model (NEXT-2)
   return UVD_OK;
 }
 
@@ -412,7 +412,7 @@ static void free_scene(uvd_scene* s) {
   Alloc& al = s->alloc;
   for (void* p : {(void*)s->centroid, (void*)s->normal, (void*)s->area, (void*)s->orig_id,
                   (void*)s->tri, (void*)s->nodes, (void*)s->walls, (void*)s->poly_xy,
-                  (void*)s->poly_off, (void*)s->err_flag, (void*)s->cov_part})
+                  (void*)s->poly_off, (void*)s->err_flag, (void*)s->cov_part, (void*)s->ptri})
     al.put(p);
   cudaStreamSynchronize(al.stream);
   delete s;

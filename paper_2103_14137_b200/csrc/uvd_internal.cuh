@@ -44,7 +44,10 @@ constexpr double kParallel = 1e-12;   // |det| <= 1e-12 |D||E1xE2| -> no crossin
 #ifndef UVD_LEAF_MAX
 #define UVD_LEAF_MAX 2
 #endif
-constexpr int kLeafMax = UVD_LEAF_MAX;  // triangles per BVH leaf (subtree collapse), <= 8
+constexpr int kLeafMax = UVD_LEAF_MAX;
+#ifndef UVD_ROWS_DFS
+#define UVD_ROWS_DFS 1  // 3D rows follow the BVH leaf (DFS) order: row r = leaf-ordered triangle r
+#endif  // triangles per BVH leaf (subtree collapse), <= 8
 constexpr int kCovBlocksMax = 1024;   // coverage partial sums (fixed, deterministic order)
 // Q20 free-space test direction (tilted off the axes).
 constexpr double kFreeDirX = 0.0123, kFreeDirY = 0.0371, kFreeDirZ = 1.0;
@@ -99,6 +102,7 @@ struct uvd_scene {
   int64_t* orig_id = nullptr; // N
   // BVH (device)
   float4* tri = nullptr;      // M*3: (v0, owner patch), (v1, orig tri), (v2, 0)  leaf order
+  float4* ptri = nullptr;     // EXTRUDED only: 2N*3 patch-ordered wall triangles (area model)
   uvd::Node* nodes = nullptr; // max(M-1, 1) BVH2 nodes
   uint32_t root = 0;          // root ref
   // 2.5D description (device + host copies) for the floorplan vantage test

@@ -58,7 +58,8 @@ class _VantageOpts(C.Structure):
 
 
 class _Lamp(C.Structure):
-    _fields_ = [("power_w", C.c_double), ("samples_per_config", C.c_int32)]
+    _fields_ = [("power_w", C.c_double), ("samples_per_config", C.c_int32), ("model", C.c_int32),
+                ("subdiv", C.c_int32)]
 
 
 class _MatrixOut(C.Structure):
@@ -272,7 +273,7 @@ class Scene:
 
     def irradiance(self, lamps: torch.Tensor, cols=None, power_w: float = 80.0, vis_bits: bool = False,
                    col_sumsq: bool = False, counters: bool = False, out: torch.Tensor | None = None,
-                   stream=None) -> dict:
+                   stream=None, area_subdiv: int | None = None) -> dict:
         """uvd_irradiance_matrix (dense column-major).  lamps: (K_total, L, 3)
         fp32 on the device; cols: None or a host sequence of global column ids.
         Returns dict(A=(n_cols, ld) fp32, [vis_bits (n_cols, L, words) int32],
@@ -307,7 +308,8 @@ class Scene:
             ct = torch.zeros(6, dtype=torch.int64, device=dev)
             m.counters = ct.data_ptr()
             res["counters"] = ct
-        lamp = _Lamp(float(power_w), int(L))
+        lamp = _Lamp(float(power_w), int(L), 0 if area_subdiv is None else 1,
+                     0 if area_subdiv is None else int(area_subdiv))
         _check(lib().uvd_irradiance_matrix(
             self.handle, _ptr(lamps), K,
             ccols.ctypes.data_as(C.c_void_p) if ccols is not None else None, n_cols,
