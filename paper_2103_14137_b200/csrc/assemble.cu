@@ -273,10 +273,16 @@ __device__ __forceinline__ DTri patch_tri(const AsmParams& P, int r, int k) {
   return t;
 }
 
-constexpr int kAreaThreads = 256;
+#ifndef UVD_AREA_THREADS
+#define UVD_AREA_THREADS 1024
+#endif
+#ifndef UVD_AREA_MINB
+#define UVD_AREA_MINB 1
+#endif
+constexpr int kAreaThreads = UVD_AREA_THREADS;
 
 template <bool COUNT>
-__global__ void __launch_bounds__(kAreaThreads, 2) k_assemble_area(AsmParams P) {
+__global__ void __launch_bounds__(kAreaThreads, UVD_AREA_MINB) k_assemble_area(AsmParams P) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kAreaThreads / 32;
   unsigned long long cnt[6] = {0, 0, 0, 0, 0, 0};
   const int64_t total = P.n_cols * P.tiles;
@@ -302,12 +308,11 @@ __global__ void __launch_bounds__(kAreaThreads, 2) k_assemble_area(AsmParams P) 
         bool front = cosd > 0.0;  // P:242, the patch's facing (as a4)
         if (d < kMinDist) { atomicExch(P.err, 1); front = false; }
         if (front) {
-          const D3 po = d3(ox, oy, oz);
           for (int k = 0; k < ntri; ++k) {
-            const DTri base = patch_tri(P, r, k);
             for (uint32_t s = 0; s < nsub; ++s) {
-              const DTri t = sub_tri(base, s, P.area_m);
-              const float3 x = sub_target(t);
+              // the sub-triangle is rebuilt after the walk rather than kept live
+              // across it (the traversal needs the registers)
+              const float3 x = sub_target(sub_tri(patch_tri(P, r, k), s, P.area_m));
               const float dx = x.x - ox, dy = x.y - oy, dz = x.z - oz;
               if ((double)dx * dx + (double)dy * dy + (double)dz * dz < kMinDist * kMinDist) {
                 atomicExch(P.err, 1);
@@ -318,7 +323,8 @@ __global__ void __launch_bounds__(kAreaThreads, 2) k_assemble_area(AsmParams P) 
               if (COUNT && res == kBlocked) cnt[5] += 1;
               pend |= res == kUndecided;
               if (res == kClear) {
-                acc += tri_solid_angle(po, t);
+                asm volatile("" ::: "memory");
+                acc += tri_solid_angle(d3(ox, oy, oz), sub_tri(patch_tri(P, r, k), s, P.area_m));
                 anyvis = true;
               }
             }

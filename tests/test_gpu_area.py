@@ -151,3 +151,30 @@ def test_area_model_rejects_csc_and_bad_level(uvd):
     rc = uvd.lib().uvd_irradiance_matrix(sc.handle, uvd._ptr(lam), lam.shape[0], None, lam.shape[0],
                                          C.byref(lamp), C.byref(m), uvd._stream())
     assert rc == uvd.UVD_ERR_INVALID
+
+
+def test_area_c4_floatbot_sampled(uvd):
+    """The area model at C4 size (the timing configuration): sampled pairs
+    against the brute-force oracle (oracle's own vantage samples)."""
+    desc = configs.c4_scene()
+    sc = uvd.Scene(desc)
+    lamps, raw = sc.vantage(configs.FLOAT_OPTS)
+    K = lamps.shape[0]
+    cols = np.arange(0, K, 64)
+    r = sc.irradiance(lamps, cols=list(cols), area_subdiv=1)
+    sc.sync_status()
+    orig = sc.patches()["orig_id"].cpu().numpy()
+    rng = np.random.default_rng(3)
+    ri = rng.integers(0, sc.N, 300)
+    ci = rng.integers(0, len(cols), 300)
+    got = r["A"][torch.from_numpy(ci).cuda(), torch.from_numpy(ri).cuda()].double().cpu().numpy()
+    uc = np.unique(ci)
+    v = O.vantage(desc, configs.FLOAT_OPTS, idx=raw.cpu().numpy()[cols[uc]])
+    lam_o = np.zeros((len(cols), 1, 3), np.float32)
+    lam_o[uc] = v["samples"]
+    assert np.array_equal(lam_o[uc], lamps.cpu().numpy()[cols[uc]])
+    ref = O.irradiance_area_pairs(O.scene_patches(desc), lam_o, orig[ri], ci, m=1)
+    ok = ~ref["deg"]
+    assert ok.mean() > 0.98
+    assert (np.abs(got[ok] - ref["A"][ok]) <= REL * ref["A"][ok] + 1e-30).all()
+    assert 0.05 < (got[ok] > 0).mean() < 0.95

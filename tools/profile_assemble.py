@@ -1,6 +1,7 @@
 """Run k_assemble on a column subset of a workload (for ncu captures).
 
 usage: python tools/profile_assemble.py [C5|C4-float|C4-tower] [n_cols] [repeats]
+env: CONTIG=1 contiguous middle columns; AREA=m the NEXT-2 area model at subdivision m
 """
 import os
 import sys
@@ -27,14 +28,15 @@ else:
     step = max(1, K // n_cols)
     cols = list(range(0, K, step))[:n_cols]
 A = torch.empty((len(cols), sc.ld()), dtype=torch.float32, device="cuda")
+area = int(os.environ["AREA"]) if os.environ.get("AREA") else None
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
 for r in range(reps):
     e0.record()
-    sc.irradiance(lamps, cols=cols, out=A)
+    sc.irradiance(lamps, cols=cols, out=A, area_subdiv=area)
     e1.record()
     torch.cuda.synchronize()
     print(f"rep {r}: {e0.elapsed_time(e1):.2f} ms for {len(cols)} cols x {sc.N} rows "
           f"= {len(cols) * sc.N / e0.elapsed_time(e1) / 1e6:.3f} G entries/s")
 sc.sync_status()
-r = sc.irradiance(lamps, cols=cols, out=A, counters=True)
+r = sc.irradiance(lamps, cols=cols, out=A, counters=True, area_subdiv=area)
 print("counters (rays, box tests, tri tests, node fetches, fp64 fixups, cache hits):", r["counters"].tolist())
