@@ -255,6 +255,20 @@ UVD_API int uvd_fluence(const uvd_matrix_out* A, int64_t n, int64_t k, int trans
 UVD_API int uvd_coverage(const uvd_scene* scene, const double* mu, double mu_min, const double* a_rowsum,
                  double out[3], void* stream);
 
+/* ------------------------------------------------------------------ NEXT-4 */
+/* Static single-point baseline (P:7, "places the disinfection light to
+ * have maximum coverage over the obstacle space, allowing it to irradiate the
+ * surfaces for as long as necessary"; P:53 the static Towerbot
+ * for a time budget).  For each local column j of a dense A (n = scene N rows):
+ *   out[3j]   = Σ_i |s_i| [A_ij > 0]            visible area (m²)
+ *   out[3j+1] = min_{i: A_ij > 0} A_ij           (+inf if none): dwell to cover
+ *               every visible patch = μ_min / out[3j+1] (s)
+ *   out[3j+2] = Σ_i |s_i| [A_ij · t_budget ≥ μ_min]  area covered in t_budget
+ * out: DEVICE fp64 [3k].  The caller picks the column (maximum visible area,
+ * reading Q24 for ties).  Deterministic.  Asynchronous. */
+UVD_API int uvd_static_columns(const uvd_scene* scene, const uvd_matrix_out* A, int64_t k, double t_budget,
+                       double mu_min, double* out, void* stream);
+
 /* ------------------------------------------------------------------ NEXT-1 */
 /* Relaxed dwell-time LP, Eq. 9 (§IV-D first stage):
  *   minimise Σ_k t_k + Σ_i p_i σ_i

@@ -360,3 +360,25 @@ def coverage(mu: np.ndarray, area: np.ndarray, mu_min: float = 280.0,
     total = float(area.sum())
     vis_total = float(area[np.asarray(rowsum) > 0].sum()) if rowsum is not None else total
     return np.array([covered, total, vis_total])
+
+
+# --------------------------------------------------------------------------- #
+# NEXT-4 — static single-point baseline                                        #
+# --------------------------------------------------------------------------- #
+def static_baseline(A: np.ndarray, area: np.ndarray, t_budget: float = 1800.0, mu_min: float = 280.0) -> dict:
+    """The paper's static illumination strategy (P:7):
+    put the lamp at the vantage configuration whose visible patch area is
+    largest and leave it until every visible patch has μ_min, i.e. for
+    max_i μ_min / A_ij over the visible patches; ties (equal visible area) go
+    to the shorter dwell, then the lower index (reading Q24).  Also the area a
+    static lamp covers within `t_budget` at each configuration.
+    A: (N, K) in W/m²."""
+    A = np.asarray(A, np.float64)
+    N, K = A.shape
+    vis = np.array([area[A[:, j] > 0].sum() for j in range(K)])
+    mn = np.array([A[A[:, j] > 0, j].min() if (A[:, j] > 0).any() else np.inf for j in range(K)])
+    cov = np.array([area[A[:, j] * t_budget >= mu_min].sum() for j in range(K)])
+    dwell = np.array([mu_min / m if np.isfinite(m) else np.inf for m in mn])
+    best = min(range(K), key=lambda j: (-vis[j], dwell[j], j))
+    return dict(visible_area=vis, min_irradiance=mn, covered_at_budget=cov, column=best, dwell_s=dwell[best],
+                best_budget_column=min(range(K), key=lambda j: (-cov[j], j)))

@@ -190,6 +190,40 @@ __global__ void k_coverage_final(const double* __restrict__ part, int nb, double
   }
 }
 
+// NEXT-4 static single-point baseline (P:7): per
+// column j of a dense shard, out[3j..3j+2] = {Σ_i |s_i| [A_ij > 0] (visible
+// area), min_{A_ij > 0} A_ij (+inf if none), Σ_i |s_i| [A_ij·T ≥ μ_min]
+// (area covered by a static lamp left at j for T)}.  One block per column
+// (contiguous column reads), fixed-order reduction.
+constexpr int kStaticThreads = 256;
+__global__ void __launch_bounds__(kStaticThreads) k_static_cols(const float* __restrict__ A, int64_t ld, int64_t n,
+                                                                const double* __restrict__ area, double t_budget,
+                                                                double mu_min, double* __restrict__ out) {
+  const int64_t c = blockIdx.x;
+  const float* col = A + c * ld;
+  double vis = 0.0, cov = 0.0, mn = INFINITY;
+  for (int64_t i = threadIdx.x; i < n; i += kStaticThreads) {
+    const double a = (double)__ldcs(col + i);
+    if (a > 0.0) {
+      vis += area[i];
+      mn = fmin(mn, a);
+      if (a * t_budget >= mu_min) cov += area[i];  // inclusive (Q16)
+    }
+  }
+  __shared__ double s[3][kStaticThreads];
+  s[0][threadIdx.x] = vis; s[1][threadIdx.x] = mn; s[2][threadIdx.x] = cov;
+  __syncthreads();
+  for (int o = kStaticThreads / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      s[0][threadIdx.x] += s[0][threadIdx.x + o];
+      s[1][threadIdx.x] = fmin(s[1][threadIdx.x], s[1][threadIdx.x + o]);
+      s[2][threadIdx.x] += s[2][threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x < 3) out[3 * c + threadIdx.x] = s[threadIdx.x][0];
+}
+
 }  // namespace uvd
 
 using namespace uvd;
@@ -310,5 +344,24 @@ extern "C" int uvd_coverage(const uvd_scene* s, const double* mu, double mu_min,
   UVD_CUDA_TRY(cudaStreamSynchronize(st));
   UVD_CUDA_TRY(cudaGetLastError());
   out[0] = h[0]; out[1] = h[1]; out[2] = h[2];
+  return UVD_OK;
+}
+
+extern "C" int uvd_static_columns(const uvd_scene* s, const uvd_matrix_out* A, int64_t k, double t_budget,
+                                  double mu_min, double* out, void* stream) {
+  clear_error();
+  if (!s || !A || !out || k < 0 || !(mu_min > 0.0) || !(t_budget >= 0.0)) {
+    set_error("uvd_static_columns: bad argument");
+    return UVD_ERR_INVALID;
+  }
+  if (A->format != UVD_DENSE_COLMAJOR || !A->values || A->ld < s->N) {
+    set_error("uvd_static_columns: needs a dense A with ld >= N");
+    return UVD_ERR_INVALID;
+  }
+  if (k == 0) return UVD_OK;
+  cudaStream_t st = (cudaStream_t)stream;
+  k_static_cols<<<(unsigned)k, kStaticThreads, 0, st>>>(A->values, A->ld, s->N, s->area, t_budget, mu_min, out);
+  note_launch();
+  UVD_CUDA_TRY(cudaGetLastError());
   return UVD_OK;
 }

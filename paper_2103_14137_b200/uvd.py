@@ -112,6 +112,8 @@ def lib():
                                   C.c_void_p, C.c_void_p]
         L.uvd_coverage.argtypes = [C.c_void_p, C.c_void_p, C.c_double, C.c_void_p,
                                    C.POINTER(C.c_double), C.c_void_p]
+        L.uvd_static_columns.argtypes = [C.c_void_p, C.POINTER(_MatrixOut), C.c_int64, C.c_double, C.c_double,
+                                         C.c_void_p, C.c_void_p]
         L.uvd_lp_solve.argtypes = [C.POINTER(_MatrixOut), C.c_int64, C.c_int64, C.POINTER(_LpOpts),
                                    C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(_LpResult), C.c_void_p]
         L.uvd_last_error.restype = C.c_char_p
@@ -123,7 +125,7 @@ def lib():
 
 EXPORTS = ("uvd_scene_create", "uvd_scene_query", "uvd_scene_patches", "uvd_scene_destroy",
            "uvd_vantage_sample", "uvd_irradiance_matrix", "uvd_sync_status", "uvd_fluence",
-           "uvd_coverage", "uvd_lp_solve", "uvd_last_error", "uvd_version", "uvd_launch_count")
+           "uvd_coverage", "uvd_static_columns", "uvd_lp_solve", "uvd_last_error", "uvd_version", "uvd_launch_count")
 
 
 def _check(rc):
@@ -365,6 +367,26 @@ class Scene:
 
     def sync_status(self, stream=None):
         _check(lib().uvd_sync_status(self.handle, _stream(stream)))
+
+    def static_baseline(self, A: torch.Tensor, t_budget: float = 1800.0, mu_min: float = 280.0,
+                        stream=None) -> dict:
+        """NEXT-4 static single-point baseline (uvd_static_columns) on a dense
+        (k, ld) A: per-column visible area, min positive entry and area covered
+        in t_budget; the chosen column maximises the visible area, ties broken
+        by the smaller dwell μ_min / min A, then the lower index (reading Q24)."""
+        k = A.shape[0]
+        out = torch.empty((k, 3), dtype=torch.float64, device=A.device)
+        m = _dense_desc(A)
+        _check(lib().uvd_static_columns(self.handle, C.byref(m), k, float(t_budget), float(mu_min),
+                                        _ptr(out), _stream(stream)))
+        o = out.cpu().numpy()
+        vis, mn, cov = o[:, 0], o[:, 1], o[:, 2]
+        dwell = np.where(np.isfinite(mn), mu_min / np.where(np.isfinite(mn), mn, 1.0), np.inf)
+        order = np.lexsort((np.arange(k), dwell, -vis))
+        j = int(order[0]) if k else -1
+        return {"visible_area": vis, "min_irradiance": mn, "covered_at_budget": cov, "column": j,
+                "dwell_s": float(dwell[j]) if k else float("inf"),
+                "best_budget_column": int(np.lexsort((np.arange(k), -cov))[0]) if k else -1}
 
     def coverage(self, mu: torch.Tensor, mu_min: float = 280.0, rowsum: torch.Tensor | None = None,
                  stream=None) -> np.ndarray:

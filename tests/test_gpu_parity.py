@@ -552,3 +552,28 @@ def test_fluence_large_sparse(uvd):
         e[i] = 1.0
         assert torch.equal(uvd.fluence(A, N, e, transpose=True), A[:, i].double())
 
+
+
+# ------------------------------------------------------------------ NEXT-4 ---
+@pytest.mark.parametrize("seed", [0, 7])
+def test_static_baseline_matches_oracle(uvd, seed):
+    """uvd_static_columns on the GPU's A against the oracle's definition on the
+    oracle's own A (C2 worlds): visible areas and chosen configuration equal,
+    dwell within 1e-5, budget coverage equal away from the μ_min threshold."""
+    c = configs.c2(seed)
+    sc = uvd.Scene(c["scene"])
+    lamps, raw = sc.vantage(c["vantage"])
+    A = sc.irradiance(lamps)["A"]
+    sc.sync_status()
+    g = sc.static_baseline(A, t_budget=configs.T_MAX)
+    pat = O.extruded_patches(c["scene"])
+    ref_A = O.irradiance_matrix(pat, oracle_lamps(c["scene"], c["vantage"], lamps, raw), mode="2d")
+    assert not ref_A["deg"].any()
+    ref = O.static_baseline(ref_A["A"], pat["area"], t_budget=configs.T_MAX)
+    assert np.allclose(g["visible_area"], ref["visible_area"], rtol=1e-12)
+    assert g["column"] == ref["column"]
+    assert abs(g["dwell_s"] - ref["dwell_s"]) <= 1e-5 * ref["dwell_s"]
+    near = np.abs(ref_A["A"] * configs.T_MAX - configs.MU_MIN) <= 1e-5 * configs.MU_MIN
+    slack = (pat["area"][:, None] * near).sum(0)
+    assert (np.abs(g["covered_at_budget"] - ref["covered_at_budget"]) <= slack + 1e-9).all()
+    assert 0 < g["visible_area"].max() < pat["area"].sum()
