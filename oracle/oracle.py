@@ -75,6 +75,11 @@ def lib():
         L.orc_irradiance_area.argtypes = [C.c_int, _f32p, _i32p, C.c_int64, _f32p, C.c_int64, _f32p, _i64p,
                                           _i32p, _f32p, _f32p, _f64p, _f32p, C.c_int, C.c_double, C.c_int,
                                           _i64p, _i64p, C.c_int64, _f64p, _u8p, _i32p, _i32p, C.c_int]
+        L.orc_cubemap.restype = None
+        L.orc_cubemap.argtypes = [_f32p, _i32p, C.c_int64, C.c_int64, _f32p, C.c_int, C.c_double, C.c_int,
+                                  _i64p, C.c_int64, _f64p, C.c_void_p, C.c_void_p, _f64p, C.c_int]
+        L.orc_pixel_solid_angle.restype = C.c_double
+        L.orc_pixel_solid_angle.argtypes = [C.c_int, C.c_int, C.c_int]
         L.orc_solid_angle.restype = C.c_double
         L.orc_solid_angle.argtypes = [_f64p, _f64p, _f64p, _f64p]
         _lib = L
@@ -382,3 +387,38 @@ def static_baseline(A: np.ndarray, area: np.ndarray, t_budget: float = 1800.0, m
     best = min(range(K), key=lambda j: (-vis[j], dwell[j], j))
     return dict(visible_area=vis, min_irradiance=mn, covered_at_budget=cov, column=best, dwell_s=dwell[best],
                 best_budget_column=min(range(K), key=lambda j: (-cov[j], j)))
+
+
+# --------------------------------------------------------------------------- #
+# NEXT-3 — the paper's visibility cube                                          #
+# --------------------------------------------------------------------------- #
+def pixel_solid_angle(R: int, a: int, b: int) -> float:
+    """Exact solid angle of cube-face pixel (a, b) of an R×R face."""
+    return float(lib().orc_pixel_solid_angle(int(R), int(a), int(b)))
+
+
+def cubemap(patches: dict, lamps: np.ndarray, cols=None, R: int = 32, P: float = 80.0, hits: bool = False,
+            n_threads: int = 0) -> dict:
+    """The paper's §IV-C pipeline by brute force: per lamp sample 6
+    R×R cube faces, each pixel's nearest triangle (closest hit) receives the
+    pixel's power (P/L)·Ω_px/(4π) when front-facing; A = F/|s|.
+    Returns A (N, n_cols), F, the energy on degenerate pixels per column and,
+    with hits=True, per-pixel winner ids (n_cols, L, 6, R, R) (-1 none,
+    -2 back-facing) and degeneracy flags."""
+    lamps = np.ascontiguousarray(lamps, np.float32)
+    K, L = lamps.shape[0], lamps.shape[1]
+    cols = np.arange(K, dtype=np.int64) if cols is None else np.ascontiguousarray(cols, np.int64)
+    n, N = len(cols), patches["N"]
+    F = np.zeros(n * N, np.float64)
+    deg_e = np.zeros(n, np.float64)
+    hit = np.zeros(n * L * 6 * R * R, np.int32) if hits else None
+    deg = np.zeros(n * L * 6 * R * R, np.uint8) if hits else None
+    lib().orc_cubemap(patches["tri"], patches["tri_patch"], len(patches["tri"]), N, lamps.reshape(-1), L, P, R,
+                      cols, n, F, hit.ctypes.data if hits else None, deg.ctypes.data if hits else None, deg_e,
+                      n_threads)
+    F = F.reshape(n, N).T
+    out = dict(A=F / patches["area"][:, None], F=F, deg_energy=deg_e)
+    if hits:
+        out["hit"] = hit.reshape(n, L, 6, R, R)
+        out["deg"] = deg.reshape(n, L, 6, R, R).astype(bool)
+    return out

@@ -727,3 +727,122 @@ int orc_irradiance_area(int mode, const float* tri, const int32_t* tri_patch, in
 double orc_solid_angle(const double* p, const double* a, const double* b, const double* c) {
   return solid_angle(mk(p[0], p[1], p[2]), mk(a[0], a[1], a[2]), mk(b[0], b[1], b[2]), mk(c[0], c[1], c[2]));
 }
+
+/* ======================================================================== */
+/* NEXT-3 — the paper's visibility-cube method                   */
+/* ======================================================================== */
+/* Per lamp sample the scene is "rendered" into 6 cube faces of R×R pixels
+ * ("six ... cameras": 512²).  Face f has the ray directions
+ *   +X (1,u,v)  −X (−1,u,v)  +Y (u,1,v)  −Y (u,−1,v)  +Z (u,v,1)  −Z (u,v,−1)
+ * with pixel (a,b) centre u = −1 + (2a+1)/R, v = −1 + (2b+1)/R.  Each pixel
+ * carries the power e = (P/L)·Ω_px/(4π) of its exact solid angle (the paper's
+ * precomputed emission texture E):
+ *   Ω_px = G(u1,v1) − G(u0,v1) − G(u1,v0) + G(u0,v0),  G(u,v) = atan(uv/√(1+u²+v²)),
+ * so each face holds P/(6L).  The pixel's nearest surface (the Z-buffer)
+ * is the closest triangle hit by the ray (fp64 Möller–Trumbore, t > 0, inclusive
+ * edges, ties to the lower triangle index); its patch receives e when the hit
+ * is front-facing, and A[i,j] = F_i/|s_i|.  A pixel is flagged
+ * degenerate when the winner's barycentric margin is < 1e-6 or the runner-up
+ * hit is within 1e-9·t of it. */
+static double px_G(double u, double v) { return atan(u * v / sqrt(1.0 + u * u + v * v)); }
+
+double orc_pixel_solid_angle(int R, int a, int b) {
+  double u0 = -1.0 + 2.0 * a / R, u1 = -1.0 + 2.0 * (a + 1) / R;
+  double v0 = -1.0 + 2.0 * b / R, v1 = -1.0 + 2.0 * (b + 1) / R;
+  return px_G(u1, v1) - px_G(u0, v1) - px_G(u1, v0) + px_G(u0, v0);
+}
+
+static v3 px_dir(int f, int R, int a, int b) {
+  double u = -1.0 + (2.0 * a + 1.0) / R, v = -1.0 + (2.0 * b + 1.0) / R;
+  switch (f) {
+    case 0: return mk(1.0, u, v);
+    case 1: return mk(-1.0, u, v);
+    case 2: return mk(u, 1.0, v);
+    case 3: return mk(u, -1.0, v);
+    case 4: return mk(u, v, 1.0);
+    default: return mk(u, v, -1.0);
+  }
+}
+
+/* closest-hit of the ray O + t D (t > 0) against triangle V0V1V2: t (or -1) and
+ * the barycentric margin min(u, v, 1-u-v) */
+static double ray_hit(v3 O, v3 D, v3 V0, v3 V1, v3 V2, double* margin, int* front) {
+  v3 E1 = sub(V1, V0), E2 = sub(V2, V0);
+  v3 P = cross(D, E2);
+  double det = dot(E1, P);
+  v3 Nrm = cross(E1, E2);
+  if (fabs(det) <= ORC_PAR * norm(D) * norm(Nrm)) return -1.0;
+  double inv = 1.0 / det;
+  v3 T = sub(O, V0);
+  double u = dot(T, P) * inv;
+  v3 Q = cross(T, E1);
+  double v = dot(D, Q) * inv;
+  double m = dmin(u, dmin(v, 1.0 - u - v));
+  if (m < 0.0) return -1.0;
+  double t = dot(E2, Q) * inv;
+  if (!(t > 0.0)) return -1.0;
+  *margin = m;
+  *front = dot(D, Nrm) < 0.0;
+  return t;
+}
+
+typedef struct {
+  const float* tri; const int32_t* tri_patch; int64_t M; int64_t N;
+  const float* lamps; int L; double P; int R;
+  const int64_t* cols; int64_t n_cols;
+  double* F;          /* [n_cols][N] flux */
+  int32_t* hit;       /* optional [n_cols][L][6][R][R] winning triangle (-1 none, -2 back-facing) */
+  uint8_t* deg;       /* optional, same shape */
+  double* deg_e;      /* [n_cols] energy on degenerate pixels */
+} cube_ctx;
+
+/* one task = one (column, lamp sample, face) */
+static void cube_task(int64_t q, void* vctx) {
+  cube_ctx* c = (cube_ctx*)vctx;
+  int64_t cl = q / (6 * (int64_t)c->L);
+  int l = (int)((q / 6) % c->L), f = (int)(q % 6);
+  int64_t j = c->cols[cl];
+  v3 O = ld3(c->lamps + 3 * (j * c->L + l));
+  for (int b = 0; b < c->R; ++b)
+    for (int a = 0; a < c->R; ++a) {
+      v3 D = px_dir(f, c->R, a, b);
+      double best = INFINITY, second = INFINITY, bm = 0.0;
+      int64_t bk = -1;
+      int bfront = 0;
+      for (int64_t k = 0; k < c->M; ++k) {
+        const float* t = c->tri + 9 * k;
+        double m; int fr;
+        double th = ray_hit(O, D, ld3(t), ld3(t + 3), ld3(t + 6), &m, &fr);
+        if (th < 0.0) continue;
+        if (th < best) { second = best; best = th; bk = k; bm = m; bfront = fr; }
+        else if (th < second) second = th;
+      }
+      double e = (c->P / c->L) * orc_pixel_solid_angle(c->R, a, b) / (4.0 * M_PI);
+      int64_t o = (((cl * c->L + l) * 6 + f) * c->R + b) * (int64_t)c->R + a;
+      int dg = bk >= 0 && (bm < ORC_DEG || second - best <= 1e-9 * best);
+      if (c->hit) c->hit[o] = bk < 0 ? -1 : (bfront ? (int32_t)bk : -2);
+      if (c->deg) c->deg[o] = (uint8_t)dg;
+      if (bk >= 0 && bfront) {
+        int64_t i = c->tri_patch[bk];
+        /* faces of one column run as concurrent tasks: atomic fp64 add */
+        double* dst = c->F + cl * c->N + i;
+        double old = *dst, nw;
+        do { nw = old + e; } while (!__atomic_compare_exchange(dst, &old, &nw, 0, __ATOMIC_RELAXED, __ATOMIC_RELAXED));
+        if (dg) {
+          double* de = c->deg_e + cl;
+          double o2 = *de, n2;
+          do { n2 = o2 + e; } while (!__atomic_compare_exchange(de, &o2, &n2, 0, __ATOMIC_RELAXED, __ATOMIC_RELAXED));
+        }
+      }
+    }
+}
+
+/* F[n_cols][N] (zeroed by the caller) gets the flux of every column; hit/deg
+ * optional per-pixel outputs.  Summation order across faces is not fixed
+ * (parallel tasks): F is exact up to fp64 rounding order. */
+void orc_cubemap(const float* tri, const int32_t* tri_patch, int64_t M, int64_t N, const float* lamps, int L,
+                 double P, int R, const int64_t* cols, int64_t n_cols, double* F, int32_t* hit, uint8_t* deg,
+                 double* deg_e, int n_threads) {
+  cube_ctx c = {tri, tri_patch, M, N, lamps, L, P, R, cols, n_cols, F, hit, deg, deg_e};
+  orc_parallel_for(n_cols * L * 6, n_threads, cube_task, &c);
+}
