@@ -255,6 +255,23 @@ UVD_API int uvd_fluence(const uvd_matrix_out* A, int64_t n, int64_t k, int trans
 UVD_API int uvd_coverage(const uvd_scene* scene, const double* mu, double mu_min, const double* a_rowsum,
                  double out[3], void* stream);
 
+/* ------------------------------------------------------------------ NEXT-3 */
+/* The paper's own irradiance pipeline, the "visibility cube" (P:244–250,
+ * P:364), for a head-to-head comparison with uvd_irradiance_matrix: per lamp
+ * sample 6 cube faces of face_res² pixels (512), face f of pixel (a,b)
+ * looking along +X (1,u,v), −X (−1,u,v), +Y (u,1,v), −Y (u,−1,v), +Z (u,v,1),
+ * −Z (u,v,−1) with u = −1 + (2a+1)/R, v = −1 + (2b+1)/R; each pixel carries
+ * e = (P/L)·Ω_px/(4π), Ω_px its exact solid angle (the emission texture E,
+ * P:250); the pixel's nearest surface (closest triangle hit, ties to the lower
+ * input triangle index; the Z-buffer) receives e if front-facing;
+ * A[i,j] = F_i/|s_i|.  Dense output only.  hits (optional, DEVICE
+ * int32 [n_cols][L][6][R][R]): the winning input triangle per pixel, −1 none,
+ * −2 back-facing (for tests).  Flux sums use fp64 atomics (order not fixed).
+ * Asynchronous. */
+UVD_API int uvd_cubemap_matrix(const uvd_scene* scene, const float* lamp_xyz, int64_t k_total,
+                       const int64_t* cols, int64_t n_cols, const uvd_lamp* lamp, int32_t face_res,
+                       uvd_matrix_out* out, int32_t* hits, void* stream);
+
 /* ------------------------------------------------------------------ NEXT-4 */
 /* Static single-point baseline (P:7, "places the disinfection light to
  * have maximum coverage over the obstacle space, allowing it to irradiate the

@@ -764,8 +764,9 @@ static v3 px_dir(int f, int R, int a, int b) {
   }
 }
 
-/* closest-hit of the ray O + t D (t > 0) against triangle V0V1V2: t (or -1) and
- * the barycentric margin min(u, v, 1-u-v) */
+/* the ray O + t D against triangle V0V1V2: returns t of the plane crossing
+ * (or -1 when parallel or t <= 0) with the barycentric margin min(u, v, 1-u-v)
+ * (a hit iff margin >= 0) and the facing */
 static double ray_hit(v3 O, v3 D, v3 V0, v3 V1, v3 V2, double* margin, int* front) {
   v3 E1 = sub(V1, V0), E2 = sub(V2, V0);
   v3 P = cross(D, E2);
@@ -777,11 +778,9 @@ static double ray_hit(v3 O, v3 D, v3 V0, v3 V1, v3 V2, double* margin, int* fron
   double u = dot(T, P) * inv;
   v3 Q = cross(T, E1);
   double v = dot(D, Q) * inv;
-  double m = dmin(u, dmin(v, 1.0 - u - v));
-  if (m < 0.0) return -1.0;
   double t = dot(E2, Q) * inv;
   if (!(t > 0.0)) return -1.0;
-  *margin = m;
+  *margin = dmin(u, dmin(v, 1.0 - u - v));
   *front = dot(D, Nrm) < 0.0;
   return t;
 }
@@ -806,7 +805,7 @@ static void cube_task(int64_t q, void* vctx) {
   for (int b = 0; b < c->R; ++b)
     for (int a = 0; a < c->R; ++a) {
       v3 D = px_dir(f, c->R, a, b);
-      double best = INFINITY, second = INFINITY, bm = 0.0;
+      double best = INFINITY, second = INFINITY, bm = 0.0, near_t = INFINITY;
       int64_t bk = -1;
       int bfront = 0;
       for (int64_t k = 0; k < c->M; ++k) {
@@ -814,12 +813,19 @@ static void cube_task(int64_t q, void* vctx) {
         double m; int fr;
         double th = ray_hit(O, D, ld3(t), ld3(t + 3), ld3(t + 6), &m, &fr);
         if (th < 0.0) continue;
+        if (m < 0.0) {                      /* a miss; remember misses by less than 1e-6 */
+          if (m > -ORC_DEG && th < near_t) near_t = th;
+          continue;
+        }
         if (th < best) { second = best; best = th; bk = k; bm = m; bfront = fr; }
         else if (th < second) second = th;
       }
       double e = (c->P / c->L) * orc_pixel_solid_angle(c->R, a, b) / (4.0 * M_PI);
       int64_t o = (((cl * c->L + l) * 6 + f) * c->R + b) * (int64_t)c->R + a;
-      int dg = bk >= 0 && (bm < ORC_DEG || second - best <= 1e-9 * best);
+      /* degenerate: the winner within 1e-6 of an edge, a runner-up within
+       * 1e-9·t, or a near miss (within 1e-6 of an edge) at or before the winner
+       * (e.g. a ray through a shared edge that both triangles miss by rounding) */
+      int dg = (bk >= 0 && (bm < ORC_DEG || second - best <= 1e-9 * best)) || near_t <= best * (1.0 + 1e-9);
       if (c->hit) c->hit[o] = bk < 0 ? -1 : (bfront ? (int32_t)bk : -2);
       if (c->deg) c->deg[o] = (uint8_t)dg;
       if (bk >= 0 && bfront) {

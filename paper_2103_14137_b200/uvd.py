@@ -112,6 +112,9 @@ def lib():
                                   C.c_void_p, C.c_void_p]
         L.uvd_coverage.argtypes = [C.c_void_p, C.c_void_p, C.c_double, C.c_void_p,
                                    C.POINTER(C.c_double), C.c_void_p]
+        L.uvd_cubemap_matrix.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
+                                         C.POINTER(_Lamp), C.c_int32, C.POINTER(_MatrixOut), C.c_void_p,
+                                         C.c_void_p]
         L.uvd_static_columns.argtypes = [C.c_void_p, C.POINTER(_MatrixOut), C.c_int64, C.c_double, C.c_double,
                                          C.c_void_p, C.c_void_p]
         L.uvd_lp_solve.argtypes = [C.POINTER(_MatrixOut), C.c_int64, C.c_int64, C.POINTER(_LpOpts),
@@ -125,7 +128,7 @@ def lib():
 
 EXPORTS = ("uvd_scene_create", "uvd_scene_query", "uvd_scene_patches", "uvd_scene_destroy",
            "uvd_vantage_sample", "uvd_irradiance_matrix", "uvd_sync_status", "uvd_fluence",
-           "uvd_coverage", "uvd_static_columns", "uvd_lp_solve", "uvd_last_error", "uvd_version", "uvd_launch_count")
+           "uvd_coverage", "uvd_cubemap_matrix", "uvd_static_columns", "uvd_lp_solve", "uvd_last_error", "uvd_version", "uvd_launch_count")
 
 
 def _check(rc):
@@ -367,6 +370,28 @@ class Scene:
 
     def sync_status(self, stream=None):
         _check(lib().uvd_sync_status(self.handle, _stream(stream)))
+
+    def cubemap(self, lamps: torch.Tensor, face_res: int = 512, cols=None, power_w: float = 80.0,
+                hits: bool = False, out: torch.Tensor | None = None, stream=None) -> dict:
+        """NEXT-3: the paper's visibility-cube irradiance (uvd_cubemap_matrix),
+        dense (n_cols, ld) fp32; hits=True also returns the per-pixel winning
+        input triangle (n_cols, L, 6, R, R) int32 (-1 none, -2 back-facing)."""
+        assert lamps.is_cuda and lamps.dtype == torch.float32 and lamps.is_contiguous()
+        K, L = lamps.shape[0], lamps.shape[1]
+        ccols = None if cols is None else np.ascontiguousarray(cols, np.int64)
+        n_cols = K if ccols is None else len(ccols)
+        ld = self.ld()
+        A = out if out is not None else torch.empty((n_cols, ld), dtype=torch.float32, device=lamps.device)
+        m = _dense_desc(A)
+        h = torch.full((n_cols, L, 6, face_res, face_res), -3, dtype=torch.int32, device=lamps.device) if hits else None
+        lamp = _Lamp(float(power_w), int(L), 0, 0)
+        _check(lib().uvd_cubemap_matrix(self.handle, _ptr(lamps), K,
+                                        ccols.ctypes.data_as(C.c_void_p) if ccols is not None else None, n_cols,
+                                        C.byref(lamp), int(face_res), C.byref(m), _ptr(h), _stream(stream)))
+        res = {"A": A}
+        if hits:
+            res["hits"] = h
+        return res
 
     def static_baseline(self, A: torch.Tensor, t_budget: float = 1800.0, mu_min: float = 280.0,
                         stream=None) -> dict:
