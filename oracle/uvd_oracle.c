@@ -825,7 +825,7 @@ static void cube_task(int64_t q, void* vctx) {
       /* degenerate: the winner within 1e-6 of an edge, a runner-up within
        * 1e-9·t, or a near miss (within 1e-6 of an edge) at or before the winner
        * (e.g. a ray through a shared edge that both triangles miss by rounding) */
-      int dg = (bk >= 0 && (bm < ORC_DEG || second - best <= 1e-9 * best)) || near_t <= best * (1.0 + 1e-9);
+      int dg = (bk >= 0 && (bm < ORC_DEG || second - best <= 1e-9 * best)) || (near_t < INFINITY && near_t <= best * (1.0 + 1e-9));
       if (c->hit) c->hit[o] = bk < 0 ? -1 : (bfront ? (int32_t)bk : -2);
       if (c->deg) c->deg[o] = (uint8_t)dg;
       if (bk >= 0 && bfront) {

@@ -51,7 +51,7 @@ def compare(U, desc, lam, R, pat):
     ref = O.cubemap(pat, lam, R=R, hits=True)
     g = r["hits"].cpu().numpy()
     ok = ~ref["deg"]
-    assert ref["deg"].mean() < 0.10   # axis-aligned pixel rays through grid-aligned tessellations graze edges
+    assert ref["deg"].mean() < 0.02
     assert np.array_equal(g[ok], ref["hit"][ok])
     F = A * pat["area"][:, None]
     slack = ref["deg_energy"][None, :] * 2 + 2e-7 * ref["F"]   # A is stored in fp32
@@ -89,14 +89,16 @@ def test_cube_c2_worlds(uvd, seed):
     """2.5D worlds (every wall quad = 2 triangles), oracle's own lamps."""
     c = configs.c2(seed)
     v = O.vantage(c["scene"], c["vantage"])
-    lam = v["samples"][v["feasible"]][::20]
+    # feasible grid lamps nudged off the grid (< clearance) so that pixel rays
+    # do not run exactly through room corners aligned with the grid
+    lam = (v["samples"][v["feasible"]][::20] + np.float32([0.0137, 0.0291, 0.0071])).astype(np.float32)
     compare(uvd, c["scene"], lam, 16, O.extruded_patches(c["scene"]))
 
 
 def test_cube_small_ward(uvd):
     w = ward.ward(seed=4, n_bays=1, e=0.3)
     v = O.vantage(w, configs.vopts(configs.FLOAT3D, 0.5, 0.05))
-    lam = v["samples"][v["feasible"]][::25]
+    lam = (v["samples"][v["feasible"]][::25] + np.float32([0.0137, 0.0291, 0.0071])).astype(np.float32)
     compare(uvd, w, lam, 12, O.trimesh_patches(w["vertices"], w["tris"]))
 
 
