@@ -62,8 +62,11 @@ def compare(U, desc, lam, R, pat):
 def test_cube_room_and_closed_forms(uvd):
     desc = cube_room_desc(0.25)
     pat = O.trimesh_patches(desc["vertices"], desc["tris"])
+    compare(uvd, desc, np.array([[[0.31, 0.62, 0.47]]], np.float32), 24, pat)
+    # closed forms on the GPU's own output; the centred lamp's pixel rays run
+    # through the room's symmetric edges, so it is not used for pixel parity
     lam = np.array([[[0.5, 0.5, 0.5]], [[0.31, 0.62, 0.47]]], np.float32)
-    A, ref = compare(uvd, desc, lam, 24, pat)
+    sc, r, A = run(uvd, desc, lam, 24, hits=False)
     flux = (pat["area"][:, None] * A).sum(0)
     assert np.allclose(flux, 80.0, rtol=2e-7)                       # closed room receives P
     n = pat["normal"]
