@@ -36,6 +36,18 @@ UNIT = "entries/s"
 # FP32 roofline denominator for the traversal kernel (bound "alu"): guide unit
 # counts × max clock = 148 SM × 128 FP32 lanes × 2 flop × 1.965 GHz.
 FP32_PEAK_TFLOPS = 148 * 128 * 2 * 1.965e9 / 1e12
+
+
+def _hbm_peak():
+    """Measured HBM copy bandwidth (MEASURED_PEAKS.json, driver-written), else
+    the profiling guide's fallback."""
+    try:
+        return float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:  # noqa: BLE001
+        return 6537.6
+
+
+HBM_PEAK_GBS = _hbm_peak()
 # algorithmic FP32-equivalent flops (fp64 op = 2) per counted unit (DESIGN.md §Roofline)
 FLOP_PER_PAIR = 26.0      # a4: ray setup + front-face test per (patch, lamp sample)
 FLOP_PER_RAY = 10.0       # a5/a6 per front-facing ray: t-range, Eq. 7 (fp64)
@@ -359,6 +371,16 @@ def main():
                                "warp_node_fetches": cnt[3], "flops_fp32eq": flops},
                 "peak_note": "148 SM x 128 FP32 lanes x 2 x 1.965 GHz (guide); measured FFMA 70.8 TFLOP/s"}
 
+    # a7 (HBM-bound GEMVs) against the measured HBM peak: algorithmic bytes of
+    # the step's three products = A's nonzero-t columns + A twice + vectors
+    nnz_t = int((t_loc != 0).sum().item())
+    a7_bytes = 4.0 * ld * (nnz_t + 2 * n_loc) + 8.0 * (4 * N + 2 * n_loc)
+    a7_ms = phases["fluence"]
+    a7 = {"kernels": "k_gemv_n (A·t, A·1), k_gemv_t (Aᵀ·y)", "bytes": a7_bytes, "ms": a7_ms,
+          "achieved_gbs": a7_bytes / (a7_ms / 1e3) / 1e9, "peak_gbs": HBM_PEAK_GBS,
+          "frac": a7_bytes / (a7_ms / 1e3) / 1e9 / HBM_PEAK_GBS,
+          "note": "phase time includes the all_reduce for N > 1"}
+
     # end to end through the public API from pinned host buffers
     e2e = None
     if not args.no_e2e:
@@ -385,7 +407,7 @@ def main():
                                  f"{K * ld * 4 / 1e9:.1f} GB dense A",
                            "precision": "fp32 conservative box tests; fp64 triangle tests and Eq. 7; A stored fp32",
                            "step": "scene_create+vantage+irradiance+fluence(A·t, A·1, Aᵀy)+coverage"},
-                "phases_ms": phases, "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e,
+                "phases_ms": phases, "roofline": roofline, "roofline_a7": a7, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": int(n_launch), "clocks": clk}
         print(json.dumps(line), flush=True)
     if ws > 1:
