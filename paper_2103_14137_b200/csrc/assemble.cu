@@ -160,7 +160,7 @@ __device__ __forceinline__ int lane_walk32(const AsmParams& P, float ox, float o
       }
     }
     if (ref == kDone) return undecided ? kUndecided : kClear;
-    // ---- leaf: up to 4 triangles ----
+    // ---- leaf: up to kLeafMax triangles ----
     const float nD = fabsf(dx) + fabsf(dy) + fabsf(dz);
     const uint32_t st = ref_start(ref), nt = ref_count(ref);
     for (uint32_t k = 0; k < nt; ++k) {
