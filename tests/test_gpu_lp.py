@@ -217,3 +217,19 @@ def test_lp_two_column_shards(uvd):
     s = out[0]["sigma"].cpu().numpy()
     viol = np.maximum(0.0, 280.0 - A.astype(np.float64) @ t - s)
     assert viol.max() <= 1e-4 * 280.0
+
+
+def test_lp_degenerate_inputs(uvd):
+    """No light at all (an all-zero A, and an empty column shard): every patch
+    takes the full slack σ = μ_min, t = 0, objective p·N·μ_min; a bad
+    argument fails loudly."""
+    n = 40
+    r = uvd.lp_solve(dense_gpu(np.zeros((n, 5), np.float32)), n, penalty=3.0, t_max=100.0, eps=1e-9)
+    assert r["status"] == 0
+    assert np.allclose(r["sigma"].cpu().numpy(), 280.0, rtol=1e-7) and not r["t"].cpu().numpy().any()
+    assert abs(r["primal_obj"] - 3.0 * n * 280.0) <= 1e-6 * 3.0 * n * 280.0
+    empty = torch.zeros((0, 64), dtype=torch.float32, device="cuda")
+    r = uvd.lp_solve(empty, n, penalty=3.0, t_max=100.0, eps=1e-9)
+    assert np.allclose(r["sigma"].cpu().numpy(), 280.0, rtol=1e-7)
+    with pytest.raises(uvd.UvdError):
+        uvd.lp_solve(dense_gpu(np.ones((n, 5), np.float32)), n, penalty=-1.0)
