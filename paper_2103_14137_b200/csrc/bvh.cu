@@ -351,7 +351,7 @@ __global__ void k_emit_small(const float4* __restrict__ tri, int64_t n, Node* no
 // per shadow ray), in the same (left, right, range, box) arrays.
 
 #ifndef UVD_PLOC_RADIUS
-#define UVD_PLOC_RADIUS 16
+#define UVD_PLOC_RADIUS 24
 #endif
 constexpr int kPlocRadius = UVD_PLOC_RADIUS;
 
