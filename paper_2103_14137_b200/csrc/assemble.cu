@@ -30,12 +30,6 @@
 
 namespace uvd {
 
-#ifndef UVD_OCT_UNIFORM
-#define UVD_OCT_UNIFORM 0
-#endif
-#ifndef UVD_ITEM_ORDER
-#define UVD_ITEM_ORDER 0
-#endif
 #ifndef UVD_ASM_WARPS
 #define UVD_ASM_WARPS 32
 #endif
@@ -90,11 +84,7 @@ enum { kClear = 0, kBlocked = 1, kUndecided = 2 };
 // certain hit, kClear when every triangle the segment may meet was a certain
 // miss, kUndecided when no certain hit was found but the fp32 filter could not
 // decide some triangle (the caller flags the entry for exact re-tracing).
-// OCT < 0: any ray; OCT = 0..7: every ray of the warp has this direction
-// octant (bit 0/1/2 = sign bit of dx/dy/dz), so the near and far slab planes
-// of each axis are known at compile time (no min/max pairs: 4 instead of 10
-// ALU min/max per child box; identical results, FFMA is monotone)
-template <bool COUNT, int OCT = -1>
+template <bool COUNT>
 __device__ __forceinline__ int lane_walk32(const AsmParams& P, float ox, float oy, float oz,
                                            float dx, float dy, float dz, int owner,
                                            unsigned long long* cnt) {
@@ -121,31 +111,16 @@ __device__ __forceinline__ int lane_walk32(const AsmParams& P, float ox, float o
       // |o| <= 20 m), which the build-time box padding (>= 1e-5 m + 4 eps x the
       // scene's largest coordinate) absorbs; the final rounding is covered by
       // the 2e-6 relative widening
-      float an, af, bn, bf;
-      if constexpr (OCT < 0) {
-        const float ax0 = fmaf(na.x, ix, -oix), ax1 = fmaf(na.y, ix, -oix);
-        const float ay0 = fmaf(na.z, iy, -oiy), ay1 = fmaf(na.w, iy, -oiy);
-        const float az0 = fmaf(nc.x, iz, -oiz), az1 = fmaf(nc.y, iz, -oiz);
-        const float bx0 = fmaf(nb.x, ix, -oix), bx1 = fmaf(nb.y, ix, -oix);
-        const float by0 = fmaf(nb.z, iy, -oiy), by1 = fmaf(nb.w, iy, -oiy);
-        const float bz0 = fmaf(nc.z, iz, -oiz), bz1 = fmaf(nc.w, iz, -oiz);
-        an = fmaxf(fmaxf(fminf(ax0, ax1), fminf(ay0, ay1)), fmaxf(fminf(az0, az1), 0.0f));
-        af = fminf(fminf(fmaxf(ax0, ax1), fmaxf(ay0, ay1)), fminf(fmaxf(az0, az1), thi));
-        bn = fmaxf(fmaxf(fminf(bx0, bx1), fminf(by0, by1)), fmaxf(fminf(bz0, bz1), 0.0f));
-        bf = fminf(fminf(fmaxf(bx0, bx1), fmaxf(by0, by1)), fminf(fmaxf(bz0, bz1), thi));
-      } else {
-        constexpr bool sx = OCT & 1, sy = (OCT >> 1) & 1, sz = (OCT >> 2) & 1;  // negative components
-        const float axn = fmaf(sx ? na.y : na.x, ix, -oix), axf = fmaf(sx ? na.x : na.y, ix, -oix);
-        const float ayn = fmaf(sy ? na.w : na.z, iy, -oiy), ayf = fmaf(sy ? na.z : na.w, iy, -oiy);
-        const float azn = fmaf(sz ? nc.y : nc.x, iz, -oiz), azf = fmaf(sz ? nc.x : nc.y, iz, -oiz);
-        const float bxn = fmaf(sx ? nb.y : nb.x, ix, -oix), bxf = fmaf(sx ? nb.x : nb.y, ix, -oix);
-        const float byn = fmaf(sy ? nb.w : nb.z, iy, -oiy), byf = fmaf(sy ? nb.z : nb.w, iy, -oiy);
-        const float bzn = fmaf(sz ? nc.w : nc.z, iz, -oiz), bzf = fmaf(sz ? nc.z : nc.w, iz, -oiz);
-        an = fmaxf(fmaxf(axn, ayn), fmaxf(azn, 0.0f));
-        af = fminf(fminf(axf, ayf), fminf(azf, thi));
-        bn = fmaxf(fmaxf(bxn, byn), fmaxf(bzn, 0.0f));
-        bf = fminf(fminf(bxf, byf), fminf(bzf, thi));
-      }
+      const float ax0 = fmaf(na.x, ix, -oix), ax1 = fmaf(na.y, ix, -oix);
+      const float ay0 = fmaf(na.z, iy, -oiy), ay1 = fmaf(na.w, iy, -oiy);
+      const float az0 = fmaf(nc.x, iz, -oiz), az1 = fmaf(nc.y, iz, -oiz);
+      const float bx0 = fmaf(nb.x, ix, -oix), bx1 = fmaf(nb.y, ix, -oix);
+      const float by0 = fmaf(nb.z, iy, -oiy), by1 = fmaf(nb.w, iy, -oiy);
+      const float bz0 = fmaf(nc.z, iz, -oiz), bz1 = fmaf(nc.w, iz, -oiz);
+      const float an = fmaxf(fmaxf(fminf(ax0, ax1), fminf(ay0, ay1)), fmaxf(fminf(az0, az1), 0.0f));
+      const float af = fminf(fminf(fmaxf(ax0, ax1), fmaxf(ay0, ay1)), fminf(fmaxf(az0, az1), thi));
+      const float bn = fmaxf(fmaxf(fminf(bx0, bx1), fminf(by0, by1)), fmaxf(fminf(bz0, bz1), 0.0f));
+      const float bf = fminf(fminf(fmaxf(bx0, bx1), fmaxf(by0, by1)), fminf(fmaxf(bz0, bz1), thi));
       const bool h0 = an <= fmaf(af, 1.000002f, 1e-7f);
       const bool h1 = bn <= fmaf(bf, 1.000002f, 1e-7f);
       if (h0 && h1) {
@@ -185,13 +160,8 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmMinBlocks) k_assemble_lane(As
   const int64_t total = P.n_cols * P.tiles;
   for (int64_t item = (int64_t)blockIdx.x * kAsmWarps + warp; item < total;
        item += (int64_t)gridDim.x * kAsmWarps) {
-#if UVD_ITEM_ORDER
-    // column fastest: concurrent warps trace the same 32 patches from adjacent lamps
-    const int64_t tile = item / P.n_cols, c = item - tile * P.n_cols;
-#else
     // tile fastest: concurrent warps trace adjacent patches from the same lamp
     const int64_t c = item / P.tiles, tile = item - c * P.tiles;
-#endif
     const int64_t j = P.cols ? P.cols[c] : c;
     const int r = (int)(tile * 32 + lane);
     const bool valid = r < P.N;
@@ -219,37 +189,10 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmMinBlocks) k_assemble_lane(As
         w = cosd / (dd * d);  // a6: Eq. 7 in fp64, added if the ray is clear
       }
       const float dx = cx - ox, dy = cy - oy, dz = cz - oz;
-#if UVD_OCT_UNIFORM
-      // warp-uniform direction octant (the usual case: 32 adjacent patches seen
-      // from one lamp) -> the specialised slab test for the whole walk
-      const int oct = (int)signbit(dx) | ((int)signbit(dy) << 1) | ((int)signbit(dz) << 2);
-      const unsigned act = __ballot_sync(0xffffffffu, front);
-      const unsigned grp = __match_any_sync(0xffffffffu, front ? oct : 8);
-      const bool uni = __all_sync(0xffffffffu, !front || (grp & act) == act);
-      const int woct = act ? __shfl_sync(0xffffffffu, oct, __ffs(act) - 1) : 0;
-#endif
       if (front) {
         if (COUNT) cnt[0] += 1;
         // a5: occlusion of the open segment, t in (1e-4/d, 1 - 1e-4/d), fp32 decisions
-        int res;
-#if UVD_OCT_UNIFORM
-        if (uni) {
-          switch (woct) {
-            case 0: res = lane_walk32<COUNT, 0>(P, ox, oy, oz, dx, dy, dz, r, cnt); break;
-            case 1: res = lane_walk32<COUNT, 1>(P, ox, oy, oz, dx, dy, dz, r, cnt); break;
-            case 2: res = lane_walk32<COUNT, 2>(P, ox, oy, oz, dx, dy, dz, r, cnt); break;
-            case 3: res = lane_walk32<COUNT, 3>(P, ox, oy, oz, dx, dy, dz, r, cnt); break;
-            case 4: res = lane_walk32<COUNT, 4>(P, ox, oy, oz, dx, dy, dz, r, cnt); break;
-            case 5: res = lane_walk32<COUNT, 5>(P, ox, oy, oz, dx, dy, dz, r, cnt); break;
-            case 6: res = lane_walk32<COUNT, 6>(P, ox, oy, oz, dx, dy, dz, r, cnt); break;
-            default: res = lane_walk32<COUNT, 7>(P, ox, oy, oz, dx, dy, dz, r, cnt); break;
-          }
-        } else {
-          res = lane_walk32<COUNT>(P, ox, oy, oz, dx, dy, dz, r, cnt);
-        }
-#else
-        res = lane_walk32<COUNT>(P, ox, oy, oz, dx, dy, dz, r, cnt);
-#endif
+        const int res = lane_walk32<COUNT>(P, ox, oy, oz, dx, dy, dz, r, cnt);
         vis = res == kClear;
         pend |= res == kUndecided;
         if (vis) acc += w;
@@ -351,15 +294,17 @@ __global__ void __launch_bounds__(kAreaThreads, UVD_AREA_MINB) k_assemble_area(A
     for (int l = 0; l < P.L; ++l) {
       const float* pl = P.lamps + 3 * (j * P.L + l);
       const float ox = pl[0], oy = pl[1], oz = pl[2];
-      bool anyvis = false;
+      bool anyvis = false, front = false;
       if (valid) {
         const float cx = P.centroid[3 * r], cy = P.centroid[3 * r + 1], cz = P.centroid[3 * r + 2];
         const float nx = P.normal[3 * r], ny = P.normal[3 * r + 1], nz = P.normal[3 * r + 2];
         const D3 D = d3((double)cx - (double)ox, (double)cy - (double)oy, (double)cz - (double)oz);
         const double d = sqrt(ddot3(D, D));
         const double cosd = -(D.x * (double)nx + D.y * (double)ny + D.z * (double)nz);
-        bool front = cosd > 0.0;  // P:242, the patch's facing (as a4)
+        front = cosd > 0.0;  // P:242, the patch's facing (as a4)
         if (d < kMinDist) { atomicExch(P.err, 1); front = false; }
+      }
+      {  // the walks are entered from one reconvergence point (as k_assemble_lane)
         if (front) {
           for (int k = 0; k < ntri; ++k) {
             for (uint32_t s = 0; s < nsub; ++s) {
