@@ -58,7 +58,7 @@ FLOP_PER_TRI = 150.0      # fp64 division-free Möller–Trumbore (75 DP ops)
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="uvd", choices=["uvd", "reference"])
     ap.add_argument("--workload", default="C5", choices=["C5", "C4-float", "C4-tower", "C2"])
