@@ -577,3 +577,30 @@ def test_static_baseline_matches_oracle(uvd, seed):
     slack = (pat["area"][:, None] * near).sum(0)
     assert (np.abs(g["covered_at_budget"] - ref["covered_at_budget"]) <= slack + 1e-9).all()
     assert 0 < g["visible_area"].max() < pat["area"].sum()
+
+
+def test_default_allocator_and_streams(uvd):
+    """The ABI's default allocator (cudaMallocAsync, no torch callback) and a
+    non-default stream give the same matrix bit for bit; two scenes on two
+    streams concurrently agree with the sequential result (immutability,
+    concurrent const calls)."""
+    c = configs.c2(4)
+    a = uvd.Scene(c["scene"])
+    lamps, _ = a.vantage(c["vantage"])
+    ref = a.irradiance(lamps, vis_bits=True)
+    b = uvd.Scene(c["scene"], torch_allocator=False)
+    s = torch.cuda.Stream()
+    with torch.cuda.stream(s):
+        got = b.irradiance(lamps, vis_bits=True, stream=s)
+    s.synchronize()
+    assert torch.equal(got["A"], ref["A"]) and torch.equal(got["vis_bits"], ref["vis_bits"])
+    s1, s2 = torch.cuda.Stream(), torch.cuda.Stream()
+    K = lamps.shape[0]
+    h = K // 2
+    with torch.cuda.stream(s1):
+        x1 = a.irradiance(lamps, cols=list(range(h)), stream=s1)
+    with torch.cuda.stream(s2):
+        x2 = a.irradiance(lamps, cols=list(range(h, K)), stream=s2)
+    torch.cuda.synchronize()
+    assert torch.equal(torch.cat([x1["A"], x2["A"]]), ref["A"])
+    b.close()
