@@ -393,7 +393,8 @@ def main():
         v, n, el, threads = oracle_time(O, pat, olamps, args.cpu_seconds)
         cpu = {"value": v, "unit": UNIT, "cores": threads, "kind": "oracle",
                "sample": f"{n} uniformly random (patch, configuration) pairs of the same workload, "
-                         f"{len(olamps)} oracle-feasible lamp positions, {el:.1f} s on {threads} threads"}
+                         f"{len(olamps)} oracle-feasible lamp positions, {el:.1f} s on {threads} threads",
+               "extrapolated_full_matrix_s": float(N) * K / v if v > 0 else None}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
