@@ -31,6 +31,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <vector>
 
@@ -44,7 +45,8 @@ struct HpScal {   // device-resident scalars
   double kc;      // iterations since the last restart
   double first;   // 1 in the first iteration after a restart
   double lam;     // budget multiplier λ of the last projection
-  double pad[3];
+  double rho;     // Halpern reflection ρ
+  double pad[2];
 };
 
 struct HpVec {
@@ -186,7 +188,7 @@ __global__ void __launch_bounds__(1024) k_hp_primal_fin(HpVec v, int64_t k, int6
 __global__ void __launch_bounds__(kHpThreads) k_hp_dual(HpVec v, int64_t n, double mu_min, double eta) {
   __shared__ double sh[32];
   const HpScal* s = v.sc;
-  const double w = s->w, om = s->omega;
+  const double w = s->w, om = s->omega, rho = s->rho;
   const bool first = s->first != 0.0;
   double r0 = 0.0, r1 = 0.0;
   for (int64_t i = blockIdx.x * (int64_t)kHpThreads + threadIdx.x; i < n; i += (int64_t)gridDim.x * kHpThreads) {
@@ -198,9 +200,9 @@ __global__ void __launch_bounds__(kHpThreads) k_hp_dual(HpVec v, int64_t n, doub
     r1 += dy * dy / v.sig1[i];
     v.sigT[i] = sn;
     v.yT[i] = yh;
-    v.sig[i] = w * (2.0 * sn - so) + (1.0 - w) * v.sig0[i];
-    v.y[i] = w * (2.0 * yh - yo) + (1.0 - w) * v.y0[i];
-    v.mu[i] = w * (2.0 * muh - muo) + (1.0 - w) * v.mu0[i];
+    v.sig[i] = w * ((1.0 + rho) * sn - rho * so) + (1.0 - w) * v.sig0[i];
+    v.y[i] = w * ((1.0 + rho) * yh - rho * yo) + (1.0 - w) * v.y0[i];
+    v.mu[i] = w * ((1.0 + rho) * muh - rho * muo) + (1.0 - w) * v.mu0[i];
   }
   const double a = block_sum(r0, sh);
   const double b = block_sum(r1, sh);
@@ -213,10 +215,10 @@ __global__ void __launch_bounds__(kHpThreads) k_hp_dual(HpVec v, int64_t n, doub
 
 // Halpern mix of t and Aᵀy
 __global__ void k_hp_mix_cols(HpVec v, int64_t k) {
-  const double w = v.sc->w;
+  const double w = v.sc->w, rho = v.sc->rho;
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < k; j += (int64_t)gridDim.x * blockDim.x) {
-    v.t[j] = w * (2.0 * v.tT[j] - v.t[j]) + (1.0 - w) * v.t0[j];
-    v.gT[j] = w * (2.0 * v.gTT[j] - v.gT[j]) + (1.0 - w) * v.gT0[j];
+    v.t[j] = w * ((1.0 + rho) * v.tT[j] - rho * v.t[j]) + (1.0 - w) * v.t0[j];
+    v.gT[j] = w * ((1.0 + rho) * v.gTT[j] - rho * v.gT[j]) + (1.0 - w) * v.gT0[j];
   }
 }
 
@@ -303,13 +305,14 @@ __global__ void k_hp_anchor_rows(HpVec v, int64_t n, int from_T) {
   }
 }
 
-__global__ void k_hp_anchor_cols(HpVec v, int64_t k, int from_T, double omega) {
+__global__ void k_hp_anchor_cols(HpVec v, int64_t k, int from_T, double omega, double rho) {
   for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < k; j += (int64_t)gridDim.x * blockDim.x) {
     if (from_T) { v.t[j] = v.tT[j]; v.gT[j] = v.gTT[j]; }
     v.t0[j] = v.t[j]; v.gT0[j] = v.gT[j];
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     v.sc->omega = omega;
+    v.sc->rho = rho;
     v.sc->kc = 0.0;
     v.sc->w = 0.5;
     v.sc->first = 1.0;
@@ -386,6 +389,14 @@ extern "C" int uvd_lp_solve(const uvd_matrix_out* A, int64_t n, int64_t k, const
   const int M = o->check_every > 0 ? o->check_every : 64;
   const double eta = 0.999;
   const double mu_min = o->mu_min, t_max = o->t_max;
+  // method constants (Lu & Yang 2024; PDLP): reflection, restart factors,
+  // primal-weight smoothing; UVD_LP_* environment overrides are for tuning runs
+  auto knob = [](const char* name, double def) {
+    const char* e = getenv(name);
+    return e ? atof(e) : def;
+  };
+  const double rho = knob("UVD_LP_RHO", 1.0), theta = knob("UVD_LP_THETA", 0.3);
+  const double b_suff = knob("UVD_LP_SUFF", 0.2), b_nec = knob("UVD_LP_NEC", 0.8), b_art = knob("UVD_LP_ART", 0.36);
   const bool multi = o->allreduce != nullptr;
   auto allreduce = [&](double* buf, int64_t cnt, int op) -> int {
     if (!multi || cnt == 0) return UVD_OK;
@@ -498,7 +509,7 @@ extern "C" int uvd_lp_solve(const uvd_matrix_out* A, int64_t n, int64_t k, const
   note_launch();
   LP_TRY(uvd_fluence(A, n, k, 1, v.y, v.gT, stream));
   k_hp_anchor_rows<<<kHpBlocks, kHpThreads, 0, st>>>(v, n, 0);
-  k_hp_anchor_cols<<<kHpBlocks, kHpThreads, 0, st>>>(v, k, 0, omega);
+  k_hp_anchor_cols<<<kHpBlocks, kHpThreads, 0, st>>>(v, k, 0, omega, rho);
   note_launch(2);
 
   // one iteration: T(z) (projection, A t̂, σ̂, ŷ, Aᵀŷ) and the Halpern mix
@@ -605,8 +616,8 @@ extern "C" int uvd_lp_solve(const uvd_matrix_out* A, int64_t n, int64_t k, const
     it += M;
     LP_TRY(evaluate(&cur));
     if (converged(cur)) { done = true; break; }
-    const bool restart = r_last <= 0.2 * r_first || (r_last <= 0.8 * r_first && r_last > r_prev) ||
-                         (double)(it - it_restart) >= 0.36 * (double)it;
+    const bool restart = r_last <= b_suff * r_first || (r_last <= b_nec * r_first && r_last > r_prev) ||
+                         (double)(it - it_restart) >= b_art * (double)it;
     r_prev = r_last;
     if (restart) {
       // ω from the movement between restart points (before the anchors move)
@@ -619,9 +630,9 @@ extern "C" int uvd_lp_solve(const uvd_matrix_out* A, int64_t n, int64_t k, const
       LP_TRY(fetch(h + 2, v.cols_out + 6, 1));
       LP_CUDA(cudaStreamSynchronize(st));
       const double dx = std::sqrt(h[2] + h[0]), dy = std::sqrt(h[1]);
-      if (dx > 1e-10 && dy > 1e-10) omega = std::exp(0.5 * std::log(dy / dx) + 0.5 * std::log(omega));
+      if (dx > 1e-10 && dy > 1e-10) omega = std::exp(theta * std::log(dy / dx) + (1.0 - theta) * std::log(omega));
       k_hp_anchor_rows<<<kHpBlocks, kHpThreads, 0, st>>>(v, n, 1);
-      k_hp_anchor_cols<<<kHpBlocks, kHpThreads, 0, st>>>(v, k, 1, omega);
+      k_hp_anchor_cols<<<kHpBlocks, kHpThreads, 0, st>>>(v, k, 1, omega, rho);
       note_launch(2);
       it_restart = it;
       r_prev = INFINITY;
