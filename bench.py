@@ -52,7 +52,7 @@ HBM_PEAK_GBS = _hbm_peak()
 FLOP_PER_PAIR = 26.0      # a4: ray setup + front-face test per (patch, lamp sample)
 FLOP_PER_RAY = 10.0       # a5/a6 per front-facing ray: t-range, Eq. 7 (fp64)
 FLOP_PER_BOX = 12.0       # fp32 slab test of one child box
-FLOP_PER_TRI = 150.0      # fp64 division-free Möller–Trumbore (75 DP ops)
+FLOP_PER_TRI = 80.0       # fp32 filtered division-free Möller–Trumbore with its error bounds (~80 ops)
 
 
 def parse():
