@@ -147,7 +147,10 @@ __device__ __forceinline__ int64_t cube_closest(const CubeParams& P, float ox, f
   return bk;
 }
 
-__global__ void __launch_bounds__(kCubeThreads) k_cube_trace(CubeParams P) {
+#ifndef UVD_CUBE_MINB
+#define UVD_CUBE_MINB 4
+#endif
+__global__ void __launch_bounds__(kCubeThreads, UVD_CUBE_MINB) k_cube_trace(CubeParams P) {
   const int lane = threadIdx.x & 31;
   const int64_t per_col = (int64_t)P.L * 6 * P.R * P.R;
   const int64_t total = P.nc * per_col;
