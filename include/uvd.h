@@ -127,6 +127,19 @@ UVD_API int uvd_scene_patches(const uvd_scene* scene, float* centroid, float* no
 
 UVD_API void uvd_scene_destroy(uvd_scene* scene);
 
+/* Introspection of the scene's BVH (a2), for structural tests and tree-quality
+ * tools.  *n_nodes = max(M-1, 1), *root = the root reference (HOST).  nodes
+ * (DEVICE, optional): n_nodes records of 64 B in depth-first preorder —
+ * float4 a = child0 (lo.x, hi.x, lo.y, hi.y), float4 b = child1 (same),
+ * float4 c = (child0 lo.z, hi.z, child1 lo.z, hi.z), uint32 refs[4] = (child0,
+ * child1, 0, 0); a reference with bit 31 set is a leaf: triangles
+ * [(ref & 0x7fffffff) >> 3, + (ref & 7) + 1) of `tri`; else a node index.
+ * Boxes are padded outward (1e-5 m + 1e-6·|x| + 4·eps32·max|coord|).
+ * tri (DEVICE, optional): M × 12 floats in leaf order, (v0, owner patch as
+ * int bits), (v1, input triangle index as int bits), (v2, 0).  Asynchronous. */
+UVD_API int uvd_scene_bvh(const uvd_scene* scene, void* nodes, float* tri, int64_t* n_nodes, uint32_t* root,
+                  void* stream);
+
 /* ---------------------------------------------------------------------- a3 */
 enum { UVD_ROBOT_DISC2D = 0, UVD_ROBOT_TOWER = 1, UVD_ROBOT_FLOAT3D = 2, UVD_ROBOT_ARM = 3 };
 

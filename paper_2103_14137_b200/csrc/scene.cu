@@ -519,3 +519,16 @@ extern "C" int uvd_sync_status(const uvd_scene* s, void* stream) {
 extern "C" const char* uvd_last_error(void) { return uvd::g_err; }
 extern "C" int uvd_version(void) { return 100; }
 extern "C" unsigned long long uvd_launch_count(void) { return g_launches.load(); }
+
+extern "C" int uvd_scene_bvh(const uvd_scene* s, void* nodes, float* tri, int64_t* n_nodes, uint32_t* root,
+                             void* stream) {
+  clear_error();
+  if (!s) { set_error("uvd_scene_bvh: null scene"); return UVD_ERR_INVALID; }
+  const int64_t nn = std::max<int64_t>(s->M - 1, 1);
+  if (n_nodes) *n_nodes = nn;
+  if (root) *root = s->root;
+  cudaStream_t st = (cudaStream_t)stream;
+  if (nodes) UVD_CUDA_TRY(cudaMemcpyAsync(nodes, s->nodes, nn * sizeof(Node), cudaMemcpyDeviceToDevice, st));
+  if (tri) UVD_CUDA_TRY(cudaMemcpyAsync(tri, s->tri, s->M * 3 * sizeof(float4), cudaMemcpyDeviceToDevice, st));
+  return UVD_OK;
+}

@@ -101,6 +101,8 @@ def lib():
                                       C.POINTER(C.c_float), C.POINTER(C.c_double)]
         L.uvd_scene_patches.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p,
                                         C.c_void_p]
+        L.uvd_scene_bvh.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64),
+                                    C.POINTER(C.c_uint32), C.c_void_p]
         L.uvd_scene_destroy.argtypes = [C.c_void_p]
         L.uvd_scene_destroy.restype = None
         L.uvd_vantage_sample.argtypes = [C.c_void_p, C.POINTER(_VantageOpts), C.c_void_p, C.c_void_p,
@@ -126,7 +128,7 @@ def lib():
     return _lib
 
 
-EXPORTS = ("uvd_scene_create", "uvd_scene_query", "uvd_scene_patches", "uvd_scene_destroy",
+EXPORTS = ("uvd_scene_create", "uvd_scene_query", "uvd_scene_patches", "uvd_scene_bvh", "uvd_scene_destroy",
            "uvd_vantage_sample", "uvd_irradiance_matrix", "uvd_sync_status", "uvd_fluence",
            "uvd_coverage", "uvd_cubemap_matrix", "uvd_static_columns", "uvd_lp_solve", "uvd_last_error", "uvd_version", "uvd_launch_count")
 
@@ -256,6 +258,18 @@ class Scene:
         _check(lib().uvd_scene_patches(self.handle, _ptr(cen), _ptr(nrm), _ptr(area), _ptr(orig),
                                        _stream(stream)))
         return dict(centroid=cen, normal=nrm, area=area, orig_id=orig)
+
+    def bvh(self, stream=None) -> dict:
+        """uvd_scene_bvh: the BVH nodes (n_nodes, 16) as raw 32-bit words (float
+        boxes viewed as int32; refs in columns 12–13) and the leaf-ordered
+        triangles (M, 12) float32, plus the root reference."""
+        n = C.c_int64()
+        root = C.c_uint32()
+        _check(lib().uvd_scene_bvh(self.handle, None, None, C.byref(n), C.byref(root), _stream(stream)))
+        nodes = torch.empty((n.value, 16), dtype=torch.int32, device=f"cuda:{self.device}")
+        tri = torch.empty((self.M, 12), dtype=torch.float32, device=f"cuda:{self.device}")
+        _check(lib().uvd_scene_bvh(self.handle, _ptr(nodes), _ptr(tri), C.byref(n), C.byref(root), _stream(stream)))
+        return {"nodes": nodes, "tri": tri, "root": int(root.value)}
 
     def vantage(self, opts: dict, stream=None):
         """uvd_vantage_sample: returns (lamps (K, L, 3) fp32, raw_index (K,) int64)."""

@@ -1,0 +1,118 @@
+"""Structural pins of row a2 (the BVH) through uvd_scene_bvh: whatever tree the
+builder makes, occlusion is exact only if (i) every triangle sits in exactly
+one leaf, (ii) no node is reached twice from the root (a tree), (iii) every
+child box contains all vertices of its subtree, (iv) the leaf-ordered
+triangles are the input triangles, unchanged, and (v) the depth fits the
+traversal stack (64).  Checked here on a 2.5D room, a small ward and C4."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+torch = pytest.importorskip("torch")
+
+from synth import configs, rooms, ward  # noqa: E402
+
+LEAF = np.int64(0x80000000)
+
+
+@pytest.fixture(scope="module")
+def uvd():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import __graft_entry__
+    __graft_entry__.build()
+    from paper_2103_14137_b200 import uvd as U
+    return U
+
+
+def check_tree(sc, input_tris=None):
+    b = sc.bvh()
+    words = b["nodes"].cpu().numpy()
+    boxes = words.view(np.float32)
+    refs = words[:, 12:14].astype(np.int64) & 0xFFFFFFFF
+    tri = b["tri"].cpu().numpy()
+    M = tri.shape[0]
+    verts = tri.reshape(M, 3, 4)[:, :, :3]
+    seen_tri = np.zeros(M, np.int32)
+    seen_node = np.zeros(len(words), np.int32)
+    # iterative DFS from the root with subtree vertex bounds checked bottom-up
+    root = b["root"]
+    assert root == 0
+    stack = [(0, 1)]
+    max_depth = 0
+    lo_of = {}
+    order = []
+    while stack:
+        n, dep = stack.pop()
+        seen_node[n] += 1
+        max_depth = max(max_depth, dep)
+        order.append(n)
+        for side in (0, 1):
+            r = refs[n, side]
+            if r & LEAF:
+                start, cnt = (r & 0x7FFFFFFF) >> 3, (r & 7) + 1
+                seen_tri[start:start + cnt] += 1
+            else:
+                assert r > n  # depth-first preorder: children after their parent
+                stack.append((int(r), dep + 1))
+    # collapsed subtrees (leaves of up to 2 triangles) leave some node records
+    # unreferenced; a reached node is reached once, and reached nodes = leaves - 1
+    n_leaves = int(((refs[seen_node == 1] & LEAF) != 0).sum())
+    assert seen_node.max() == 1, "no node reached twice"
+    assert int((seen_node == 1).sum()) == n_leaves - 1 or len(words) == 1
+    assert (seen_tri == 1).all(), "every triangle in exactly one leaf"
+    assert max_depth < 64
+    # boxes contain their subtrees: compute subtree bounds in reverse preorder
+    lo = np.full((len(words), 3), np.inf, np.float32)
+    hi = np.full((len(words), 3), -np.inf, np.float32)
+    for n in reversed(order):
+        for side in (0, 1):
+            r = refs[n, side]
+            if r & LEAF:
+                start, cnt = (r & 0x7FFFFFFF) >> 3, (r & 7) + 1
+                v = verts[start:start + cnt].reshape(-1, 3)
+                clo, chi = v.min(0), v.max(0)
+            else:
+                clo, chi = lo[int(r)], hi[int(r)]
+            bx = boxes[n]
+            if side == 0:
+                blo = np.array([bx[0], bx[2], bx[8]]); bhi = np.array([bx[1], bx[3], bx[9]])
+            else:
+                blo = np.array([bx[4], bx[6], bx[10]]); bhi = np.array([bx[5], bx[7], bx[11]])
+            if r & LEAF and cnt == 1 and len(words) == 1 and side == 1:
+                continue  # the empty second child of a single-leaf tree
+            assert (blo <= clo).all() and (bhi >= chi).all(), (n, side)
+            lo[n] = np.minimum(lo[n], clo)
+            hi[n] = np.maximum(hi[n], chi)
+    if input_tris is not None:
+        orig = tri[:, 7].view(np.int32)
+        assert np.array_equal(np.sort(orig), np.arange(M))
+        assert np.array_equal(verts[np.argsort(orig)], input_tris)
+    return b
+
+
+def test_bvh_room_2p5d(uvd):
+    sc = uvd.Scene(rooms.random_room(3))
+    check_tree(sc)
+
+
+def test_bvh_small_ward(uvd):
+    w = ward.ward(seed=4, n_bays=1, e=0.3)
+    sc = uvd.Scene(w)
+    check_tree(sc, w["vertices"][w["tris"]])
+
+
+@pytest.mark.slow
+def test_bvh_c4(uvd):
+    w = configs.c4_scene()
+    sc = uvd.Scene(w)
+    check_tree(sc, w["vertices"][w["tris"]])
+
+
+def test_bvh_tiny(uvd):
+    s = 1.0 / 64
+    V = np.array([[-s, -s, 0], [2 * s, -s, 0], [-s, 2 * s, 0]], np.float32)
+    sc = uvd.Scene(dict(vertices=V, tris=np.array([[0, 1, 2]], np.int32)))
+    b = sc.bvh()
+    assert b["nodes"].shape[0] == 1
