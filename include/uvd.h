@@ -99,9 +99,9 @@ typedef struct {
 
 /* Build a scene on `device`: copy the input, compute the canonical patch
  * attributes (a1), build the BVH over all triangles (a2: Morton codes, radix
- * sort, PLOC agglomerative clustering — Karras LBVH + bottom-up refit when the
- * environment sets UVD_BVH=karras — then nodes in depth-first preorder, leaves
- * of <= 2 triangles).  Synchronises `stream`.
+ * sort, top-down binned-SAH splits, bottom-up refit — PLOC clustering or the
+ * Karras LBVH when the environment sets UVD_BVH=ploc / karras — then nodes in
+ * depth-first preorder, leaves of <= 2 triangles).  Synchronises `stream`.
  * Canonical patch attributes (fp64 arithmetic, rounded once to fp32):
  *   3D : c = fl32((a+b+c)/3), n = fl32(cross(b-a,c-a)/|.|), area = |cross|/2;
  *   2.5D: q_s = fl32(e0 + ((e1-e0)*s)/n_seg) (q_nseg = e1), c = fl32((q_s+q_{s+1})/2, h/2),

@@ -638,6 +638,276 @@ static int build_ploc(uvd_scene* s, int64_t M, int32_t* left, int32_t* right, in
   return UVD_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Top-down binned-SAH builder (UVD_BVH=sah): level-synchronous, one CTA per
+// node of the level; the CTA bins its triangles' box centres (16 bins per
+// axis; bin boxes kept exact with ordered-int shared-memory atomics), sweeps
+// the bins for the split of least SAH cost, partitions its range stably (left
+// first, so every subtree is a contiguous DFS range), and creates its children
+// (a single triangle is a leaf reference).  Node boxes come from k_refit.
+constexpr int kSahBins = 16;
+constexpr int kSahBig = 8192;  // nodes above this many triangles get 1024-thread CTAs
+
+__device__ __forceinline__ int f2o(float f) {  // order-preserving float -> int
+  const int i = __float_as_int(f);
+  return i >= 0 ? i : i ^ 0x7fffffff;
+}
+__device__ __forceinline__ float o2f(int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7fffffff); }
+
+__device__ __forceinline__ float sah_area(float lx, float ly, float lz, float hx, float hy, float hz) {
+  const float dx = hx - lx, dy = hy - ly, dz = hz - lz;
+  return dx * dy + dy * dz + dz * dx;
+}
+
+template <int kSahThreads>
+__global__ void __launch_bounds__(kSahThreads) k_sah_split(const float4* __restrict__ tri, int32_t* __restrict__ perm,
+                                                           int32_t* __restrict__ tmp, const int32_t* __restrict__ list,
+                                                           int32_t* __restrict__ rf, int32_t* __restrict__ rl,
+                                                           int32_t* __restrict__ left, int32_t* __restrict__ right,
+                                                           int32_t* __restrict__ pint, int32_t* __restrict__ pleaf,
+                                                           int* __restrict__ ctr, int32_t* __restrict__ next,
+                                                           int32_t* __restrict__ next_big) {
+  __shared__ int s_cnt[3][kSahBins];
+  __shared__ int s_lo[3][kSahBins][3], s_hi[3][kSahBins][3];
+  __shared__ int s_cb[6];      // centre bounds (ordered ints)
+  __shared__ int s_split[3];  // axis, bin, n_left
+  __shared__ int s_scan[kSahThreads / 32];
+  const int node = list[blockIdx.x];
+  const int first = rf[node], last = rl[node], n = last - first + 1;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  // 1. bounds of the box centres
+  float cl[3] = {INFINITY, INFINITY, INFINITY}, ch[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int p = first + tid; p <= last; p += kSahThreads) {
+    const Box b = tri_box(tri, perm[p]);
+    const float c[3] = {0.5f * (b.lx + b.hx), 0.5f * (b.ly + b.hy), 0.5f * (b.lz + b.hz)};
+    for (int a = 0; a < 3; ++a) { cl[a] = fminf(cl[a], c[a]); ch[a] = fmaxf(ch[a], c[a]); }
+  }
+  for (int a = 0; a < 3; ++a)
+    for (int o = 16; o > 0; o >>= 1) {
+      cl[a] = fminf(cl[a], __shfl_xor_sync(0xffffffffu, cl[a], o));
+      ch[a] = fmaxf(ch[a], __shfl_xor_sync(0xffffffffu, ch[a], o));
+    }
+  // bins cleared; centre bounds reduced across warps as ordered ints
+  if (tid < 3 * kSahBins) {
+    const int a = tid / kSahBins, b = tid % kSahBins;
+    s_cnt[a][b] = 0;
+    for (int k = 0; k < 3; ++k) { s_lo[a][b][k] = 0x7fffffff; s_hi[a][b][k] = (int)0x80000000; }
+  }
+  if (tid < 6) s_cb[tid] = tid < 3 ? 0x7fffffff : (int)0x80000000;
+  __syncthreads();
+  if (lane == 0)
+    for (int a = 0; a < 3; ++a) {
+      atomicMin(&s_cb[a], f2o(cl[a]));
+      atomicMax(&s_cb[3 + a], f2o(ch[a]));
+    }
+  __syncthreads();
+  float cmin[3], cscale[3];
+  for (int a = 0; a < 3; ++a) {
+    const float lo = o2f(s_cb[a]), hi = o2f(s_cb[3 + a]);
+    cmin[a] = lo;
+    cscale[a] = hi > lo ? (float)kSahBins / (hi - lo) : 0.f;
+  }
+  // 2. bins (skipped for n == 2: split at the middle)
+  if (n > 2) {
+    for (int p = first + tid; p <= last; p += kSahThreads) {
+      const Box b = tri_box(tri, perm[p]);
+      const float c[3] = {0.5f * (b.lx + b.hx), 0.5f * (b.ly + b.hy), 0.5f * (b.lz + b.hz)};
+      const int lo[3] = {f2o(b.lx), f2o(b.ly), f2o(b.lz)}, hi[3] = {f2o(b.hx), f2o(b.hy), f2o(b.hz)};
+      for (int a = 0; a < 3; ++a) {
+        if (cscale[a] == 0.f) continue;
+        const int bin = min(kSahBins - 1, max(0, (int)((c[a] - cmin[a]) * cscale[a])));
+        atomicAdd(&s_cnt[a][bin], 1);
+        for (int k = 0; k < 3; ++k) { atomicMin(&s_lo[a][bin][k], lo[k]); atomicMax(&s_hi[a][bin][k], hi[k]); }
+      }
+    }
+  }
+  __syncthreads();
+  // 3. sweep (thread 0): least SAH cost split among the 3 x (B-1) bin planes
+  if (tid == 0) {
+    float best = INFINITY;
+    int ba = -1, bb = -1, bnl = 0;
+    if (n > 2) {
+      for (int a = 0; a < 3; ++a) {
+        if (cscale[a] == 0.f) continue;
+        float rarea[kSahBins];
+        int rcnt[kSahBins];
+        float lx = INFINITY, ly = INFINITY, lz = INFINITY, hx = -INFINITY, hy = -INFINITY, hz = -INFINITY;
+        int c = 0;
+        for (int b = kSahBins - 1; b >= 0; --b) {
+          if (s_cnt[a][b]) {
+            lx = fminf(lx, o2f(s_lo[a][b][0])); ly = fminf(ly, o2f(s_lo[a][b][1])); lz = fminf(lz, o2f(s_lo[a][b][2]));
+            hx = fmaxf(hx, o2f(s_hi[a][b][0])); hy = fmaxf(hy, o2f(s_hi[a][b][1])); hz = fmaxf(hz, o2f(s_hi[a][b][2]));
+            c += s_cnt[a][b];
+          }
+          rarea[b] = c ? sah_area(lx, ly, lz, hx, hy, hz) : 0.f;
+          rcnt[b] = c;
+        }
+        lx = ly = lz = INFINITY; hx = hy = hz = -INFINITY;
+        c = 0;
+        for (int b = 0; b < kSahBins - 1; ++b) {
+          if (s_cnt[a][b]) {
+            lx = fminf(lx, o2f(s_lo[a][b][0])); ly = fminf(ly, o2f(s_lo[a][b][1])); lz = fminf(lz, o2f(s_lo[a][b][2]));
+            hx = fmaxf(hx, o2f(s_hi[a][b][0])); hy = fmaxf(hy, o2f(s_hi[a][b][1])); hz = fmaxf(hz, o2f(s_hi[a][b][2]));
+            c += s_cnt[a][b];
+          }
+          if (c == 0 || rcnt[b + 1] == 0) continue;
+          const float cost = sah_area(lx, ly, lz, hx, hy, hz) * c + rarea[b + 1] * rcnt[b + 1];
+          if (cost < best) { best = cost; ba = a; bb = b; bnl = c; }
+        }
+      }
+    }
+    s_split[0] = ba;  // -1: median split by position
+    s_split[1] = bb;
+    s_split[2] = ba < 0 ? n / 2 : bnl;
+  }
+  __syncthreads();
+  const int sa = s_split[0], sb = s_split[1], nl = s_split[2];
+  // 4. stable partition of the range (left first) through tmp
+  if (sa >= 0) {
+    int base_l = 0, base_r = 0;
+    for (int p0 = first; p0 <= last; p0 += kSahThreads) {
+      const int p = p0 + tid;
+      int flag = 0, t = 0;
+      if (p <= last) {
+        t = perm[p];
+        const Box b = tri_box(tri, t);
+        const float c = sa == 0 ? 0.5f * (b.lx + b.hx) : sa == 1 ? 0.5f * (b.ly + b.hy) : 0.5f * (b.lz + b.hz);
+        const int bin = min(kSahBins - 1, max(0, (int)((c - cmin[sa]) * cscale[sa])));
+        flag = bin <= sb;
+      }
+      // block exclusive scan of flag
+      const unsigned bal = __ballot_sync(0xffffffffu, flag);
+      const int in_warp = __popc(bal & ((1u << lane) - 1u));
+      if (lane == 0) s_scan[wid] = __popc(bal);
+      __syncthreads();
+      int before = 0, total = 0;
+      for (int w = 0; w < kSahThreads / 32; ++w) {
+        const int v = s_scan[w];
+        if (w < wid) before += v;
+        total += v;
+      }
+      if (p <= last) {
+        const int rank_l = base_l + before + in_warp;
+        const int idx = p - p0;
+        const int rank_r = base_r + (idx - (before + in_warp));
+        tmp[flag ? first + rank_l : first + nl + rank_r] = t;
+      }
+      const int chunk = min(kSahThreads, last - p0 + 1);
+      base_l += total;
+      base_r += chunk - total;
+      __syncthreads();
+    }
+    __syncthreads();
+    for (int p = first + tid; p <= last; p += kSahThreads) perm[p] = tmp[p];
+  }
+  // 5. children
+  if (tid == 0) {
+    const int l0 = first, l1 = first + nl - 1, r0 = first + nl, r1 = last;
+    int32_t refl, refr;
+    if (l1 == l0) { refl = (int32_t)(0x80000000u | (uint32_t)l0); pleaf[l0] = node; }
+    else {
+      refl = atomicAdd(&ctr[0], 1);
+      rf[refl] = l0; rl[refl] = l1; pint[refl] = node;
+      if (l1 - l0 + 1 > kSahBig) next_big[atomicAdd(&ctr[2], 1)] = refl;
+      else next[atomicAdd(&ctr[1], 1)] = refl;
+    }
+    if (r1 == r0) { refr = (int32_t)(0x80000000u | (uint32_t)r0); pleaf[r0] = node; }
+    else {
+      refr = atomicAdd(&ctr[0], 1);
+      rf[refr] = r0; rl[refr] = r1; pint[refr] = node;
+      if (r1 - r0 + 1 > kSahBig) next_big[atomicAdd(&ctr[2], 1)] = refr;
+      else next[atomicAdd(&ctr[1], 1)] = refr;
+    }
+    left[node] = refl;
+    right[node] = refr;
+  }
+}
+
+__global__ void k_iota32(int32_t* __restrict__ x, int64_t n) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) x[i] = (int32_t)i;
+}
+
+__global__ void k_gather_tri_i32(const float4* __restrict__ in, const int32_t* __restrict__ perm, int64_t n,
+                                 float4* __restrict__ out) {
+  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  const int64_t t = perm[r];
+  out[3 * r] = in[3 * t]; out[3 * r + 1] = in[3 * t + 1]; out[3 * r + 2] = in[3 * t + 2];
+}
+
+__global__ void k_gather_u32(const uint32_t* __restrict__ in, const int32_t* __restrict__ perm, int64_t n,
+                             uint32_t* __restrict__ out) {
+  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r < n) out[r] = in[perm[r]];
+}
+
+static int build_sah(uvd_scene* s, int64_t M, int32_t* left, int32_t* right, int32_t* rf, int32_t* rl,
+                     int32_t* pint, int32_t* pleaf, float* ibox, int* arrive, uint32_t* order, cudaStream_t st) {
+  Alloc& al = s->alloc;
+  int32_t* perm = (int32_t*)al.get(M * 4);
+  int32_t* tmp = (int32_t*)al.get(M * 4);
+  int32_t* la = (int32_t*)al.get(M * 4);   // small-node lists (this level, next level)
+  int32_t* lb = (int32_t*)al.get(M * 4);
+  int32_t* ba = (int32_t*)al.get(M * 4);   // big-node lists
+  int32_t* bb = (int32_t*)al.get(M * 4);
+  int* ctr = (int*)al.get(4 * sizeof(int));
+  float4* tri2 = (float4*)al.get(3 * M * sizeof(float4));
+  if (!perm || !tmp || !la || !lb || !ba || !bb || !ctr || !tri2) {
+    set_error("scene: out of device memory (SAH scratch)");
+    return UVD_ERR_NOMEM;
+  }
+  k_iota32<<<grid_for(M, 256), 256, 0, st>>>(perm, M);
+  note_launch();
+  int h[4] = {1, 0, 0, 0};  // next internal node id, next-level small / big list lengths
+  int32_t zero = 0, last = (int32_t)(M - 1);
+  UVD_CUDA_TRY(cudaMemcpyAsync(rf, &zero, 4, cudaMemcpyHostToDevice, st));
+  UVD_CUDA_TRY(cudaMemcpyAsync(rl, &last, 4, cudaMemcpyHostToDevice, st));
+  UVD_CUDA_TRY(cudaMemcpyAsync(M > kSahBig ? ba : la, &zero, 4, cudaMemcpyHostToDevice, st));
+  UVD_CUDA_TRY(cudaMemcpyAsync(pint, &zero, 4, cudaMemcpyHostToDevice, st));
+  UVD_CUDA_TRY(cudaMemcpyAsync(ctr, h, sizeof(int), cudaMemcpyHostToDevice, st));  // node id 1 next
+  int n_small = M > kSahBig ? 0 : 1, n_big = M > kSahBig ? 1 : 0, levels = 0;
+  while (n_small + n_big > 0) {
+    UVD_CUDA_TRY(cudaMemsetAsync(ctr + 1, 0, 2 * sizeof(int), st));  // next level's list lengths
+    if (n_big)
+      k_sah_split<1024><<<n_big, 1024, 0, st>>>(s->tri, perm, tmp, ba, rf, rl, left, right, pint, pleaf, ctr, lb, bb);
+    if (n_small)
+      k_sah_split<128><<<n_small, 128, 0, st>>>(s->tri, perm, tmp, la, rf, rl, left, right, pint, pleaf, ctr, lb, bb);
+    note_launch((n_big > 0) + (n_small > 0));
+    UVD_CUDA_TRY(cudaMemcpyAsync(h, ctr, 3 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    UVD_CUDA_TRY(cudaStreamSynchronize(st));
+    n_small = h[1];
+    n_big = h[2];
+    std::swap(la, lb);
+    std::swap(ba, bb);
+    if (++levels > 4096) { set_error("scene: SAH build did not terminate"); return UVD_ERR_CUDA; }
+  }
+  if (h[0] != M - 1) { set_error("scene: SAH build made %d internal nodes, expected %lld", h[0], (long long)(M - 1)); return UVD_ERR_CUDA; }
+  // triangles (and the sorted -> input map) into the DFS leaf order of the tree
+  k_gather_tri_i32<<<grid_for(M, 256), 256, 0, st>>>(s->tri, perm, M, tri2);
+  note_launch();
+  UVD_CUDA_TRY(cudaMemcpyAsync(s->tri, tri2, 3 * M * sizeof(float4), cudaMemcpyDeviceToDevice, st));
+  if (order) {
+    uint32_t* o2 = (uint32_t*)tri2;
+    k_gather_u32<<<grid_for(M, 256), 256, 0, st>>>(order, perm, M, o2);
+    note_launch();
+    UVD_CUDA_TRY(cudaMemcpyAsync(order, o2, M * sizeof(uint32_t), cudaMemcpyDeviceToDevice, st));
+  }
+  if (s->kind == UVD_SCENE_TRIMESH) {  // rows follow the leaf order
+    k_set_owner<<<grid_for(M, 256), 256, 0, st>>>(s->tri, M);
+    note_launch();
+  }
+  k_refit<<<grid_for(M, 256), 256, 0, st>>>(s->tri, M, left, right, pint, pleaf, ibox, arrive);
+  note_launch();
+  UVD_CUDA_TRY(cudaGetLastError());
+  for (void* p : {(void*)perm, (void*)tmp, (void*)la, (void*)lb, (void*)ba, (void*)bb, (void*)ctr, (void*)tri2})
+    al.put(p);
+  return UVD_OK;
+}
+
+#ifndef UVD_BVH_DEFAULT
+#define UVD_BVH_DEFAULT 2  // binned SAH; UVD_BVH=ploc / karras select the others
+#endif
 // Morton-sort the triangles (tri_in, input order) and build the BVH over them.
 // On return s->tri is leaf-ordered and `order` (if non-null) receives the
 // sorted -> input permutation (caller frees).
@@ -686,12 +956,16 @@ int build_bvh(uvd_scene* s, float4* tri_in, uint32_t** order_out, cudaStream_t s
       return UVD_ERR_NOMEM;
     }
     UVD_CUDA_TRY(cudaMemsetAsync(arrive, 0, ni * sizeof(int), st));
-    static int use_karras = -1;
-    if (use_karras < 0) {
+    static int builder = -1;  // 0 PLOC, 1 Karras LBVH, 2 binned SAH (default)
+    if (builder < 0) {
       const char* e = getenv("UVD_BVH");
-      use_karras = e && std::string(e) == "karras";
+      const std::string v = e ? e : "";
+      builder = v == "ploc" ? 0 : v == "karras" ? 1 : v == "sah" ? 2 : UVD_BVH_DEFAULT;
     }
-    if (use_karras) {  // Karras 2012 LBVH + bottom-up refit
+    if (builder == 2) {  // top-down binned SAH (level-synchronous, one CTA per node)
+      UVD_TRY(build_sah(s, M, left, right, rf, rl, pint, pleaf, ibox, arrive,
+                        s->kind == UVD_SCENE_TRIMESH ? vals : nullptr, st));
+    } else if (builder == 1) {  // Karras 2012 LBVH + bottom-up refit
       k_karras<<<grid_for(ni, 256), 256, 0, st>>>(keys, M, left, right, rf, rl, pint, pleaf);
       note_launch();
       k_refit<<<grid_for(M, 256), 256, 0, st>>>(s->tri, M, left, right, pint, pleaf, ibox, arrive);
