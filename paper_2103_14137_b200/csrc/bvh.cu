@@ -645,7 +645,10 @@ static int build_ploc(uvd_scene* s, int64_t M, int32_t* left, int32_t* right, in
 // the bins for the split of least SAH cost, partitions its range stably (left
 // first, so every subtree is a contiguous DFS range), and creates its children
 // (a single triangle is a leaf reference).  Node boxes come from k_refit.
-constexpr int kSahBins = 16;
+#ifndef UVD_SAH_BINS
+#define UVD_SAH_BINS 32
+#endif
+constexpr int kSahBins = UVD_SAH_BINS;
 constexpr int kSahBig = 8192;  // nodes above this many triangles get 1024-thread CTAs
 
 __device__ __forceinline__ int f2o(float f) {  // order-preserving float -> int
