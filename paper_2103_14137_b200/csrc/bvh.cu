@@ -959,12 +959,10 @@ int build_bvh(uvd_scene* s, float4* tri_in, uint32_t** order_out, cudaStream_t s
       return UVD_ERR_NOMEM;
     }
     UVD_CUDA_TRY(cudaMemsetAsync(arrive, 0, ni * sizeof(int), st));
-    static int builder = -1;  // 0 PLOC, 1 Karras LBVH, 2 binned SAH (default)
-    if (builder < 0) {
-      const char* e = getenv("UVD_BVH");
-      const std::string v = e ? e : "";
-      builder = v == "ploc" ? 0 : v == "karras" ? 1 : v == "sah" ? 2 : UVD_BVH_DEFAULT;
-    }
+    // 0 PLOC, 1 Karras LBVH, 2 binned SAH (default); read per build
+    const char* e = getenv("UVD_BVH");
+    const std::string v = e ? e : "";
+    const int builder = v == "ploc" ? 0 : v == "karras" ? 1 : v == "sah" ? 2 : UVD_BVH_DEFAULT;
     if (builder == 2) {  // top-down binned SAH (level-synchronous, one CTA per node)
       UVD_TRY(build_sah(s, M, left, right, rf, rl, pint, pleaf, ibox, arrive,
                         s->kind == UVD_SCENE_TRIMESH ? vals : nullptr, st));

@@ -116,3 +116,26 @@ def test_bvh_tiny(uvd):
     sc = uvd.Scene(dict(vertices=V, tris=np.array([[0, 1, 2]], np.int32)))
     b = sc.bvh()
     assert b["nodes"].shape[0] == 1
+
+
+@pytest.mark.parametrize("builder", ["sah", "ploc", "karras"])
+def test_builders_give_identical_matrices(uvd, builder, monkeypatch):
+    """The three builders (binned SAH default, PLOC, Karras LBVH) make
+    different trees; the occlusion decisions — hence A and the visibility bits
+    in input row order — are identical (exact tests, tree-independent)."""
+    w = ward.ward(seed=5, n_bays=1, e=0.25)
+    monkeypatch.setenv("UVD_BVH", builder)
+    sc = uvd.Scene(w)
+    check_tree(sc, w["vertices"][w["tris"]])
+    lam, _ = sc.vantage(configs.vopts(configs.FLOAT3D, 0.6, 0.05))
+    r = sc.irradiance(lam)
+    orig = sc.patches()["orig_id"].cpu().numpy()
+    A = np.zeros((sc.N, lam.shape[0]), np.float32)
+    A[orig] = r["A"][:, :sc.N].T.cpu().numpy()
+    monkeypatch.setenv("UVD_BVH", "sah")
+    ref_sc = uvd.Scene(w)
+    rr = ref_sc.irradiance(lam)
+    ro = ref_sc.patches()["orig_id"].cpu().numpy()
+    R = np.zeros_like(A)
+    R[ro] = rr["A"][:, :ref_sc.N].T.cpu().numpy()
+    assert np.array_equal(A, R)
