@@ -712,7 +712,11 @@ __global__ void __launch_bounds__(kSahThreads) k_sah_split(const float4* __restr
   }
   // 2. bins (skipped for n == 2: split at the middle)
   if (n > 2) {
-    for (int p = first + tid; p <= last; p += kSahThreads) {
+    // each thread bins a contiguous run: the input is Morton-ordered, so lanes
+    // striding by one would all hit the same few bins (serialised atomics)
+    const int per = (n + kSahThreads - 1) / kSahThreads;
+    const int p_end = min(first + (tid + 1) * per, last + 1);
+    for (int p = first + tid * per; p < p_end; ++p) {
       const Box b = tri_box(tri, perm[p]);
       const float c[3] = {0.5f * (b.lx + b.hx), 0.5f * (b.ly + b.hy), 0.5f * (b.lz + b.hz)};
       const int lo[3] = {f2o(b.lx), f2o(b.ly), f2o(b.lz)}, hi[3] = {f2o(b.hx), f2o(b.hy), f2o(b.hz)};
