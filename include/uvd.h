@@ -244,7 +244,9 @@ UVD_API int uvd_irradiance_matrix(const uvd_scene* scene, const float* lamp_xyz,
                           uvd_matrix_out* out, void* stream);
 
 /* Synchronise `stream` and report (then clear) the scene's in-kernel error flag:
- * UVD_OK or UVD_ERR_DOMAIN. */
+ * UVD_OK, UVD_ERR_DOMAIN (a lamp–centroid distance < 1e-9 m), or UVD_ERR_CUDA
+ * for a traversal-stack overflow (cannot happen: scene creation refuses BVHs
+ * deeper than the 64-entry stacks with UVD_ERR_INVALID). */
 UVD_API int uvd_sync_status(const uvd_scene* scene, void* stream);
 
 /* ---------------------------------------------------------------------- a7 */

@@ -912,6 +912,16 @@ static int build_sah(uvd_scene* s, int64_t M, int32_t* left, int32_t* right, int
   return UVD_OK;
 }
 
+// deepest leaf (an upper bound of the traversal stack depth), via parent links
+__global__ void k_max_depth(const int32_t* __restrict__ parent_leaf, const int32_t* __restrict__ parent_int,
+                            int64_t n, int* __restrict__ depth) {
+  int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (r >= n) return;
+  int d = 1;
+  for (int32_t p = parent_leaf[r]; p != 0 && d < 4096; p = parent_int[p]) ++d;
+  atomicMax(depth, d);
+}
+
 #ifndef UVD_BVH_DEFAULT
 #define UVD_BVH_DEFAULT 2  // binned SAH; UVD_BVH=ploc / karras select the others
 #endif
@@ -977,6 +987,21 @@ int build_bvh(uvd_scene* s, float4* tri_in, uint32_t** order_out, cudaStream_t s
       note_launch();
     } else {  // PLOC (default): agglomerative clustering over the Morton order
       UVD_TRY(build_ploc(s, M, left, right, rf, rl, pint, pleaf, ibox, arrive, vals, st));
+    }
+    {  // the traversal stacks hold 64 entries: refuse deeper trees loudly
+      int* dd = (int*)al.get(sizeof(int));
+      if (!dd) { set_error("scene: out of device memory"); return UVD_ERR_NOMEM; }
+      UVD_CUDA_TRY(cudaMemsetAsync(dd, 0, sizeof(int), st));
+      k_max_depth<<<grid_for(M, 256), 256, 0, st>>>(pleaf, pint, M, dd);
+      note_launch();
+      int hd = 0;
+      UVD_CUDA_TRY(cudaMemcpyAsync(&hd, dd, sizeof(int), cudaMemcpyDeviceToHost, st));
+      UVD_CUDA_TRY(cudaStreamSynchronize(st));
+      al.put(dd);
+      if (hd > 62) {
+        set_error("scene: BVH depth %d exceeds the traversal stack (64)", hd);
+        return UVD_ERR_INVALID;
+      }
     }
     int32_t* pre = (int32_t*)arrive;  // arrival counters are free again
     k_preorder<<<grid_for(ni, 256), 256, 0, st>>>(left, pint, rf, rl, ni, pre);

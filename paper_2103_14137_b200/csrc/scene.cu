@@ -510,6 +510,10 @@ extern "C" int uvd_sync_status(const uvd_scene* s, void* stream) {
   const int flag = *hflag;
   if (flag) {
     UVD_CUDA_TRY(cudaMemsetAsync(s->err_flag, 0, sizeof(int), st));
+    if (flag == 2) {  // cannot happen: scene creation refuses trees deeper than the stacks
+      set_error("traversal stack overflow (BVH deeper than 64)");
+      return UVD_ERR_CUDA;
+    }
     set_error("lamp–centroid distance below 1e-9 m (S:160)");
     return UVD_ERR_DOMAIN;
   }
