@@ -649,7 +649,9 @@ static int build_ploc(uvd_scene* s, int64_t M, int32_t* left, int32_t* right, in
 #define UVD_SAH_BINS 32
 #endif
 constexpr int kSahBins = UVD_SAH_BINS;
-constexpr int kSahBig = 8192;  // nodes above this many triangles get 1024-thread CTAs
+constexpr int kSahBig = 8192;     // nodes above this many triangles get 1024-thread CTAs
+constexpr int kSahHuge = 65536;   // ... and above this, several CTAs (chunks of kSahChunk)
+constexpr int kSahChunk = 32768;
 
 __device__ __forceinline__ int f2o(float f) {  // order-preserving float -> int
   const int i = __float_as_int(f);
@@ -662,6 +664,31 @@ __device__ __forceinline__ float sah_area(float lx, float ly, float lz, float hx
   return dx * dy + dy * dz + dz * dx;
 }
 
+// children of a split node: a single triangle is a leaf reference, larger
+// ranges become internal nodes routed to the next level's small / big / huge list
+__device__ void sah_children(int node, int first, int last, int nl, int32_t* rf, int32_t* rl, int32_t* left,
+                             int32_t* right, int32_t* pint, int32_t* pleaf, int* ctr, int32_t* next,
+                             int32_t* next_big, int32_t* next_huge, int huge) {
+  const int lo[2] = {first, first + nl}, hi[2] = {first + nl - 1, last};
+  int32_t ref[2];
+  for (int s = 0; s < 2; ++s) {
+    if (hi[s] == lo[s]) {
+      ref[s] = (int32_t)(0x80000000u | (uint32_t)lo[s]);
+      pleaf[lo[s]] = node;
+      continue;
+    }
+    const int id = atomicAdd(&ctr[0], 1);
+    rf[id] = lo[s]; rl[id] = hi[s]; pint[id] = node;
+    const int n = hi[s] - lo[s] + 1;
+    if (n > huge) next_huge[atomicAdd(&ctr[3], 1)] = id;
+    else if (n > kSahBig) next_big[atomicAdd(&ctr[2], 1)] = id;
+    else next[atomicAdd(&ctr[1], 1)] = id;
+    ref[s] = id;
+  }
+  left[node] = ref[0];
+  right[node] = ref[1];
+}
+
 template <int kSahThreads>
 __global__ void __launch_bounds__(kSahThreads) k_sah_split(const float4* __restrict__ tri, int32_t* __restrict__ perm,
                                                            int32_t* __restrict__ tmp, const int32_t* __restrict__ list,
@@ -669,7 +696,7 @@ __global__ void __launch_bounds__(kSahThreads) k_sah_split(const float4* __restr
                                                            int32_t* __restrict__ left, int32_t* __restrict__ right,
                                                            int32_t* __restrict__ pint, int32_t* __restrict__ pleaf,
                                                            int* __restrict__ ctr, int32_t* __restrict__ next,
-                                                           int32_t* __restrict__ next_big) {
+                                                           int32_t* __restrict__ next_big, int32_t* __restrict__ next_huge, int huge) {
   __shared__ int s_cnt[3][kSahBins];
   __shared__ int s_lo[3][kSahBins][3], s_hi[3][kSahBins][3];
   __shared__ int s_cb[6];      // centre bounds (ordered ints)
@@ -808,26 +835,200 @@ __global__ void __launch_bounds__(kSahThreads) k_sah_split(const float4* __restr
     for (int p = first + tid; p <= last; p += kSahThreads) perm[p] = tmp[p];
   }
   // 5. children
-  if (tid == 0) {
-    const int l0 = first, l1 = first + nl - 1, r0 = first + nl, r1 = last;
-    int32_t refl, refr;
-    if (l1 == l0) { refl = (int32_t)(0x80000000u | (uint32_t)l0); pleaf[l0] = node; }
-    else {
-      refl = atomicAdd(&ctr[0], 1);
-      rf[refl] = l0; rl[refl] = l1; pint[refl] = node;
-      if (l1 - l0 + 1 > kSahBig) next_big[atomicAdd(&ctr[2], 1)] = refl;
-      else next[atomicAdd(&ctr[1], 1)] = refl;
-    }
-    if (r1 == r0) { refr = (int32_t)(0x80000000u | (uint32_t)r0); pleaf[r0] = node; }
-    else {
-      refr = atomicAdd(&ctr[0], 1);
-      rf[refr] = r0; rl[refr] = r1; pint[refr] = node;
-      if (r1 - r0 + 1 > kSahBig) next_big[atomicAdd(&ctr[2], 1)] = refr;
-      else next[atomicAdd(&ctr[1], 1)] = refr;
-    }
-    left[node] = refl;
-    right[node] = refr;
+  if (tid == 0) sah_children(node, first, last, nl, rf, rl, left, right, pint, pleaf, ctr, next, next_big, next_huge, huge);
+}
+
+// ---- huge nodes: several CTAs per node, one per chunk of kSahChunk positions ----
+struct SahChunks {
+  const int32_t* node;   // [n_chunks] node id
+  const int32_t* hidx;   // [n_chunks] index of the node in this level's huge list
+  const int32_t* cbeg;   // [n_chunks] first position
+  const int32_t* cend;   // [n_chunks] last position + 1
+  const int32_t* hfirst; // [n_huge + 1] first chunk of each huge node
+  int* cb;               // [n_huge][6] centre bounds (ordered ints)
+  int* bcnt;             // [n_huge][3][B] bin counts
+  int* blo;              // [n_huge][3][B][3] bin box lows (ordered ints)
+  int* bhi;              // [n_huge][3][B][3]
+  int* ccnt;             // [n_chunks][3][B] per-chunk bin counts
+  int* split;            // [n_huge][3] axis, bin, n_left
+  int* off;              // [n_chunks][2] left / right offsets of each chunk within its node
+};
+
+constexpr int kHugeThreads = 1024;
+
+__global__ void __launch_bounds__(kHugeThreads) k_sah_huge_bounds(const float4* __restrict__ tri,
+                                                                   const int32_t* __restrict__ perm, SahChunks C) {
+  const int c = blockIdx.x, h = C.hidx[c];
+  float cl[3] = {INFINITY, INFINITY, INFINITY}, ch[3] = {-INFINITY, -INFINITY, -INFINITY};
+  for (int p = C.cbeg[c] + threadIdx.x; p < C.cend[c]; p += kHugeThreads) {
+    const Box b = tri_box(tri, perm[p]);
+    const float x[3] = {0.5f * (b.lx + b.hx), 0.5f * (b.ly + b.hy), 0.5f * (b.lz + b.hz)};
+    for (int a = 0; a < 3; ++a) { cl[a] = fminf(cl[a], x[a]); ch[a] = fmaxf(ch[a], x[a]); }
   }
+  for (int a = 0; a < 3; ++a)
+    for (int o = 16; o > 0; o >>= 1) {
+      cl[a] = fminf(cl[a], __shfl_xor_sync(0xffffffffu, cl[a], o));
+      ch[a] = fmaxf(ch[a], __shfl_xor_sync(0xffffffffu, ch[a], o));
+    }
+  if ((threadIdx.x & 31) == 0)
+    for (int a = 0; a < 3; ++a) { atomicMin(&C.cb[6 * h + a], f2o(cl[a])); atomicMax(&C.cb[6 * h + 3 + a], f2o(ch[a])); }
+}
+
+__device__ __forceinline__ void huge_scale(const SahChunks& C, int h, float* cmin, float* cscale) {
+  for (int a = 0; a < 3; ++a) {
+    const float lo = o2f(C.cb[6 * h + a]), hi = o2f(C.cb[6 * h + 3 + a]);
+    cmin[a] = lo;
+    cscale[a] = hi > lo ? (float)kSahBins / (hi - lo) : 0.f;
+  }
+}
+
+__global__ void __launch_bounds__(kHugeThreads) k_sah_huge_bins(const float4* __restrict__ tri,
+                                                                 const int32_t* __restrict__ perm, SahChunks C) {
+  __shared__ int s_cnt[3][kSahBins];
+  __shared__ int s_lo[3][kSahBins][3], s_hi[3][kSahBins][3];
+  const int c = blockIdx.x, h = C.hidx[c], tid = threadIdx.x;
+  if (tid < 3 * kSahBins) {
+    const int a = tid / kSahBins, b = tid % kSahBins;
+    s_cnt[a][b] = 0;
+    for (int k = 0; k < 3; ++k) { s_lo[a][b][k] = 0x7fffffff; s_hi[a][b][k] = (int)0x80000000; }
+  }
+  __syncthreads();
+  float cmin[3], cscale[3];
+  huge_scale(C, h, cmin, cscale);
+  const int beg = C.cbeg[c], n = C.cend[c] - beg;
+  const int per = (n + kHugeThreads - 1) / kHugeThreads;
+  const int p_end = min(beg + (tid + 1) * per, beg + n);
+  for (int p = beg + tid * per; p < p_end; ++p) {
+    const Box b = tri_box(tri, perm[p]);
+    const float x[3] = {0.5f * (b.lx + b.hx), 0.5f * (b.ly + b.hy), 0.5f * (b.lz + b.hz)};
+    const int lo[3] = {f2o(b.lx), f2o(b.ly), f2o(b.lz)}, hi[3] = {f2o(b.hx), f2o(b.hy), f2o(b.hz)};
+    for (int a = 0; a < 3; ++a) {
+      if (cscale[a] == 0.f) continue;
+      const int bin = min(kSahBins - 1, max(0, (int)((x[a] - cmin[a]) * cscale[a])));
+      atomicAdd(&s_cnt[a][bin], 1);
+      for (int k = 0; k < 3; ++k) { atomicMin(&s_lo[a][bin][k], lo[k]); atomicMax(&s_hi[a][bin][k], hi[k]); }
+    }
+  }
+  __syncthreads();
+  if (tid < 3 * kSahBins) {
+    const int a = tid / kSahBins, b = tid % kSahBins, cnt = s_cnt[a][b];
+    C.ccnt[(c * 3 + a) * kSahBins + b] = cnt;
+    if (cnt) {
+      atomicAdd(&C.bcnt[(h * 3 + a) * kSahBins + b], cnt);
+      for (int k = 0; k < 3; ++k) {
+        atomicMin(&C.blo[((h * 3 + a) * kSahBins + b) * 3 + k], s_lo[a][b][k]);
+        atomicMax(&C.bhi[((h * 3 + a) * kSahBins + b) * 3 + k], s_hi[a][b][k]);
+      }
+    }
+  }
+}
+
+// one thread per huge node: the split, the chunks' partition offsets, the children
+__global__ void k_sah_huge_decide(const int32_t* __restrict__ list, int n_huge, SahChunks C, int32_t* rf, int32_t* rl,
+                                  int32_t* left, int32_t* right, int32_t* pint, int32_t* pleaf, int* ctr,
+                                  int32_t* next, int32_t* next_big, int32_t* next_huge, int huge) {
+  const int h = blockIdx.x * blockDim.x + threadIdx.x;
+  if (h >= n_huge) return;
+  const int node = list[h], first = rf[node], last = rl[node], n = last - first + 1;
+  float cmin[3], cscale[3];
+  huge_scale(C, h, cmin, cscale);
+  float best = INFINITY;
+  int ba = -1, bb = -1, bnl = 0;
+  for (int a = 0; a < 3; ++a) {
+    if (cscale[a] == 0.f) continue;
+    const int* cnt = C.bcnt + (h * 3 + a) * kSahBins;
+    const int* blo = C.blo + (h * 3 + a) * kSahBins * 3;
+    const int* bhi = C.bhi + (h * 3 + a) * kSahBins * 3;
+    float rarea[kSahBins];
+    int rcnt[kSahBins];
+    float lx = INFINITY, ly = INFINITY, lz = INFINITY, hx = -INFINITY, hy = -INFINITY, hz = -INFINITY;
+    int c = 0;
+    for (int b = kSahBins - 1; b >= 0; --b) {
+      if (cnt[b]) {
+        lx = fminf(lx, o2f(blo[3 * b])); ly = fminf(ly, o2f(blo[3 * b + 1])); lz = fminf(lz, o2f(blo[3 * b + 2]));
+        hx = fmaxf(hx, o2f(bhi[3 * b])); hy = fmaxf(hy, o2f(bhi[3 * b + 1])); hz = fmaxf(hz, o2f(bhi[3 * b + 2]));
+        c += cnt[b];
+      }
+      rarea[b] = c ? sah_area(lx, ly, lz, hx, hy, hz) : 0.f;
+      rcnt[b] = c;
+    }
+    lx = ly = lz = INFINITY; hx = hy = hz = -INFINITY;
+    c = 0;
+    for (int b = 0; b < kSahBins - 1; ++b) {
+      if (cnt[b]) {
+        lx = fminf(lx, o2f(blo[3 * b])); ly = fminf(ly, o2f(blo[3 * b + 1])); lz = fminf(lz, o2f(blo[3 * b + 2]));
+        hx = fmaxf(hx, o2f(bhi[3 * b])); hy = fmaxf(hy, o2f(bhi[3 * b + 1])); hz = fmaxf(hz, o2f(bhi[3 * b + 2]));
+        c += cnt[b];
+      }
+      if (c == 0 || rcnt[b + 1] == 0) continue;
+      const float cost = sah_area(lx, ly, lz, hx, hy, hz) * c + rarea[b + 1] * rcnt[b + 1];
+      if (cost < best) { best = cost; ba = a; bb = b; bnl = c; }
+    }
+  }
+  const int nl = ba < 0 ? n / 2 : bnl;
+  C.split[3 * h] = ba; C.split[3 * h + 1] = bb; C.split[3 * h + 2] = nl;
+  // stable partition offsets of each chunk (chunks are in position order)
+  int before_l = 0, before = 0;
+  for (int cc = C.hfirst[h]; cc < C.hfirst[h + 1]; ++cc) {
+    int l = 0;
+    if (ba >= 0)
+      for (int b = 0; b <= bb; ++b) l += C.ccnt[(cc * 3 + ba) * kSahBins + b];
+    C.off[2 * cc] = before_l;
+    C.off[2 * cc + 1] = before - before_l;
+    before_l += l;
+    before += C.cend[cc] - C.cbeg[cc];
+  }
+  sah_children(node, first, last, nl, rf, rl, left, right, pint, pleaf, ctr, next, next_big, next_huge, huge);
+}
+
+__global__ void __launch_bounds__(kHugeThreads) k_sah_huge_partition(const float4* __restrict__ tri,
+                                                                      const int32_t* __restrict__ perm,
+                                                                      int32_t* __restrict__ tmp, const int32_t* __restrict__ rf,
+                                                                      SahChunks C) {
+  __shared__ int s_scan[kHugeThreads / 32];
+  const int c = blockIdx.x, h = C.hidx[c], tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const int sa = C.split[3 * h], sb = C.split[3 * h + 1], nl = C.split[3 * h + 2];
+  const int first = rf[C.node[c]], beg = C.cbeg[c], end = C.cend[c];
+  if (sa < 0) {  // median split by position: the order is kept
+    for (int p = beg + tid; p < end; p += kHugeThreads) tmp[p] = perm[p];
+    return;
+  }
+  float cmin[3], cscale[3];
+  huge_scale(C, h, cmin, cscale);
+  int base_l = C.off[2 * c], base_r = C.off[2 * c + 1];
+  for (int p0 = beg; p0 < end; p0 += kHugeThreads) {
+    const int p = p0 + tid;
+    int flag = 0, t = 0;
+    if (p < end) {
+      t = perm[p];
+      const Box b = tri_box(tri, t);
+      const float x = sa == 0 ? 0.5f * (b.lx + b.hx) : sa == 1 ? 0.5f * (b.ly + b.hy) : 0.5f * (b.lz + b.hz);
+      flag = min(kSahBins - 1, max(0, (int)((x - cmin[sa]) * cscale[sa]))) <= sb;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, flag);
+    const int in_warp = __popc(bal & ((1u << lane) - 1u));
+    if (lane == 0) s_scan[wid] = __popc(bal);
+    __syncthreads();
+    int before = 0, total = 0;
+    for (int w = 0; w < kHugeThreads / 32; ++w) {
+      const int v = s_scan[w];
+      if (w < wid) before += v;
+      total += v;
+    }
+    if (p < end) {
+      const int rank_l = base_l + before + in_warp;
+      const int rank_r = base_r + (p - p0 - (before + in_warp));
+      tmp[flag ? first + rank_l : first + nl + rank_r] = t;
+    }
+    base_l += total;
+    base_r += min(kHugeThreads, end - p0) - total;
+    __syncthreads();
+  }
+}
+
+__global__ void k_sah_huge_copy(int32_t* __restrict__ perm, const int32_t* __restrict__ tmp, SahChunks C) {
+  const int c = blockIdx.x;
+  for (int p = C.cbeg[c] + threadIdx.x; p < C.cend[c]; p += blockDim.x) perm[p] = tmp[p];
 }
 
 __global__ void k_iota32(int32_t* __restrict__ x, int64_t n) {
@@ -852,41 +1053,122 @@ __global__ void k_gather_u32(const uint32_t* __restrict__ in, const int32_t* __r
 static int build_sah(uvd_scene* s, int64_t M, int32_t* left, int32_t* right, int32_t* rf, int32_t* rl,
                      int32_t* pint, int32_t* pleaf, float* ibox, int* arrive, uint32_t* order, cudaStream_t st) {
   Alloc& al = s->alloc;
+  // thresholds of the multi-CTA path; UVD_SAH_HUGE / UVD_SAH_CHUNK override them (tests
+  // force the chunked path on small scenes with them)
+  auto env_pos = [](const char* name, int dflt) {
+    const char* e = getenv(name);
+    const int v = e ? atoi(e) : 0;
+    return v >= 2 ? v : dflt;
+  };
+  const int huge = std::max(env_pos("UVD_SAH_HUGE", kSahHuge), 2), chunk = env_pos("UVD_SAH_CHUNK", kSahChunk);
   int32_t* perm = (int32_t*)al.get(M * 4);
   int32_t* tmp = (int32_t*)al.get(M * 4);
   int32_t* la = (int32_t*)al.get(M * 4);   // small-node lists (this level, next level)
   int32_t* lb = (int32_t*)al.get(M * 4);
   int32_t* ba = (int32_t*)al.get(M * 4);   // big-node lists
   int32_t* bb = (int32_t*)al.get(M * 4);
+  const int64_t max_huge = M / huge + 2, max_chunks = M / chunk + 2 * max_huge + 2;
+  int32_t* ha = (int32_t*)al.get(max_huge * 4);  // huge-node lists
+  int32_t* hb = (int32_t*)al.get(max_huge * 4);
+  // chunk tables and per-huge-node bins (one block of scratch)
+  const size_t huge_ints = (size_t)max_chunks * (4 + 3 * kSahBins + 2) + (size_t)(max_huge + 1) +
+                           (size_t)max_huge * (6 + 3 * kSahBins * 7 + 3);
+  int* hs = (int*)al.get(huge_ints * sizeof(int));
   int* ctr = (int*)al.get(4 * sizeof(int));
   float4* tri2 = (float4*)al.get(3 * M * sizeof(float4));
-  if (!perm || !tmp || !la || !lb || !ba || !bb || !ctr || !tri2) {
+  if (!perm || !tmp || !la || !lb || !ba || !bb || !ha || !hb || !hs || !ctr || !tri2) {
     set_error("scene: out of device memory (SAH scratch)");
     return UVD_ERR_NOMEM;
   }
+  SahChunks C;
+  {
+    int* q = hs;
+    C.node = q; q += max_chunks;
+    C.hidx = q; q += max_chunks;
+    C.cbeg = q; q += max_chunks;
+    C.cend = q; q += max_chunks;
+    C.ccnt = q; q += (size_t)max_chunks * 3 * kSahBins;
+    C.off = q; q += (size_t)max_chunks * 2;
+    C.hfirst = q; q += max_huge + 1;
+    C.cb = q; q += (size_t)max_huge * 6;
+    C.bcnt = q; q += (size_t)max_huge * 3 * kSahBins;
+    C.blo = q; q += (size_t)max_huge * 3 * kSahBins * 3;
+    C.bhi = q; q += (size_t)max_huge * 3 * kSahBins * 3;
+    C.split = q; q += (size_t)max_huge * 3;
+  }
+  std::vector<int32_t> h_list, h_rf, h_rl, t_node, t_hidx, t_beg, t_end, t_first;
+  std::vector<int> h_init;
   k_iota32<<<grid_for(M, 256), 256, 0, st>>>(perm, M);
   note_launch();
-  int h[4] = {1, 0, 0, 0};  // next internal node id, next-level small / big list lengths
+  int h[4] = {1, 0, 0, 0};  // next internal node id, next-level small / big / huge list lengths
   int32_t zero = 0, last = (int32_t)(M - 1);
   UVD_CUDA_TRY(cudaMemcpyAsync(rf, &zero, 4, cudaMemcpyHostToDevice, st));
   UVD_CUDA_TRY(cudaMemcpyAsync(rl, &last, 4, cudaMemcpyHostToDevice, st));
-  UVD_CUDA_TRY(cudaMemcpyAsync(M > kSahBig ? ba : la, &zero, 4, cudaMemcpyHostToDevice, st));
+  UVD_CUDA_TRY(cudaMemcpyAsync(M > huge ? ha : M > kSahBig ? ba : la, &zero, 4, cudaMemcpyHostToDevice, st));
   UVD_CUDA_TRY(cudaMemcpyAsync(pint, &zero, 4, cudaMemcpyHostToDevice, st));
   UVD_CUDA_TRY(cudaMemcpyAsync(ctr, h, sizeof(int), cudaMemcpyHostToDevice, st));  // node id 1 next
-  int n_small = M > kSahBig ? 0 : 1, n_big = M > kSahBig ? 1 : 0, levels = 0;
-  while (n_small + n_big > 0) {
-    UVD_CUDA_TRY(cudaMemsetAsync(ctr + 1, 0, 2 * sizeof(int), st));  // next level's list lengths
+  int n_small = M <= kSahBig && M <= huge, n_big = M > kSahBig && M <= huge, n_huge = M > huge, levels = 0;
+  while (n_small + n_big + n_huge > 0) {
+    UVD_CUDA_TRY(cudaMemsetAsync(ctr + 1, 0, 3 * sizeof(int), st));  // next level's list lengths
+    if (n_huge) {
+      // chunk table of this level's huge nodes (few: host-built)
+      h_list.resize(n_huge); h_rf.resize(n_huge); h_rl.resize(n_huge);
+      UVD_CUDA_TRY(cudaMemcpyAsync(h_list.data(), ha, n_huge * 4, cudaMemcpyDeviceToHost, st));
+      UVD_CUDA_TRY(cudaStreamSynchronize(st));
+      for (int k = 0; k < n_huge; ++k) {
+        UVD_CUDA_TRY(cudaMemcpyAsync(&h_rf[k], rf + h_list[k], 4, cudaMemcpyDeviceToHost, st));
+        UVD_CUDA_TRY(cudaMemcpyAsync(&h_rl[k], rl + h_list[k], 4, cudaMemcpyDeviceToHost, st));
+      }
+      UVD_CUDA_TRY(cudaStreamSynchronize(st));
+      t_node.clear(); t_hidx.clear(); t_beg.clear(); t_end.clear(); t_first.assign(1, 0);
+      for (int k = 0; k < n_huge; ++k) {
+        for (int p = h_rf[k]; p <= h_rl[k]; p += chunk) {
+          t_node.push_back(h_list[k]); t_hidx.push_back(k);
+          t_beg.push_back(p); t_end.push_back(std::min(p + chunk, h_rl[k] + 1));
+        }
+        t_first.push_back((int32_t)t_node.size());
+      }
+      const int nch = (int)t_node.size();
+      if (nch > max_chunks) { set_error("scene: SAH chunk table overflow"); return UVD_ERR_CUDA; }
+      UVD_CUDA_TRY(cudaMemcpyAsync((void*)C.node, t_node.data(), nch * 4, cudaMemcpyHostToDevice, st));
+      UVD_CUDA_TRY(cudaMemcpyAsync((void*)C.hidx, t_hidx.data(), nch * 4, cudaMemcpyHostToDevice, st));
+      UVD_CUDA_TRY(cudaMemcpyAsync((void*)C.cbeg, t_beg.data(), nch * 4, cudaMemcpyHostToDevice, st));
+      UVD_CUDA_TRY(cudaMemcpyAsync((void*)C.cend, t_end.data(), nch * 4, cudaMemcpyHostToDevice, st));
+      UVD_CUDA_TRY(cudaMemcpyAsync((void*)C.hfirst, t_first.data(), (n_huge + 1) * 4, cudaMemcpyHostToDevice, st));
+      // per-node bounds / bins reset: ordered-int "+inf" lows, "-inf" highs, zero counts
+      h_init.assign((size_t)n_huge * (6 + 3 * kSahBins * 7), 0);
+      for (int k = 0; k < n_huge; ++k)
+        for (int a = 0; a < 6; ++a) h_init[6 * k + a] = a < 3 ? 0x7fffffff : (int)0x80000000;
+      int* bcnt0 = h_init.data() + 6 * n_huge;
+      int* blo0 = bcnt0 + (size_t)n_huge * 3 * kSahBins;
+      int* bhi0 = blo0 + (size_t)n_huge * 3 * kSahBins * 3;
+      for (size_t q = 0; q < (size_t)n_huge * 3 * kSahBins * 3; ++q) { blo0[q] = 0x7fffffff; bhi0[q] = (int)0x80000000; }
+      UVD_CUDA_TRY(cudaMemcpyAsync(C.cb, h_init.data(), (size_t)n_huge * 6 * 4, cudaMemcpyHostToDevice, st));
+      UVD_CUDA_TRY(cudaMemcpyAsync(C.bcnt, bcnt0, (size_t)n_huge * 3 * kSahBins * 4, cudaMemcpyHostToDevice, st));
+      UVD_CUDA_TRY(cudaMemcpyAsync(C.blo, blo0, (size_t)n_huge * 3 * kSahBins * 3 * 4, cudaMemcpyHostToDevice, st));
+      UVD_CUDA_TRY(cudaMemcpyAsync(C.bhi, bhi0, (size_t)n_huge * 3 * kSahBins * 3 * 4, cudaMemcpyHostToDevice, st));
+      k_sah_huge_bounds<<<nch, kHugeThreads, 0, st>>>(s->tri, perm, C);
+      k_sah_huge_bins<<<nch, kHugeThreads, 0, st>>>(s->tri, perm, C);
+      k_sah_huge_decide<<<(n_huge + 31) / 32, 32, 0, st>>>(ha, n_huge, C, rf, rl, left, right, pint, pleaf, ctr, lb,
+                                                            bb, hb, huge);
+      k_sah_huge_partition<<<nch, kHugeThreads, 0, st>>>(s->tri, perm, tmp, rf, C);
+      k_sah_huge_copy<<<nch, 1024, 0, st>>>(perm, tmp, C);
+      note_launch(5);
+      UVD_CUDA_TRY(cudaStreamSynchronize(st));  // the host vectors above are reused next level
+    }
     if (n_big)
-      k_sah_split<1024><<<n_big, 1024, 0, st>>>(s->tri, perm, tmp, ba, rf, rl, left, right, pint, pleaf, ctr, lb, bb);
+      k_sah_split<1024><<<n_big, 1024, 0, st>>>(s->tri, perm, tmp, ba, rf, rl, left, right, pint, pleaf, ctr, lb, bb, hb, huge);
     if (n_small)
-      k_sah_split<128><<<n_small, 128, 0, st>>>(s->tri, perm, tmp, la, rf, rl, left, right, pint, pleaf, ctr, lb, bb);
+      k_sah_split<128><<<n_small, 128, 0, st>>>(s->tri, perm, tmp, la, rf, rl, left, right, pint, pleaf, ctr, lb, bb, hb, huge);
     note_launch((n_big > 0) + (n_small > 0));
-    UVD_CUDA_TRY(cudaMemcpyAsync(h, ctr, 3 * sizeof(int), cudaMemcpyDeviceToHost, st));
+    UVD_CUDA_TRY(cudaMemcpyAsync(h, ctr, 4 * sizeof(int), cudaMemcpyDeviceToHost, st));
     UVD_CUDA_TRY(cudaStreamSynchronize(st));
     n_small = h[1];
     n_big = h[2];
+    n_huge = h[3];
     std::swap(la, lb);
     std::swap(ba, bb);
+    std::swap(ha, hb);
     if (++levels > 4096) { set_error("scene: SAH build did not terminate"); return UVD_ERR_CUDA; }
   }
   if (h[0] != M - 1) { set_error("scene: SAH build made %d internal nodes, expected %lld", h[0], (long long)(M - 1)); return UVD_ERR_CUDA; }
@@ -907,7 +1189,8 @@ static int build_sah(uvd_scene* s, int64_t M, int32_t* left, int32_t* right, int
   k_refit<<<grid_for(M, 256), 256, 0, st>>>(s->tri, M, left, right, pint, pleaf, ibox, arrive);
   note_launch();
   UVD_CUDA_TRY(cudaGetLastError());
-  for (void* p : {(void*)perm, (void*)tmp, (void*)la, (void*)lb, (void*)ba, (void*)bb, (void*)ctr, (void*)tri2})
+  for (void* p : {(void*)perm, (void*)tmp, (void*)la, (void*)lb, (void*)ba, (void*)bb, (void*)ha, (void*)hb,
+                  (void*)hs, (void*)ctr, (void*)tri2})
     al.put(p);
   return UVD_OK;
 }

@@ -118,12 +118,18 @@ def test_bvh_tiny(uvd):
     assert b["nodes"].shape[0] == 1
 
 
-@pytest.mark.parametrize("builder", ["sah", "ploc", "karras"])
+@pytest.mark.parametrize("builder", ["sah", "sah-chunked", "ploc", "karras"])
 def test_builders_give_identical_matrices(uvd, builder, monkeypatch):
     """The three builders (binned SAH default, PLOC, Karras LBVH) make
     different trees; the occlusion decisions — hence A and the visibility bits
-    in input row order — are identical (exact tests, tree-independent)."""
+    in input row order — are identical (exact tests, tree-independent).
+    "sah-chunked" forces the SAH builder's multi-CTA path for nodes above 1000
+    triangles, in chunks of 300 positions (ragged last chunks)."""
     w = ward.ward(seed=5, n_bays=1, e=0.25)
+    if builder == "sah-chunked":
+        monkeypatch.setenv("UVD_SAH_HUGE", "1000")
+        monkeypatch.setenv("UVD_SAH_CHUNK", "300")
+        builder = "sah"
     monkeypatch.setenv("UVD_BVH", builder)
     sc = uvd.Scene(w)
     check_tree(sc, w["vertices"][w["tris"]])
@@ -133,9 +139,29 @@ def test_builders_give_identical_matrices(uvd, builder, monkeypatch):
     A = np.zeros((sc.N, lam.shape[0]), np.float32)
     A[orig] = r["A"][:, :sc.N].T.cpu().numpy()
     monkeypatch.setenv("UVD_BVH", "sah")
+    monkeypatch.delenv("UVD_SAH_HUGE", raising=False)
+    monkeypatch.delenv("UVD_SAH_CHUNK", raising=False)
     ref_sc = uvd.Scene(w)
     rr = ref_sc.irradiance(lam)
     ro = ref_sc.patches()["orig_id"].cpu().numpy()
     R = np.zeros_like(A)
     R[ro] = rr["A"][:, :ref_sc.N].T.cpu().numpy()
     assert np.array_equal(A, R)
+
+
+def test_sah_chunked_same_tree(uvd, monkeypatch):
+    """The multi-CTA (chunked) SAH path bins the same centroids into the same
+    bins as the one-CTA path, and picks the split by the same sweep: the trees
+    have the same SAH split decisions, so the same leaf order of triangles."""
+    w = ward.ward(seed=6, n_bays=1, e=0.2)
+    monkeypatch.setenv("UVD_BVH", "sah")
+    a = uvd.Scene(w).bvh()
+    monkeypatch.setenv("UVD_SAH_HUGE", "64")
+    monkeypatch.setenv("UVD_SAH_CHUNK", "100")
+    sc = uvd.Scene(w)
+    b = check_tree(sc, w["vertices"][w["tris"]])
+    # the leaf order can differ only where a bin's atomic box merge order differs
+    # (it cannot: min / max are order-free), so the triangle order is identical
+    ta = a["tri"].cpu().numpy()[:, 7].view(np.int32)
+    tb = b["tri"].cpu().numpy()[:, 7].view(np.int32)
+    assert np.array_equal(ta, tb)
