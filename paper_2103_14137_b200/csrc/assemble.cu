@@ -551,33 +551,61 @@ __device__ void fixup_entry(const AsmParams& P, int64_t c, int r) {
   if (P.values) P.values[c * P.ld + r] = (float)(P.area_m >= 0 ? acc * P.scale / P.area[r] : acc * P.scale);
 }
 
-__global__ void k_fixup_collect(AsmParams P, uint64_t* __restrict__ list, int64_t cap,
-                                unsigned long long* __restrict__ count) {
+// out-of-line: keeps the collect loop's registers free of the re-trace
+__device__ __noinline__ void fixup_entry_overflow(const AsmParams& P, int64_t c, int r) { fixup_entry(P, c, r); }
+
+// Compaction of the pending bits into (column, row) entries: each thread owns 4
+// consecutive words, blocks with no pending bit (almost all) leave after one
+// __syncthreads_or; otherwise one atomic per block reserves the slots.
+constexpr int kCollectThreads = 256, kCollectWords = 4;
+__global__ void __launch_bounds__(kCollectThreads) k_fixup_collect(AsmParams P, uint64_t* __restrict__ list,
+                                                                    int64_t cap,
+                                                                    unsigned long long* __restrict__ count) {
+  __shared__ int s_warp[kCollectThreads / 32];
+  __shared__ unsigned long long s_base;
   const int64_t nwords = P.n_cols * P.words;
-  const int lane = threadIdx.x & 31;
-  for (int64_t w0 = blockIdx.x * (int64_t)blockDim.x; w0 < nwords; w0 += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t w = w0 + threadIdx.x;
-    uint32_t bits = w < nwords ? P.pending[w] : 0u;
-    const int n = __popc(bits);
-    int incl = n;  // warp inclusive scan of the counts
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  constexpr int64_t kPer = (int64_t)kCollectThreads * kCollectWords;
+  for (int64_t w0 = blockIdx.x * kPer; w0 < nwords; w0 += (int64_t)gridDim.x * kPer) {
+    const int64_t w = w0 + (int64_t)threadIdx.x * kCollectWords;
+    uint32_t bits[kCollectWords];
+    int n = 0;
+#pragma unroll
+    for (int k = 0; k < kCollectWords; ++k) {
+      bits[k] = w + k < nwords ? P.pending[w + k] : 0u;
+      n += __popc(bits[k]);
+    }
+    if (!__syncthreads_or(n)) continue;
+    int incl = n;  // block exclusive scan of the counts
     for (int o = 1; o < 32; o <<= 1) {
       const int v = __shfl_up_sync(0xffffffffu, incl, o);
       if (lane >= o) incl += v;
     }
-    const int total = __shfl_sync(0xffffffffu, incl, 31);
-    unsigned long long base = 0;
-    if (lane == 31 && total) base = atomicAdd(count, (unsigned long long)total);
-    base = __shfl_sync(0xffffffffu, base, 31);
-    int64_t slot = (int64_t)base + incl - n;
-    if (!bits) continue;
-    const int64_t c = w / P.words, word = w - c * P.words;
-    while (bits) {
-      const int b = __ffs(bits) - 1;
-      bits &= bits - 1;
-      const int r = (int)(word * 32 + b);
-      if (slot < cap) list[slot] = ((uint64_t)c << 32) | (uint32_t)r;
-      else fixup_entry(P, c, r);  // list full: re-trace here
-      ++slot;
+    if (lane == 31) s_warp[wid] = incl;
+    __syncthreads();
+    int before = 0, total = 0;
+#pragma unroll
+    for (int k = 0; k < kCollectThreads / 32; ++k) {
+      const int v = s_warp[k];
+      before += k < wid ? v : 0;
+      total += v;
+    }
+    if (threadIdx.x == 0) s_base = atomicAdd(count, (unsigned long long)total);
+    __syncthreads();
+    int64_t slot = (int64_t)s_base + before + incl - n;
+    __syncthreads();  // s_warp / s_base are rewritten by the next iteration
+#pragma unroll
+    for (int k = 0; k < kCollectWords; ++k) {
+      uint32_t b = bits[k];
+      if (!b) continue;
+      const int64_t wk = w + k, c = wk / P.words, word = wk - c * P.words;
+      while (b) {
+        const int r = (int)(word * 32 + __ffs(b) - 1);
+        b &= b - 1;
+        if (slot < cap) list[slot] = ((uint64_t)c << 32) | (uint32_t)r;
+        else fixup_entry_overflow(P, c, r);  // list full: re-trace here
+        ++slot;
+      }
     }
   }
 }
@@ -746,13 +774,15 @@ extern "C" int uvd_irradiance_matrix(const uvd_scene* s, const float* lamp_xyz, 
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t nwords = n_cols * P.words;
-    const int64_t cap = std::min<int64_t>(nwords * 32, (int64_t)1 << 22);
+    // room for 2^24 entries (128 MB): C5 flags ~6.6 M; beyond it the collect kernel re-traces inline
+    const int64_t cap = std::min<int64_t>(nwords * 32, (int64_t)1 << 24);
     uint64_t* list = (uint64_t*)al.get((size_t)cap * sizeof(uint64_t) + 256);
     if (!list) { set_error("uvd_irradiance_matrix: out of device memory"); return UVD_ERR_NOMEM; }
     unsigned long long* count = (unsigned long long*)((char*)list + (size_t)cap * sizeof(uint64_t));
     UVD_CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(unsigned long long), st));
-    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nwords + 255) / 256, 8 * sms));
-    k_fixup_collect<<<g, 256, 0, st>>>(P, list, cap, count);
+    const int64_t per = (int64_t)kCollectThreads * kCollectWords;
+    const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nwords + per - 1) / per, 8 * sms));
+    k_fixup_collect<<<g, kCollectThreads, 0, st>>>(P, list, cap, count);
     k_fixup_run<<<4 * sms, 128, 0, st>>>(P, list, cap, count);
     note_launch(2);
     al.put(list);
