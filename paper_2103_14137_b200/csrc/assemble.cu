@@ -43,6 +43,8 @@ constexpr int kAsmMinBlocks = UVD_ASM_MINB;  // 1024-thread blocks x 1 per SM: <
 struct AsmParams {
   const float4* __restrict__ tri;
   const Node* __restrict__ nodes;
+  const Node* __restrict__ onodes;  // 8 octant copies of nodes (near, far slab order)
+  int64_t n_nodes;
   uint32_t root;
   const float* __restrict__ centroid;
   const float* __restrict__ normal;
@@ -98,11 +100,15 @@ __device__ __forceinline__ int lane_walk32(const AsmParams& P, float ox, float o
   // flat leaf and its flat ancestors) are never visited
   const float tlo = (float)kSelfEps * rsqrtf(dx * dx + dy * dy + dz * dz);
   const float thi = 1.0f - tlo;
-  uint32_t ref = P.root;
+  // start in the copy of the nodes whose slabs are stored (near, far) for this
+  // ray's octant; child refs stay inside that copy
+  const uint32_t oct = (__float_as_uint(ix) >> 31) | ((__float_as_uint(iy) >> 31) << 1) |
+                       ((__float_as_uint(iz) >> 31) << 2);
+  uint32_t ref = ref_is_leaf(P.root) ? P.root : P.root + oct * (uint32_t)P.n_nodes;
   for (;;) {
     // ---- inner nodes until this lane holds a leaf (or is done) ----
     while (!ref_is_leaf(ref)) {
-      const Node* nd = P.nodes + ref;
+      const Node* nd = P.onodes + ref;
       const float4 na = __ldg(&nd->a), nb = __ldg(&nd->b), nc = __ldg(&nd->c);
       const uint2 ch = __ldg(reinterpret_cast<const uint2*>(&nd->d));
       if (COUNT) { cnt[1] += 2; cnt[3] += 1; }
@@ -110,17 +116,18 @@ __device__ __forceinline__ int lane_walk32(const AsmParams& P, float ox, float o
       // slab parameter of the plane b shifted by at most eps|o| (<= 1.2e-6 m for
       // |o| <= 20 m), which the build-time box padding (>= 1e-5 m + 4 eps x the
       // scene's largest coordinate) absorbs; the final rounding is covered by
-      // the 2e-6 relative widening
+      // the 2e-6 relative widening.  In this octant's copy the first plane of
+      // each slab is the entry (t rounds monotonically: entry <= exit).
       const float ax0 = fmaf(na.x, ix, -oix), ax1 = fmaf(na.y, ix, -oix);
       const float ay0 = fmaf(na.z, iy, -oiy), ay1 = fmaf(na.w, iy, -oiy);
       const float az0 = fmaf(nc.x, iz, -oiz), az1 = fmaf(nc.y, iz, -oiz);
       const float bx0 = fmaf(nb.x, ix, -oix), bx1 = fmaf(nb.y, ix, -oix);
       const float by0 = fmaf(nb.z, iy, -oiy), by1 = fmaf(nb.w, iy, -oiy);
       const float bz0 = fmaf(nc.z, iz, -oiz), bz1 = fmaf(nc.w, iz, -oiz);
-      const float an = fmaxf(fmaxf(fminf(ax0, ax1), fminf(ay0, ay1)), fmaxf(fminf(az0, az1), 0.0f));
-      const float af = fminf(fminf(fmaxf(ax0, ax1), fmaxf(ay0, ay1)), fminf(fmaxf(az0, az1), thi));
-      const float bn = fmaxf(fmaxf(fminf(bx0, bx1), fminf(by0, by1)), fmaxf(fminf(bz0, bz1), 0.0f));
-      const float bf = fminf(fminf(fmaxf(bx0, bx1), fmaxf(by0, by1)), fminf(fmaxf(bz0, bz1), thi));
+      const float an = fmaxf(fmaxf(ax0, ay0), fmaxf(az0, 0.0f));
+      const float af = fminf(fminf(ax1, ay1), fminf(az1, thi));
+      const float bn = fmaxf(fmaxf(bx0, by0), fmaxf(bz0, 0.0f));
+      const float bf = fminf(fminf(bx1, by1), fminf(bz1, thi));
       const bool h0 = an <= fmaf(af, 1.000002f, 1e-7f);
       const bool h1 = bn <= fmaf(bf, 1.000002f, 1e-7f);
       if (h0 && h1) {
@@ -710,6 +717,8 @@ extern "C" int uvd_irradiance_matrix(const uvd_scene* s, const float* lamp_xyz, 
   AsmParams P;
   P.tri = s->tri;
   P.nodes = s->nodes;
+  P.onodes = s->onodes;
+  P.n_nodes = s->n_nodes;
   P.root = s->root;
   P.centroid = s->centroid;
   P.normal = s->normal;

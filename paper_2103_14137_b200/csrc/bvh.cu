@@ -328,6 +328,24 @@ __global__ void k_emit(const float4* __restrict__ tri, int64_t n, const int32_t*
   nodes[pre[i]] = nd;
 }
 
+// Octant copies of the nodes: copy o (bit 0/1/2 = the ray's 1/d is negative in
+// x/y/z) stores every child box slab as (near plane, far plane) for rays of that
+// octant, so the traversal takes the slab entry and exit without a min/max per
+// axis.  Same boxes; internal child refs point into the same copy (+ o x nn).
+__global__ void k_octant_nodes(const Node* __restrict__ nodes, int64_t nn, Node* __restrict__ onodes) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= 8 * nn) return;
+  const int o = (int)(i / nn);
+  Node nd = nodes[i - o * nn];
+  float t;
+  if (o & 1) { t = nd.a.x; nd.a.x = nd.a.y; nd.a.y = t; t = nd.b.x; nd.b.x = nd.b.y; nd.b.y = t; }
+  if (o & 2) { t = nd.a.z; nd.a.z = nd.a.w; nd.a.w = t; t = nd.b.z; nd.b.z = nd.b.w; nd.b.w = t; }
+  if (o & 4) { t = nd.c.x; nd.c.x = nd.c.y; nd.c.y = t; t = nd.c.z; nd.c.z = nd.c.w; nd.c.w = t; }
+  if (!ref_is_leaf(nd.d.x)) nd.d.x += (uint32_t)(o * nn);
+  if (!ref_is_leaf(nd.d.y)) nd.d.y += (uint32_t)(o * nn);
+  onodes[i] = nd;
+}
+
 // single-leaf scene (M <= kLeafMax): a root node with one leaf child and an
 // empty second child
 __global__ void k_emit_small(const float4* __restrict__ tri, int64_t n, Node* nodes, float cp) {
@@ -1295,6 +1313,22 @@ int build_bvh(uvd_scene* s, float4* tri_in, uint32_t** order_out, cudaStream_t s
     for (void* p : {(void*)left, (void*)right, (void*)rf, (void*)rl, (void*)pint, (void*)pleaf,
                     (void*)ibox, (void*)arrive})
       al.put(p);
+  }
+  {
+    const int64_t nn = std::max<int64_t>(M - 1, 1);
+    if (8 * nn >= (int64_t)1 << 31) {
+      set_error("scene: too many triangles (%lld) for 31-bit node refs", (long long)M);
+      return UVD_ERR_INVALID;
+    }
+    if (s->onodes) al.put(s->onodes);
+    s->n_nodes = nn;
+    s->onodes = (Node*)al.get(8 * nn * sizeof(Node));
+    if (!s->onodes) {
+      set_error("scene: out of device memory (octant nodes)");
+      return UVD_ERR_NOMEM;
+    }
+    k_octant_nodes<<<grid_for(8 * nn, 256), 256, 0, st>>>(s->nodes, nn, s->onodes);
+    note_launch();
   }
   UVD_CUDA_TRY(cudaGetLastError());
   al.put(keys);

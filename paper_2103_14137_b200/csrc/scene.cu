@@ -412,7 +412,7 @@ static void free_scene(uvd_scene* s) {
   Alloc& al = s->alloc;
   for (void* p : {(void*)s->centroid, (void*)s->normal, (void*)s->area, (void*)s->orig_id,
                   (void*)s->tri, (void*)s->nodes, (void*)s->walls, (void*)s->poly_xy,
-                  (void*)s->poly_off, (void*)s->err_flag, (void*)s->cov_part, (void*)s->ptri})
+                  (void*)s->poly_off, (void*)s->err_flag, (void*)s->cov_part, (void*)s->ptri, (void*)s->onodes})
     al.put(p);
   cudaStreamSynchronize(al.stream);
   delete s;

@@ -104,6 +104,8 @@ struct uvd_scene {
   float4* tri = nullptr;      // M*3: (v0, owner patch), (v1, orig tri), (v2, 0)  leaf order
   float4* ptri = nullptr;     // EXTRUDED only: 2N*3 patch-ordered wall triangles (area model)
   uvd::Node* nodes = nullptr; // max(M-1, 1) BVH2 nodes
+  uvd::Node* onodes = nullptr; // 8 x max(M-1, 1): the nodes with each child box stored (near, far) per ray octant
+  int64_t n_nodes = 0;
   uint32_t root = 0;          // root ref
   // 2.5D description (device + host copies) for the floorplan vantage test
   uvd::Wall* walls = nullptr;  // device
