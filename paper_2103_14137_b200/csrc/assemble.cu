@@ -116,8 +116,11 @@ __device__ __forceinline__ int lane_walk32(const AsmParams& P, float ox, float o
       // slab parameter of the plane b shifted by at most eps|o| (<= 1.2e-6 m for
       // |o| <= 20 m), which the build-time box padding (>= 1e-5 m + 4 eps x the
       // scene's largest coordinate) absorbs; the final rounding is covered by
-      // the 2e-6 relative widening.  In this octant's copy the first plane of
-      // each slab is the entry (t rounds monotonically: entry <= exit).
+      // the padding as well: the FFMA's one rounding and fl(1/d) scale each t by
+      // at most (1 + 2^-23), i.e. move a plane by <= 2^-23 |b - o| <= 5e-6 m, under
+      // the >= 1e-5 m padding, so a box the exact segment meets passes an <= af
+      // with no widening.  In this octant's copy the first plane of each slab is
+      // the entry (t rounds monotonically: entry <= exit).
       const float ax0 = fmaf(na.x, ix, -oix), ax1 = fmaf(na.y, ix, -oix);
       const float ay0 = fmaf(na.z, iy, -oiy), ay1 = fmaf(na.w, iy, -oiy);
       const float az0 = fmaf(nc.x, iz, -oiz), az1 = fmaf(nc.y, iz, -oiz);
@@ -128,8 +131,8 @@ __device__ __forceinline__ int lane_walk32(const AsmParams& P, float ox, float o
       const float af = fminf(fminf(ax1, ay1), fminf(az1, thi));
       const float bn = fmaxf(fmaxf(bx0, by0), fmaxf(bz0, 0.0f));
       const float bf = fminf(fminf(bx1, by1), fminf(bz1, thi));
-      const bool h0 = an <= fmaf(af, 1.000002f, 1e-7f);
-      const bool h1 = bn <= fmaf(bf, 1.000002f, 1e-7f);
+      const bool h0 = an <= af;
+      const bool h1 = bn <= bf;
       if (h0 && h1) {
         const bool swap = bn < an;  // near child first
         ref = swap ? ch.y : ch.x;
