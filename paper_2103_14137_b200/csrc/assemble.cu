@@ -78,6 +78,9 @@ struct AsmParams {
 // patches, so the lanes fetch mostly the same nodes (L1 broadcast) and
 // diverge little.
 constexpr int kLaneStack = 64;
+#ifndef UVD_OCT
+#define UVD_OCT 1  // dev switch: 0 = the single node array with a min/max per slab
+#endif
 constexpr uint32_t kDone = 0xffffffffu;
 
 enum { kClear = 0, kBlocked = 1, kUndecided = 2 };
@@ -104,11 +107,20 @@ __device__ __forceinline__ int lane_walk32(const AsmParams& P, float ox, float o
   // ray's octant; child refs stay inside that copy
   const uint32_t oct = (__float_as_uint(ix) >> 31) | ((__float_as_uint(iy) >> 31) << 1) |
                        ((__float_as_uint(iz) >> 31) << 2);
+#if UVD_OCT
   uint32_t ref = ref_is_leaf(P.root) ? P.root : P.root + oct * (uint32_t)P.n_nodes;
+#else
+  (void)oct;
+  uint32_t ref = P.root;
+#endif
   for (;;) {
     // ---- inner nodes until this lane holds a leaf (or is done) ----
     while (!ref_is_leaf(ref)) {
+#if UVD_OCT
       const Node* nd = P.onodes + ref;
+#else
+      const Node* nd = P.nodes + ref;
+#endif
       const float4 na = __ldg(&nd->a), nb = __ldg(&nd->b), nc = __ldg(&nd->c);
       const uint2 ch = __ldg(reinterpret_cast<const uint2*>(&nd->d));
       if (COUNT) { cnt[1] += 2; cnt[3] += 1; }
@@ -127,10 +139,17 @@ __device__ __forceinline__ int lane_walk32(const AsmParams& P, float ox, float o
       const float bx0 = fmaf(nb.x, ix, -oix), bx1 = fmaf(nb.y, ix, -oix);
       const float by0 = fmaf(nb.z, iy, -oiy), by1 = fmaf(nb.w, iy, -oiy);
       const float bz0 = fmaf(nc.z, iz, -oiz), bz1 = fmaf(nc.w, iz, -oiz);
+#if UVD_OCT
       const float an = fmaxf(fmaxf(ax0, ay0), fmaxf(az0, 0.0f));
       const float af = fminf(fminf(ax1, ay1), fminf(az1, thi));
       const float bn = fmaxf(fmaxf(bx0, by0), fmaxf(bz0, 0.0f));
       const float bf = fminf(fminf(bx1, by1), fminf(bz1, thi));
+#else
+      const float an = fmaxf(fmaxf(fminf(ax0, ax1), fminf(ay0, ay1)), fmaxf(fminf(az0, az1), 0.0f));
+      const float af = fminf(fminf(fmaxf(ax0, ax1), fmaxf(ay0, ay1)), fminf(fmaxf(az0, az1), thi));
+      const float bn = fmaxf(fmaxf(fminf(bx0, bx1), fminf(by0, by1)), fmaxf(fminf(bz0, bz1), 0.0f));
+      const float bf = fminf(fminf(fmaxf(bx0, bx1), fmaxf(by0, by1)), fminf(fmaxf(bz0, bz1), thi));
+#endif
       const bool h0 = an <= af;
       const bool h1 = bn <= bf;
       if (h0 && h1) {
