@@ -55,6 +55,8 @@ struct AsmParams {
   const int64_t* __restrict__ cols;  // device, nullptr = identity
   int64_t n_cols;
   int64_t tiles;  // ceil(rows / 32): ld/32 (dense) or words (CSC)
+  bool items32;  // n_cols * tiles < 2^32: 32-bit work-item arithmetic
+  int super_log2;  // work order: < 0 column-major, else 2^super_log2 tiles per super-tile (item_to_tile)
   int64_t words;  // ceil(N/32)
   float* __restrict__ values;  // dense [n_cols][ld] or nullptr
   int64_t ld;
@@ -182,6 +184,38 @@ __device__ __forceinline__ int lane_walk32(const AsmParams& P, float ox, float o
   }
 }
 
+// work item -> (column, tile).  P.super_log2 < 0: column-major (all SMs sweep
+// one column's tiles: rays from one or two lamps in flight); > 0: super-tiles of
+// that many tiles, every column of a super-tile before the next one (rays from
+// ~9 lamps to the same 16 K patches in flight), chosen when the BVH is several
+// times the L2: the paths near the patches are then shared across lamps.
+__device__ __forceinline__ void item_to_tile(const AsmParams& P, int64_t item, int64_t& c, int64_t& tile) {
+  if (P.super_log2 < 0) {
+    if (P.items32) {  // 32-bit division (a 64-bit one is a ~70-instruction sequence)
+      const uint32_t cc = (uint32_t)item / (uint32_t)P.tiles;
+      c = cc;
+      tile = (int64_t)((uint32_t)item - cc * (uint32_t)P.tiles);
+    } else {
+      c = item / P.tiles;
+      tile = item - c * P.tiles;
+    }
+    return;
+  }
+  // super-tiles of T = 2^super_log2 tiles; items < 2^32 (checked on the host)
+  const uint32_t sh = (uint32_t)P.super_log2, T = 1u << sh, it = (uint32_t)item;
+  const uint32_t full = (uint32_t)P.tiles >> sh, per = (uint32_t)P.n_cols << sh, base = full * per;
+  if (it < base) {
+    const uint32_t s = it / per, rem = it - s * per;
+    c = rem >> sh;
+    tile = (int64_t)((s << sh) + (rem & (T - 1u)));
+  } else {
+    const uint32_t rem = it - base, tl = (uint32_t)P.tiles - (full << sh);
+    const uint32_t cc = rem / tl;
+    c = cc;
+    tile = (int64_t)((full << sh) + rem - cc * tl);
+  }
+}
+
 template <bool COUNT>
 __global__ void __launch_bounds__(kAsmThreads, kAsmMinBlocks) k_assemble_lane(AsmParams P) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -190,7 +224,8 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmMinBlocks) k_assemble_lane(As
   for (int64_t item = (int64_t)blockIdx.x * kAsmWarps + warp; item < total;
        item += (int64_t)gridDim.x * kAsmWarps) {
     // tile fastest: concurrent warps trace adjacent patches from the same lamp
-    const int64_t c = item / P.tiles, tile = item - c * P.tiles;
+    int64_t c, tile;
+    item_to_tile(P, item, c, tile);
     const int64_t j = P.cols ? P.cols[c] : c;
     const int r = (int)(tile * 32 + lane);
     const bool valid = r < P.N;
@@ -751,6 +786,18 @@ extern "C" int uvd_irradiance_matrix(const uvd_scene* s, const float* lamp_xyz, 
   P.n_cols = n_cols;
   P.words = (s->N + 31) / 32;
   P.tiles = csc ? P.words : out->ld / 32;
+  {  // work order (item_to_tile): super-tiles of 512 tiles when the traversal data is > 2x the L2
+    int dev = 0, l2 = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
+    const double bvh_bytes = 8.0 * (double)s->n_nodes * sizeof(Node) + 48.0 * (double)s->M;
+    P.super_log2 = bvh_bytes > 2.0 * (double)l2 ? 9 : -1;
+    if (const char* e = getenv("UVD_ASM_SUPER")) P.super_log2 = atoi(e);  // dev override (log2, < 0 off)
+    P.items32 = n_cols * P.tiles < ((int64_t)1 << 32);
+    if (P.super_log2 > 30 || !P.items32 ||
+        (P.super_log2 >= 0 && (n_cols << P.super_log2) >= ((int64_t)1 << 32)))
+      P.super_log2 = -1;
+  }
   P.values = csc ? nullptr : out->values;
   P.ld = csc ? P.words * 32 : out->ld;
   P.counters = out->counters;
