@@ -80,9 +80,6 @@ struct AsmParams {
 // patches, so the lanes fetch mostly the same nodes (L1 broadcast) and
 // diverge little.
 constexpr int kLaneStack = 64;
-#ifndef UVD_OCT
-#define UVD_OCT 1  // dev switch: 0 = the single node array with a min/max per slab
-#endif
 constexpr uint32_t kDone = 0xffffffffu;
 
 enum { kClear = 0, kBlocked = 1, kUndecided = 2 };
@@ -91,7 +88,7 @@ enum { kClear = 0, kBlocked = 1, kUndecided = 2 };
 // certain hit, kClear when every triangle the segment may meet was a certain
 // miss, kUndecided when no certain hit was found but the fp32 filter could not
 // decide some triangle (the caller flags the entry for exact re-tracing).
-template <bool COUNT>
+template <bool COUNT, bool OCT>
 __device__ __forceinline__ int lane_walk32(const AsmParams& P, float ox, float oy, float oz,
                                            float dx, float dy, float dz, int owner,
                                            unsigned long long* cnt) {
@@ -109,20 +106,12 @@ __device__ __forceinline__ int lane_walk32(const AsmParams& P, float ox, float o
   // ray's octant; child refs stay inside that copy
   const uint32_t oct = (__float_as_uint(ix) >> 31) | ((__float_as_uint(iy) >> 31) << 1) |
                        ((__float_as_uint(iz) >> 31) << 2);
-#if UVD_OCT
-  uint32_t ref = ref_is_leaf(P.root) ? P.root : P.root + oct * (uint32_t)P.n_nodes;
-#else
-  (void)oct;
-  uint32_t ref = P.root;
-#endif
+  // OCT = false: the scene has no octant copies (memory cap), one array, min/max per slab
+  uint32_t ref = (!OCT || ref_is_leaf(P.root)) ? P.root : P.root + oct * (uint32_t)P.n_nodes;
   for (;;) {
     // ---- inner nodes until this lane holds a leaf (or is done) ----
     while (!ref_is_leaf(ref)) {
-#if UVD_OCT
-      const Node* nd = P.onodes + ref;
-#else
-      const Node* nd = P.nodes + ref;
-#endif
+      const Node* nd = (OCT ? P.onodes : P.nodes) + ref;
       const float4 na = __ldg(&nd->a), nb = __ldg(&nd->b), nc = __ldg(&nd->c);
       const uint2 ch = __ldg(reinterpret_cast<const uint2*>(&nd->d));
       if (COUNT) { cnt[1] += 2; cnt[3] += 1; }
@@ -141,17 +130,18 @@ __device__ __forceinline__ int lane_walk32(const AsmParams& P, float ox, float o
       const float bx0 = fmaf(nb.x, ix, -oix), bx1 = fmaf(nb.y, ix, -oix);
       const float by0 = fmaf(nb.z, iy, -oiy), by1 = fmaf(nb.w, iy, -oiy);
       const float bz0 = fmaf(nc.z, iz, -oiz), bz1 = fmaf(nc.w, iz, -oiz);
-#if UVD_OCT
-      const float an = fmaxf(fmaxf(ax0, ay0), fmaxf(az0, 0.0f));
-      const float af = fminf(fminf(ax1, ay1), fminf(az1, thi));
-      const float bn = fmaxf(fmaxf(bx0, by0), fmaxf(bz0, 0.0f));
-      const float bf = fminf(fminf(bx1, by1), fminf(bz1, thi));
-#else
-      const float an = fmaxf(fmaxf(fminf(ax0, ax1), fminf(ay0, ay1)), fmaxf(fminf(az0, az1), 0.0f));
-      const float af = fminf(fminf(fmaxf(ax0, ax1), fmaxf(ay0, ay1)), fminf(fmaxf(az0, az1), thi));
-      const float bn = fmaxf(fmaxf(fminf(bx0, bx1), fminf(by0, by1)), fmaxf(fminf(bz0, bz1), 0.0f));
-      const float bf = fminf(fminf(fmaxf(bx0, bx1), fmaxf(by0, by1)), fminf(fmaxf(bz0, bz1), thi));
-#endif
+      float an, af, bn, bf;
+      if (OCT) {
+        an = fmaxf(fmaxf(ax0, ay0), fmaxf(az0, 0.0f));
+        af = fminf(fminf(ax1, ay1), fminf(az1, thi));
+        bn = fmaxf(fmaxf(bx0, by0), fmaxf(bz0, 0.0f));
+        bf = fminf(fminf(bx1, by1), fminf(bz1, thi));
+      } else {
+        an = fmaxf(fmaxf(fminf(ax0, ax1), fminf(ay0, ay1)), fmaxf(fminf(az0, az1), 0.0f));
+        af = fminf(fminf(fmaxf(ax0, ax1), fmaxf(ay0, ay1)), fminf(fmaxf(az0, az1), thi));
+        bn = fmaxf(fmaxf(fminf(bx0, bx1), fminf(by0, by1)), fmaxf(fminf(bz0, bz1), 0.0f));
+        bf = fminf(fminf(fmaxf(bx0, bx1), fmaxf(by0, by1)), fminf(fmaxf(bz0, bz1), thi));
+      }
       const bool h0 = an <= af;
       const bool h1 = bn <= bf;
       if (h0 && h1) {
@@ -216,7 +206,7 @@ __device__ __forceinline__ void item_to_tile(const AsmParams& P, int64_t item, i
   }
 }
 
-template <bool COUNT>
+template <bool COUNT, bool OCT>
 __global__ void __launch_bounds__(kAsmThreads, kAsmMinBlocks) k_assemble_lane(AsmParams P) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   unsigned long long cnt[6] = {0, 0, 0, 0, 0, 0};  // per-lane tallies (COUNT only)
@@ -256,7 +246,7 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmMinBlocks) k_assemble_lane(As
       if (front) {
         if (COUNT) cnt[0] += 1;
         // a5: occlusion of the open segment, t in (1e-4/d, 1 - 1e-4/d), fp32 decisions
-        const int res = lane_walk32<COUNT>(P, ox, oy, oz, dx, dy, dz, r, cnt);
+        const int res = lane_walk32<COUNT, OCT>(P, ox, oy, oz, dx, dy, dz, r, cnt);
         vis = res == kClear;
         pend |= res == kUndecided;
         if (vis) acc += w;
@@ -341,7 +331,7 @@ __device__ __forceinline__ DTri patch_tri(const AsmParams& P, int r, int k) {
 #endif
 constexpr int kAreaThreads = UVD_AREA_THREADS;
 
-template <bool COUNT>
+template <bool COUNT, bool OCT>
 __global__ void __launch_bounds__(kAreaThreads, UVD_AREA_MINB) k_assemble_area(AsmParams P) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kAreaThreads / 32;
   unsigned long long cnt[6] = {0, 0, 0, 0, 0, 0};
@@ -381,7 +371,7 @@ __global__ void __launch_bounds__(kAreaThreads, UVD_AREA_MINB) k_assemble_area(A
                 continue;
               }
               if (COUNT) cnt[0] += 1;
-              const int res = lane_walk32<COUNT>(P, ox, oy, oz, dx, dy, dz, r, cnt);
+              const int res = lane_walk32<COUNT, OCT>(P, ox, oy, oz, dx, dy, dz, r, cnt);
               if (COUNT && res == kBlocked) cnt[5] += 1;
               pend |= res == kUndecided;
               if (res == kClear) {
@@ -713,7 +703,7 @@ static int grid_size_assemble() {
   int dev = 0, sms = 0, per = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_assemble_lane<false>, kAsmThreads, 0);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_assemble_lane<false, true>, kAsmThreads, 0);
   return std::max(1, sms * std::max(per, 1));
 }
 
@@ -827,7 +817,7 @@ extern "C" int uvd_irradiance_matrix(const uvd_scene* s, const float* lamp_xyz, 
     int dev = 0, sms = 0, per = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_assemble_lane<true>, kAsmThreads, 0);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_assemble_lane<true, true>, kAsmThreads, 0);
     grid_c = std::max(1, sms * std::max(per, 1));
   }
   if (area_model) {
@@ -836,15 +826,23 @@ extern "C" int uvd_irradiance_matrix(const uvd_scene* s, const float* lamp_xyz, 
       int dev = 0, sms = 0, per = 0;
       cudaGetDevice(&dev);
       cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_assemble_area<false>, kAreaThreads, 0);
+      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_assemble_area<false, true>, kAreaThreads, 0);
       grid_a = std::max(1, sms * std::max(per, 1));
     }
-    if (P.counters) k_assemble_area<true><<<grid_a, kAreaThreads, 0, st>>>(P);
-    else k_assemble_area<false><<<grid_a, kAreaThreads, 0, st>>>(P);
+    // octant node copies when the scene has them (bvh.cu caps their memory)
+    if (P.counters) {
+      if (P.onodes) k_assemble_area<true, true><<<grid_a, kAreaThreads, 0, st>>>(P);
+      else k_assemble_area<true, false><<<grid_a, kAreaThreads, 0, st>>>(P);
+    } else {
+      if (P.onodes) k_assemble_area<false, true><<<grid_a, kAreaThreads, 0, st>>>(P);
+      else k_assemble_area<false, false><<<grid_a, kAreaThreads, 0, st>>>(P);
+    }
   } else if (P.counters) {
-    k_assemble_lane<true><<<grid_c, kAsmThreads, 0, st>>>(P);
+    if (P.onodes) k_assemble_lane<true, true><<<grid_c, kAsmThreads, 0, st>>>(P);
+    else k_assemble_lane<true, false><<<grid_c, kAsmThreads, 0, st>>>(P);
   } else {
-    k_assemble_lane<false><<<grid, kAsmThreads, 0, st>>>(P);
+    if (P.onodes) k_assemble_lane<false, true><<<grid, kAsmThreads, 0, st>>>(P);
+    else k_assemble_lane<false, false><<<grid, kAsmThreads, 0, st>>>(P);
   }
   note_launch();
   {  // exact fp64 re-trace of the (rare) entries the fp32 pass left undecided

@@ -1314,21 +1314,22 @@ int build_bvh(uvd_scene* s, float4* tri_in, uint32_t** order_out, cudaStream_t s
                     (void*)ibox, (void*)arrive})
       al.put(p);
   }
-  {
+  {  // octant copies of the nodes (k_octant_nodes) unless they would take > 1/16 of the
+     // device memory or UVD_OCT=0: the traversal then reads the one array (min/max per slab)
     const int64_t nn = std::max<int64_t>(M - 1, 1);
-    if (8 * nn >= (int64_t)1 << 31) {
-      set_error("scene: too many triangles (%lld) for 31-bit node refs", (long long)M);
-      return UVD_ERR_INVALID;
-    }
     if (s->onodes) al.put(s->onodes);
+    s->onodes = nullptr;
     s->n_nodes = nn;
-    s->onodes = (Node*)al.get(8 * nn * sizeof(Node));
-    if (!s->onodes) {
-      set_error("scene: out of device memory (octant nodes)");
-      return UVD_ERR_NOMEM;
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    const char* e = getenv("UVD_OCT");
+    const bool want = !(e && atoi(e) == 0) && 8 * nn < ((int64_t)1 << 31) &&
+                      (double)(8 * nn * (int64_t)sizeof(Node)) <= (double)total_b / 16.0;
+    if (want) s->onodes = (Node*)al.get(8 * nn * sizeof(Node));  // nullptr (no memory): one array
+    if (s->onodes) {
+      k_octant_nodes<<<grid_for(8 * nn, 256), 256, 0, st>>>(s->nodes, nn, s->onodes);
+      note_launch();
     }
-    k_octant_nodes<<<grid_for(8 * nn, 256), 256, 0, st>>>(s->nodes, nn, s->onodes);
-    note_launch();
   }
   UVD_CUDA_TRY(cudaGetLastError());
   al.put(keys);

@@ -38,3 +38,26 @@ def test_work_order_bit_identical(uvd, super_log2, monkeypatch):
     assert torch.equal(ref["A"], got["A"])
     assert torch.equal(ref["vis_bits"], got["vis_bits"])
     assert float(ref["A"].abs().sum()) > 0
+
+
+def test_octant_copies_off_bit_identical(uvd, monkeypatch):
+    """Scenes whose octant node copies would exceed their memory cap (or with
+    UVD_OCT=0) traverse the one node array with a min/max per slab: the same
+    boxes, hence the same decisions, bit for bit, for both models."""
+    w = ward.ward(seed=8, n_bays=1, e=0.25)
+    lam_opts = configs.vopts(configs.FLOAT3D, 0.6, 0.05)
+    monkeypatch.delenv("UVD_OCT", raising=False)
+    sc = uvd.Scene(w)
+    lam, _ = sc.vantage(lam_opts)
+    cols = list(range(0, lam.shape[0], 2))
+    ref = sc.irradiance(lam, cols=cols, vis_bits=True)
+    ref_area = sc.irradiance(lam, cols=cols[:6], area_subdiv=1)
+    monkeypatch.setenv("UVD_OCT", "0")
+    sc0 = uvd.Scene(w)
+    got = sc0.irradiance(lam, cols=cols, vis_bits=True)
+    got_area = sc0.irradiance(lam, cols=cols[:6], area_subdiv=1)
+    sc.sync_status()
+    sc0.sync_status()
+    assert torch.equal(ref["A"], got["A"])
+    assert torch.equal(ref["vis_bits"], got["vis_bits"])
+    assert torch.equal(ref_area["A"], got_area["A"])
