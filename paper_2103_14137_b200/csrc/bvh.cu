@@ -736,8 +736,8 @@ __global__ void __launch_bounds__(kSahThreads) k_sah_split(const float4* __restr
       ch[a] = fmaxf(ch[a], __shfl_xor_sync(0xffffffffu, ch[a], o));
     }
   // bins cleared; centre bounds reduced across warps as ordered ints
-  if (tid < 3 * kSahBins) {
-    const int a = tid / kSahBins, b = tid % kSahBins;
+  for (int q = tid; q < 3 * kSahBins; q += kSahThreads) {
+    const int a = q / kSahBins, b = q % kSahBins;
     s_cnt[a][b] = 0;
     for (int k = 0; k < 3; ++k) { s_lo[a][b][k] = 0x7fffffff; s_hi[a][b][k] = (int)0x80000000; }
   }
@@ -873,6 +873,7 @@ struct SahChunks {
 };
 
 constexpr int kHugeThreads = 1024;
+static_assert(3 * kSahBins <= kHugeThreads, "the huge-node kernels clear / merge one bin per thread");
 
 __global__ void __launch_bounds__(kHugeThreads) k_sah_huge_bounds(const float4* __restrict__ tri,
                                                                    const int32_t* __restrict__ perm, SahChunks C) {
