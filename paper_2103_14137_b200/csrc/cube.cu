@@ -42,6 +42,8 @@ __global__ void k_cube_emission(int R, double* __restrict__ E) {
 struct CubeParams {
   const float4* __restrict__ tri;
   const Node* __restrict__ nodes;
+  const Node* __restrict__ onodes;  // octant copies (nullptr: not built for this scene)
+  int64_t n_nodes;
   uint32_t root;
   const float* __restrict__ lamps;
   int L;
@@ -61,6 +63,7 @@ constexpr int kCubeThreads = 256;
 
 // closest front-or-back hit along O + t D, t > 0; returns the triangle position
 // in leaf order (or -1), its facing, and its owner patch
+template <bool OCT>
 __device__ __forceinline__ int64_t cube_closest(const CubeParams& P, float ox, float oy, float oz, double dxd,
                                                 double dyd, double dzd, bool* front, int* owner) {
   const float dx = (float)dxd, dy = (float)dyd, dz = (float)dzd;
@@ -77,7 +80,10 @@ __device__ __forceinline__ int64_t cube_closest(const CubeParams& P, float ox, f
   float tmax = 3.0e38f;
   uint32_t stk[kCubeStack];
   int sp = 0;
-  uint32_t ref = P.root;
+  // the octant copy of the nodes for this ray (slabs stored entry, exit), as in k_assemble_lane
+  const uint32_t oct = (__float_as_uint(ix) >> 31) | ((__float_as_uint(iy) >> 31) << 1) |
+                       ((__float_as_uint(iz) >> 31) << 2);
+  uint32_t ref = (!OCT || ref_is_leaf(P.root)) ? P.root : P.root + oct * (uint32_t)P.n_nodes;
   for (;;) {
     if (ref_is_leaf(ref)) {
       const uint32_t st = ref_start(ref), nt = ref_count(ref);
@@ -115,7 +121,7 @@ __device__ __forceinline__ int64_t cube_closest(const CubeParams& P, float ox, f
       ref = stk[--sp];
       continue;
     }
-    const Node* nd = P.nodes + ref;
+    const Node* nd = (OCT ? P.onodes : P.nodes) + ref;
     const float4 na = __ldg(&nd->a), nb = __ldg(&nd->b), nc = __ldg(&nd->c);
     const uint2 ch = __ldg(reinterpret_cast<const uint2*>(&nd->d));
     const float ax0 = fmaf(na.x, ix, -oix), ax1 = fmaf(na.y, ix, -oix);
@@ -124,12 +130,24 @@ __device__ __forceinline__ int64_t cube_closest(const CubeParams& P, float ox, f
     const float bx0 = fmaf(nb.x, ix, -oix), bx1 = fmaf(nb.y, ix, -oix);
     const float by0 = fmaf(nb.z, iy, -oiy), by1 = fmaf(nb.w, iy, -oiy);
     const float bz0 = fmaf(nc.z, iz, -oiz), bz1 = fmaf(nc.w, iz, -oiz);
-    const float an = fmaxf(fmaxf(fminf(ax0, ax1), fminf(ay0, ay1)), fmaxf(fminf(az0, az1), 0.0f));
-    const float af = fminf(fminf(fmaxf(ax0, ax1), fmaxf(ay0, ay1)), fminf(fmaxf(az0, az1), tmax));
-    const float bn = fmaxf(fmaxf(fminf(bx0, bx1), fminf(by0, by1)), fmaxf(fminf(bz0, bz1), 0.0f));
-    const float bf = fminf(fminf(fmaxf(bx0, bx1), fmaxf(by0, by1)), fminf(fmaxf(bz0, bz1), tmax));
-    const bool h0 = an <= fmaf(af, 1.000002f, 1e-7f);
-    const bool h1 = bn <= fmaf(bf, 1.000002f, 1e-7f);
+    // no widening per node: fl(1/d), fl(d) and the FFMA's rounding move a plane by
+    // <= 2^-22 |b - o| + 2^-24 |o| <= 1e-5 m for |coords| <= 20 m, inside the box
+    // padding (k_assemble_lane's argument, plus the fp32 rounding of the direction);
+    // tmax keeps its widening above ru(best) (ties go to the lower input index)
+    float an, af, bn, bf;
+    if (OCT) {
+      an = fmaxf(fmaxf(ax0, ay0), fmaxf(az0, 0.0f));
+      af = fminf(fminf(ax1, ay1), fminf(az1, tmax));
+      bn = fmaxf(fmaxf(bx0, by0), fmaxf(bz0, 0.0f));
+      bf = fminf(fminf(bx1, by1), fminf(bz1, tmax));
+    } else {
+      an = fmaxf(fmaxf(fminf(ax0, ax1), fminf(ay0, ay1)), fmaxf(fminf(az0, az1), 0.0f));
+      af = fminf(fminf(fmaxf(ax0, ax1), fmaxf(ay0, ay1)), fminf(fmaxf(az0, az1), tmax));
+      bn = fmaxf(fmaxf(fminf(bx0, bx1), fminf(by0, by1)), fmaxf(fminf(bz0, bz1), 0.0f));
+      bf = fminf(fminf(fmaxf(bx0, bx1), fmaxf(by0, by1)), fminf(fmaxf(bz0, bz1), tmax));
+    }
+    const bool h0 = an <= af;
+    const bool h1 = bn <= bf;
     if (h0 && h1) {
       const bool swap = bn < an;  // near child first: the closest hit shrinks tmax early
       ref = swap ? ch.y : ch.x;
@@ -150,6 +168,7 @@ __device__ __forceinline__ int64_t cube_closest(const CubeParams& P, float ox, f
 #ifndef UVD_CUBE_MINB
 #define UVD_CUBE_MINB 4
 #endif
+template <bool OCT>
 __global__ void __launch_bounds__(kCubeThreads, UVD_CUBE_MINB) k_cube_trace(CubeParams P) {
   const int lane = threadIdx.x & 31;
   const int64_t per_col = (int64_t)P.L * 6 * P.R * P.R;
@@ -182,7 +201,7 @@ __global__ void __launch_bounds__(kCubeThreads, UVD_CUBE_MINB) k_cube_trace(Cube
       }
       bool front = false;
       int owner = -1;
-      const int64_t k = cube_closest(P, pl[0], pl[1], pl[2], dx, dy, dz, &front, &owner);
+      const int64_t k = cube_closest<OCT>(P, pl[0], pl[1], pl[2], dx, dy, dz, &front, &owner);
       if (P.hits) P.hits[c * per_col + (q - cl * per_col)] = k < 0 ? -1 : (front ? __float_as_int(P.tri[3 * k + 1].w) : -2);
       if (k >= 0 && front) {
         key = owner;
@@ -252,6 +271,8 @@ extern "C" int uvd_cubemap_matrix(const uvd_scene* s, const float* lamp_xyz, int
   CubeParams P;
   P.tri = s->tri;
   P.nodes = s->nodes;
+  P.onodes = s->onodes;
+  P.n_nodes = s->n_nodes;
   P.root = s->root;
   P.lamps = lamp_xyz;
   P.L = lamp->samples_per_config;
@@ -270,7 +291,8 @@ extern "C" int uvd_cubemap_matrix(const uvd_scene* s, const float* lamp_xyz, int
     UVD_CUDA_TRY(cudaMemsetAsync(F, 0, (size_t)nc * s->N * sizeof(double), st));
     const int64_t rays = nc * P.L * 6 * (int64_t)R * R;
     const unsigned g = (unsigned)std::min<int64_t>((rays + kCubeThreads - 1) / kCubeThreads, (int64_t)sms * 8);
-    k_cube_trace<<<g, kCubeThreads, 0, st>>>(P);
+    if (P.onodes) k_cube_trace<true><<<g, kCubeThreads, 0, st>>>(P);
+    else k_cube_trace<false><<<g, kCubeThreads, 0, st>>>(P);
     k_cube_finish<<<(unsigned)std::min<int64_t>((nc * out->ld + 255) / 256, (int64_t)sms * 16), 256, 0, st>>>(
         F, s->area, nc, s->N, out->values, out->ld, c0);
     note_launch(2);
