@@ -677,9 +677,14 @@ __device__ __forceinline__ int f2o(float f) {  // order-preserving float -> int
 }
 __device__ __forceinline__ float o2f(int i) { return __int_as_float(i >= 0 ? i : i ^ 0x7fffffff); }
 
+// half the box surface; explicit roundings (no contraction) so every sweep of
+// the builder computes the same cost bits for the same bins
 __device__ __forceinline__ float sah_area(float lx, float ly, float lz, float hx, float hy, float hz) {
-  const float dx = hx - lx, dy = hy - ly, dz = hz - lz;
-  return dx * dy + dy * dz + dz * dx;
+  const float dx = __fsub_rn(hx, lx), dy = __fsub_rn(hy, ly), dz = __fsub_rn(hz, lz);
+  return __fadd_rn(__fadd_rn(__fmul_rn(dx, dy), __fmul_rn(dy, dz)), __fmul_rn(dz, dx));
+}
+__device__ __forceinline__ float sah_cost(float area_l, int n_l, float area_r, int n_r) {
+  return __fadd_rn(__fmul_rn(area_l, (float)n_l), __fmul_rn(area_r, (float)n_r));
 }
 
 // children of a split node: a single triangle is a leaf reference, larger
@@ -720,6 +725,9 @@ __global__ void __launch_bounds__(kSahThreads) k_sah_split(const float4* __restr
   __shared__ int s_cb[6];      // centre bounds (ordered ints)
   __shared__ int s_split[3];  // axis, bin, n_left
   __shared__ int s_scan[kSahThreads / 32];
+  __shared__ float s_cost[3];
+  __shared__ int s_bin[3], s_nl[3];
+  static_assert(kSahBins == 32 && kSahThreads >= 96, "the sweep maps one warp per axis, one lane per bin");
   const int node = list[blockIdx.x];
   const int first = rf[node], last = rl[node], n = last - first + 1;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -774,40 +782,66 @@ __global__ void __launch_bounds__(kSahThreads) k_sah_split(const float4* __restr
     }
   }
   __syncthreads();
-  // 3. sweep (thread 0): least SAH cost split among the 3 x (B-1) bin planes
-  if (tid == 0) {
-    float best = INFINITY;
-    int ba = -1, bb = -1, bnl = 0;
-    if (n > 2) {
-      for (int a = 0; a < 3; ++a) {
-        if (cscale[a] == 0.f) continue;
-        float rarea[kSahBins];
-        int rcnt[kSahBins];
-        float lx = INFINITY, ly = INFINITY, lz = INFINITY, hx = -INFINITY, hy = -INFINITY, hz = -INFINITY;
-        int c = 0;
-        for (int b = kSahBins - 1; b >= 0; --b) {
-          if (s_cnt[a][b]) {
-            lx = fminf(lx, o2f(s_lo[a][b][0])); ly = fminf(ly, o2f(s_lo[a][b][1])); lz = fminf(lz, o2f(s_lo[a][b][2]));
-            hx = fmaxf(hx, o2f(s_hi[a][b][0])); hy = fmaxf(hy, o2f(s_hi[a][b][1])); hz = fmaxf(hz, o2f(s_hi[a][b][2]));
-            c += s_cnt[a][b];
-          }
-          rarea[b] = c ? sah_area(lx, ly, lz, hx, hy, hz) : 0.f;
-          rcnt[b] = c;
-        }
-        lx = ly = lz = INFINITY; hx = hy = hz = -INFINITY;
-        c = 0;
-        for (int b = 0; b < kSahBins - 1; ++b) {
-          if (s_cnt[a][b]) {
-            lx = fminf(lx, o2f(s_lo[a][b][0])); ly = fminf(ly, o2f(s_lo[a][b][1])); lz = fminf(lz, o2f(s_lo[a][b][2]));
-            hx = fmaxf(hx, o2f(s_hi[a][b][0])); hy = fmaxf(hy, o2f(s_hi[a][b][1])); hz = fmaxf(hz, o2f(s_hi[a][b][2]));
-            c += s_cnt[a][b];
-          }
-          if (c == 0 || rcnt[b + 1] == 0) continue;
-          const float cost = sah_area(lx, ly, lz, hx, hy, hz) * c + rarea[b + 1] * rcnt[b + 1];
-          if (cost < best) { best = cost; ba = a; bb = b; bnl = c; }
-        }
+  // 3. sweep: least SAH cost split among the 3 x (B-1) bin planes; warp a scans
+  // axis a (lane = bin: prefix / suffix boxes by shuffles), ties to the lowest
+  // (axis, bin) as a sequential sweep would take them
+  if (wid < 3) {
+    const int ax = wid, b = lane;
+    const bool on = n > 2 && cscale[ax] != 0.f;
+    int c = 0;
+    float l0 = INFINITY, l1 = INFINITY, l2 = INFINITY, h0 = -INFINITY, h1 = -INFINITY, h2 = -INFINITY;
+    if (on && s_cnt[ax][b]) {
+      c = s_cnt[ax][b];
+      l0 = o2f(s_lo[ax][b][0]); l1 = o2f(s_lo[ax][b][1]); l2 = o2f(s_lo[ax][b][2]);
+      h0 = o2f(s_hi[ax][b][0]); h1 = o2f(s_hi[ax][b][1]); h2 = o2f(s_hi[ax][b][2]);
+    }
+    float pl0 = l0, pl1 = l1, pl2 = l2, ph0 = h0, ph1 = h1, ph2 = h2;  // bins <= b
+    float ql0 = l0, ql1 = l1, ql2 = l2, qh0 = h0, qh1 = h1, qh2 = h2;  // bins >= b
+    int pc = c, qc = c;
+    for (int o = 1; o < 32; o <<= 1) {
+      const float u0 = __shfl_up_sync(0xffffffffu, pl0, o), u1 = __shfl_up_sync(0xffffffffu, pl1, o);
+      const float u2 = __shfl_up_sync(0xffffffffu, pl2, o), v0 = __shfl_up_sync(0xffffffffu, ph0, o);
+      const float v1 = __shfl_up_sync(0xffffffffu, ph1, o), v2 = __shfl_up_sync(0xffffffffu, ph2, o);
+      const int uc = __shfl_up_sync(0xffffffffu, pc, o);
+      if (lane >= o) {
+        pl0 = fminf(pl0, u0); pl1 = fminf(pl1, u1); pl2 = fminf(pl2, u2);
+        ph0 = fmaxf(ph0, v0); ph1 = fmaxf(ph1, v1); ph2 = fmaxf(ph2, v2);
+        pc += uc;
+      }
+      const float w0 = __shfl_down_sync(0xffffffffu, ql0, o), w1 = __shfl_down_sync(0xffffffffu, ql1, o);
+      const float w2 = __shfl_down_sync(0xffffffffu, ql2, o), x0 = __shfl_down_sync(0xffffffffu, qh0, o);
+      const float x1 = __shfl_down_sync(0xffffffffu, qh1, o), x2 = __shfl_down_sync(0xffffffffu, qh2, o);
+      const int wc = __shfl_down_sync(0xffffffffu, qc, o);
+      if (lane + o < 32) {
+        ql0 = fminf(ql0, w0); ql1 = fminf(ql1, w1); ql2 = fminf(ql2, w2);
+        qh0 = fmaxf(qh0, x0); qh1 = fmaxf(qh1, x1); qh2 = fmaxf(qh2, x2);
+        qc += wc;
       }
     }
+    // the right side of the plane after bin b is the suffix from bin b + 1
+    const float r0 = __shfl_down_sync(0xffffffffu, ql0, 1), r1 = __shfl_down_sync(0xffffffffu, ql1, 1);
+    const float r2 = __shfl_down_sync(0xffffffffu, ql2, 1), s0 = __shfl_down_sync(0xffffffffu, qh0, 1);
+    const float s1 = __shfl_down_sync(0xffffffffu, qh1, 1), s2 = __shfl_down_sync(0xffffffffu, qh2, 1);
+    const int rc = __shfl_down_sync(0xffffffffu, qc, 1);
+    float cost = INFINITY;
+    if (on && b < kSahBins - 1 && pc > 0 && rc > 0)
+      cost = sah_cost(sah_area(pl0, pl1, pl2, ph0, ph1, ph2), pc, sah_area(r0, r1, r2, s0, s1, s2), rc);
+    // warp argmin (cost, bin)
+    float bc = cost;
+    int bbin = cost < INFINITY ? b : kSahBins, bnl = pc;
+    for (int o = 16; o > 0; o >>= 1) {
+      const float oc = __shfl_xor_sync(0xffffffffu, bc, o);
+      const int ob = __shfl_xor_sync(0xffffffffu, bbin, o), onl = __shfl_xor_sync(0xffffffffu, bnl, o);
+      if (oc < bc || (oc == bc && ob < bbin)) { bc = oc; bbin = ob; bnl = onl; }
+    }
+    if (lane == 0) { s_cost[ax] = bc; s_bin[ax] = bbin; s_nl[ax] = bnl; }
+  }
+  __syncthreads();
+  if (tid == 0) {
+    int ba = -1, bb = -1, bnl = 0;
+    float best = INFINITY;
+    for (int ax = 0; ax < 3; ++ax)
+      if (s_bin[ax] < kSahBins && s_cost[ax] < best) { best = s_cost[ax]; ba = ax; bb = s_bin[ax]; bnl = s_nl[ax]; }
     s_split[0] = ba;  // -1: median split by position
     s_split[1] = bb;
     s_split[2] = ba < 0 ? n / 2 : bnl;
@@ -980,7 +1014,7 @@ __global__ void k_sah_huge_decide(const int32_t* __restrict__ list, int n_huge, 
         c += cnt[b];
       }
       if (c == 0 || rcnt[b + 1] == 0) continue;
-      const float cost = sah_area(lx, ly, lz, hx, hy, hz) * c + rarea[b + 1] * rcnt[b + 1];
+      const float cost = sah_cost(sah_area(lx, ly, lz, hx, hy, hz), c, rarea[b + 1], rcnt[b + 1]);
       if (cost < best) { best = cost; ba = a; bb = b; bnl = c; }
     }
   }
