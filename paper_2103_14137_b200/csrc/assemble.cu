@@ -851,7 +851,8 @@ extern "C" int uvd_irradiance_matrix(const uvd_scene* s, const float* lamp_xyz, 
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t nwords = n_cols * P.words;
     // room for 2^24 entries (128 MB): C5 flags ~6.6 M; beyond it the collect kernel re-traces inline
-    const int64_t cap = std::min<int64_t>(nwords * 32, (int64_t)1 << 24);
+    int64_t cap = std::min<int64_t>(nwords * 32, (int64_t)1 << 24);
+    if (const char* e = getenv("UVD_FIXUP_CAP")) cap = std::max<int64_t>(1, std::min<int64_t>(cap, atoll(e)));  // tests
     uint64_t* list = (uint64_t*)al.get((size_t)cap * sizeof(uint64_t) + 256);
     if (!list) { set_error("uvd_irradiance_matrix: out of device memory"); return UVD_ERR_NOMEM; }
     unsigned long long* count = (unsigned long long*)((char*)list + (size_t)cap * sizeof(uint64_t));

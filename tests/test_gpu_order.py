@@ -61,3 +61,22 @@ def test_octant_copies_off_bit_identical(uvd, monkeypatch):
     assert torch.equal(ref["A"], got["A"])
     assert torch.equal(ref["vis_bits"], got["vis_bits"])
     assert torch.equal(ref_area["A"], got_area["A"])
+
+
+@pytest.mark.parametrize("cap", ["1", "5"])
+def test_fixup_list_overflow_bit_identical(uvd, cap, monkeypatch):
+    """Entries the fp32 pass leaves undecided go to a list re-traced by
+    k_fixup_run; beyond the list's capacity the collect kernel re-traces them
+    itself.  Both routes give the same exact decisions (UVD_FIXUP_CAP shrinks
+    the list to force the second)."""
+    w = ward.ward(seed=9, n_bays=1, e=0.25)
+    sc = uvd.Scene(w)
+    lam, _ = sc.vantage(configs.vopts(configs.FLOAT3D, 0.5, 0.05))
+    monkeypatch.delenv("UVD_FIXUP_CAP", raising=False)
+    ref = sc.irradiance(lam, vis_bits=True, counters=True)
+    assert int(ref["counters"][4]) > 5, "the scene must flag some entries for the exact re-trace"
+    monkeypatch.setenv("UVD_FIXUP_CAP", cap)
+    got = sc.irradiance(lam, vis_bits=True)
+    sc.sync_status()
+    assert torch.equal(ref["A"], got["A"])
+    assert torch.equal(ref["vis_bits"], got["vis_bits"])
