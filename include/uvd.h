@@ -27,6 +27,20 @@
  * error, outputs are unspecified.  In-kernel domain errors (lamp–centroid
  * distance < 1e-9 m) set a per-scene device flag reported by
  * uvd_sync_status.
+ *
+ * Environment (read per call; defaults are the measured best):
+ *   UVD_BVH=sah|ploc|karras   BVH builder of uvd_scene_create (default sah)
+ *   UVD_SAH_HUGE=n, UVD_SAH_CHUNK=n   nodes above n triangles split over CTAs
+ *                             in chunks (default 65536 / 32768; tests only)
+ *   UVD_OCT=0                 no octant node copies (default: built when they
+ *                             take <= 1/16 of device memory)
+ *   UVD_ASM_SUPER=k           assembly work order: super-tiles of 2^k tiles,
+ *                             < 0 column-major (default: 9 when the traversal
+ *                             data exceeds 2x the L2, else column-major)
+ *   UVD_FIXUP_CAP=n           capacity of the exact re-trace list (tests only)
+ *   UVD_LP_*                  PDHG tuning knobs of uvd_lp_solve (lp.cu)
+ * None changes a result: every setting gives bit-identical A and visibility
+ * bits (tests/test_gpu_order.py, tests/test_gpu_bvh.py).
  */
 #ifndef UVD_H_
 #define UVD_H_
