@@ -38,9 +38,10 @@
  *                             < 0 column-major (default: 9 when the traversal
  *                             data exceeds 2x the L2, else column-major)
  *   UVD_FIXUP_CAP=n           capacity of the exact re-trace list (tests only)
- *   UVD_LP_*                  PDHG tuning knobs of uvd_lp_solve (lp.cu)
- * None changes a result: every setting gives bit-identical A and visibility
- * bits (tests/test_gpu_order.py, tests/test_gpu_bvh.py).
+ *   UVD_LP_*                  PDHG tuning knobs of uvd_lp_solve (lp.cu; they
+ *                             change the iterates, not the optimum)
+ * The others never change a result: every setting gives bit-identical A and
+ * visibility bits (tests/test_gpu_order.py, tests/test_gpu_bvh.py).
  */
 #ifndef UVD_H_
 #define UVD_H_
