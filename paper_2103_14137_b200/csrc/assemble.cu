@@ -605,13 +605,10 @@ __device__ void fixup_entry(const AsmParams& P, int64_t c, int r) {
   if (P.values) P.values[c * P.ld + r] = (float)(P.area_m >= 0 ? acc * P.scale / P.area[r] : acc * P.scale);
 }
 
-// out-of-line: keeps the collect loop's registers free of the re-trace
-__device__ __noinline__ void fixup_entry_overflow(const AsmParams& P, int64_t c, int r) { fixup_entry(P, c, r); }
-
 // Compaction of the pending bits into (column, row) entries: each thread owns 4
 // consecutive words, blocks with no pending bit (almost all) leave after one
 // __syncthreads_or; otherwise one atomic per block reserves the slots.
-constexpr int kCollectThreads = 256, kCollectWords = 4;
+constexpr int kCollectThreads = 256, kCollectWords = 16;  // 64 B per thread: 4 x 16-B loads in flight
 __global__ void __launch_bounds__(kCollectThreads) k_fixup_collect(AsmParams P, uint64_t* __restrict__ list,
                                                                     int64_t cap,
                                                                     unsigned long long* __restrict__ count) {
@@ -624,11 +621,19 @@ __global__ void __launch_bounds__(kCollectThreads) k_fixup_collect(AsmParams P, 
     const int64_t w = w0 + (int64_t)threadIdx.x * kCollectWords;
     uint32_t bits[kCollectWords];
     int n = 0;
+    if (w + kCollectWords <= nwords) {  // the buffer and w are 64-B aligned
+      const uint4* p4 = reinterpret_cast<const uint4*>(P.pending + w);
 #pragma unroll
-    for (int k = 0; k < kCollectWords; ++k) {
-      bits[k] = w + k < nwords ? P.pending[w + k] : 0u;
-      n += __popc(bits[k]);
+      for (int k = 0; k < kCollectWords / 4; ++k) {
+        const uint4 v = __ldcs(p4 + k);
+        bits[4 * k] = v.x; bits[4 * k + 1] = v.y; bits[4 * k + 2] = v.z; bits[4 * k + 3] = v.w;
+      }
+    } else {
+#pragma unroll
+      for (int k = 0; k < kCollectWords; ++k) bits[k] = w + k < nwords ? P.pending[w + k] : 0u;
     }
+#pragma unroll
+    for (int k = 0; k < kCollectWords; ++k) n += __popc(bits[k]);
     if (!__syncthreads_or(n)) continue;
     int incl = n;  // block exclusive scan of the counts
     for (int o = 1; o < 32; o <<= 1) {
@@ -653,13 +658,31 @@ __global__ void __launch_bounds__(kCollectThreads) k_fixup_collect(AsmParams P, 
       uint32_t b = bits[k];
       if (!b) continue;
       const int64_t wk = w + k, c = wk / P.words, word = wk - c * P.words;
+      uint32_t keep = 0;  // entries beyond the list's capacity stay pending for k_fixup_overflow
       while (b) {
-        const int r = (int)(word * 32 + __ffs(b) - 1);
+        const int bit = __ffs(b) - 1;
         b &= b - 1;
-        if (slot < cap) list[slot] = ((uint64_t)c << 32) | (uint32_t)r;
-        else fixup_entry_overflow(P, c, r);  // list full: re-trace here
+        if (slot < cap) list[slot] = ((uint64_t)c << 32) | (uint32_t)(word * 32 + bit);
+        else keep |= 1u << bit;
         ++slot;
       }
+      P.pending[wk] = keep;
+    }
+  }
+}
+
+// Entries the list had no room for (count > cap): re-traced here, found by
+// their pending bits (k_fixup_collect cleared the listed ones).
+__global__ void k_fixup_overflow(AsmParams P, int64_t cap, const unsigned long long* __restrict__ count) {
+  if ((int64_t)*count <= cap) return;
+  const int64_t nwords = P.n_cols * P.words;
+  for (int64_t w = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; w < nwords; w += (int64_t)gridDim.x * blockDim.x) {
+    uint32_t b = P.pending[w];
+    const int64_t c = w / P.words, word = w - c * P.words;
+    while (b) {
+      const int bit = __ffs(b) - 1;
+      b &= b - 1;
+      fixup_entry(P, c, (int)(word * 32 + bit));
     }
   }
 }
@@ -804,6 +827,11 @@ extern "C" int uvd_irradiance_matrix(const uvd_scene* s, const float* lamp_xyz, 
   int64_t* colcnt = nullptr;
   if (cols) dcols = (int64_t*)al.get(n_cols * sizeof(int64_t));
   P.pending = (uint32_t*)al.get((size_t)n_cols * P.words * sizeof(uint32_t));
+  if (P.pending && ((uintptr_t)P.pending & 15u)) {  // k_fixup_collect reads it with 16-B loads
+    set_error("uvd_irradiance_matrix: allocator returned a buffer not 16-B aligned");
+    al.put(P.pending);
+    return UVD_ERR_INVALID;
+  }
   if (csc && !out->vis_bits)
     vis_scratch = (uint32_t*)al.get((size_t)n_cols * P.L * P.words * sizeof(uint32_t));
   if (csc) colcnt = (int64_t*)al.get(n_cols * sizeof(int64_t));
@@ -853,7 +881,7 @@ extern "C" int uvd_irradiance_matrix(const uvd_scene* s, const float* lamp_xyz, 
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t nwords = n_cols * P.words;
-    // room for 2^24 entries (128 MB): C5 flags ~6.6 M; beyond it the collect kernel re-traces inline
+    // room for 2^24 entries (128 MB): C5 flags ~6.6 M; beyond it k_fixup_overflow re-traces the rest
     int64_t cap = std::min<int64_t>(nwords * 32, (int64_t)1 << 24);
     if (const char* e = getenv("UVD_FIXUP_CAP")) cap = std::max<int64_t>(1, std::min<int64_t>(cap, atoll(e)));  // tests
     uint64_t* list = (uint64_t*)al.get((size_t)cap * sizeof(uint64_t) + 256);
@@ -864,7 +892,8 @@ extern "C" int uvd_irradiance_matrix(const uvd_scene* s, const float* lamp_xyz, 
     const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nwords + per - 1) / per, 8 * sms));
     k_fixup_collect<<<g, kCollectThreads, 0, st>>>(P, list, cap, count);
     k_fixup_run<<<UVD_FIX_MINB * sms, 128, 0, st>>>(P, list, cap, count);
-    note_launch(2);
+    k_fixup_overflow<<<2 * sms, 256, 0, st>>>(P, cap, count);
+    note_launch(3);
     al.put(list);
   }
   int rc = UVD_OK;

@@ -66,9 +66,9 @@ def test_octant_copies_off_bit_identical(uvd, monkeypatch):
 @pytest.mark.parametrize("cap", ["1", "5"])
 def test_fixup_list_overflow_bit_identical(uvd, cap, monkeypatch):
     """Entries the fp32 pass leaves undecided go to a list re-traced by
-    k_fixup_run; beyond the list's capacity the collect kernel re-traces them
-    itself.  Both routes give the same exact decisions (UVD_FIXUP_CAP shrinks
-    the list to force the second)."""
+    k_fixup_run; beyond the list's capacity they stay pending and
+    k_fixup_overflow re-traces them.  Both routes give the same exact decisions
+    (UVD_FIXUP_CAP shrinks the list to force the second)."""
     w = ward.ward(seed=9, n_bays=1, e=0.25)
     sc = uvd.Scene(w)
     lam, _ = sc.vantage(configs.vopts(configs.FLOAT3D, 0.5, 0.05))
