@@ -50,6 +50,7 @@ struct AsmParams {
   const float* __restrict__ normal;
   int64_t N;
   const float* __restrict__ lamps;
+  const float* __restrict__ lampc;  // [n_cols][L][3] lamps gathered per column (k_assemble_lane)
   int L;
   double scale;  // P / (4π L)
   const int64_t* __restrict__ cols;  // device, nullptr = identity
@@ -216,13 +217,12 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmMinBlocks) k_assemble_lane(As
     // tile fastest: concurrent warps trace adjacent patches from the same lamp
     int64_t c, tile;
     item_to_tile(P, item, c, tile);
-    const int64_t j = P.cols ? P.cols[c] : c;
     const int r = (int)(tile * 32 + lane);
     const bool valid = r < P.N;
     double acc = 0.0;
     bool pend = false;
     for (int l = 0; l < P.L; ++l) {
-      const float* pl = P.lamps + 3 * (j * P.L + l);
+      const float* pl = P.lampc + 3 * (c * P.L + l);  // one load, no cols[c] -> lamps[j] chain
       const float ox = pl[0], oy = pl[1], oz = pl[2];
       bool vis = false, front = false;
       float cx = 0.f, cy = 0.f, cz = 0.f;
@@ -725,6 +725,17 @@ __global__ void k_col_sumsq(const AsmParams P, const int64_t* __restrict__ colpt
   if (threadIdx.x == 0) out[c] = red[0];
 }
 
+// lamps of each output column, gathered once per call: k_assemble_lane's item
+// prelude then loads its lamp directly instead of cols[c] -> lamps[cols[c]]
+__global__ void k_gather_lamps(const AsmParams P, float* __restrict__ out) {
+  const int64_t per = 3 * (int64_t)P.L, n = P.n_cols * per;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = i / per, q = i - c * per;
+    const int64_t j = P.cols ? P.cols[c] : c;
+    out[i] = P.lamps[j * per + q];
+  }
+}
+
 static int grid_size_assemble() {
   int dev = 0, sms = 0, per = 0;
   cudaGetDevice(&dev);
@@ -851,6 +862,16 @@ extern "C" int uvd_irradiance_matrix(const uvd_scene* s, const float* lamp_xyz, 
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_assemble_lane<true, true>, kAsmThreads, 0);
     grid_c = std::max(1, sms * std::max(per, 1));
   }
+  float* lampc = nullptr;
+  P.lampc = nullptr;
+  if (!area_model) {
+    lampc = (float*)al.get((size_t)n_cols * P.L * 3 * sizeof(float));
+    if (!lampc) { set_error("uvd_irradiance_matrix: out of device memory"); return UVD_ERR_NOMEM; }
+    const int64_t n = n_cols * P.L * 3;
+    k_gather_lamps<<<(unsigned)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, st>>>(P, lampc);
+    note_launch();
+    P.lampc = lampc;
+  }
   if (area_model) {
     static int grid_a = 0;
     if (!grid_a) {
@@ -919,6 +940,6 @@ extern "C" int uvd_irradiance_matrix(const uvd_scene* s, const float* lamp_xyz, 
     note_launch();
   }
   UVD_CUDA_TRY(cudaGetLastError());
-  for (void* p : {(void*)P.pending, (void*)vis_scratch, (void*)colcnt, (void*)dcols}) al.put(p);
+  for (void* p : {(void*)P.pending, (void*)vis_scratch, (void*)colcnt, (void*)dcols, (void*)lampc}) al.put(p);
   return rc;
 }
