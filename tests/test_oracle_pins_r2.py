@@ -1,0 +1,364 @@
+"""Pins for the three oracle parts round 1 left unpinned (VERDICT r1 "What's
+missing" 1): the L > 1 lamp split, the 3D point–triangle clearance distance
+and the Armbot reach proxy.  CPU only; every expected value comes from a
+closed form or a hand-built construction written here, never from the oracle
+itself.
+
+* lamp split ("a set of evenly distributed point sources", reading Q11;
+  S:186–187 "cylinder with L=1 equals point source at the cylinder midpoint"):
+  samples z_l = z0 + (l + 1/2)H/L of power P/L each; the L-sample matrix is the
+  mean of L single-point matrices (superposition, with and without a shadow);
+  a facing patch converges to the analytic line-source irradiance at the
+  midpoint rule's O(1/L²) rate.
+* clearance distance ("dilated by 5 cm"; reading Q10): the oracle's
+  point–triangle distance against the closed form of every Voronoi region of
+  a right triangle, against an independent projection/segment formula and
+  dense sampling on random triangles, and — through the vantage test — on a
+  room with box obstacles whose faces, edges and corners sit 0.05 ± 1e-3 m
+  from grid points (box distance in closed form).
+* reach proxy (P:366 Armbot = mobile base + UR5e; reading Q12): a corridor
+  room whose feasible bases are known by construction, one of two blocked by
+  a hanging plate; lamp points at 0.85 ± 1e-3 m of the free and of the
+  blocked base.
+"""
+import math
+
+import numpy as np
+import pytest
+
+from synth import configs, ward
+
+P_W = configs.P_WATTS
+
+
+def _mesh(boxes):
+    """boxes: list of (lo, hi, inward); each face one quad (2 triangles)."""
+    m = ward._Mesh()
+    for lo, hi, inward in boxes:
+        m.box(lo, hi, 100.0, np.eye(4), inward=inward)
+    V = np.concatenate(m.V).astype(np.float32)
+    F = np.concatenate(m.F).astype(np.int32)
+    return V, F
+
+
+# ----------------------------------------------------------- lamp split ---
+def _line_scene(h=0.75, zc=1.0):
+    """A small triangle in the plane x = 0 facing +x with centroid (0, 0, zc)
+    exactly, plus a helper triangle behind it (x = -1) that widens the bbox so
+    the Towerbot grid has a column at (h, 0); the helper cannot occlude
+    segments from x = h > 0 to the patch."""
+    s = 1.0 / 64
+    V = np.array([[0, -s, zc - s], [0, 2 * s, zc - s], [0, -s, zc + 2 * s],
+                  [-1.0, -0.25, 0.0], [-1.0, 0.25, 0.0], [-1.0, 0.0, 2.5],
+                  [1.0, 0.0, 0.0]], np.float32)
+    # helper: facing -x (away from the lamps); a zero-area-free sliver to x = 1
+    F = np.array([[0, 1, 2], [3, 5, 4], [3, 6, 4]], np.int32)
+    return dict(vertices=V, tris=F)
+
+
+def _tower(scene, L, z0, z1, spacing=0.5):
+    from oracle import oracle as O
+    opts = configs.vopts(configs.TOWER, spacing, 0.0, lamp_z0=z0, lamp_z1=z1, lamp_samples=L)
+    return O.vantage_candidates(scene, opts)
+
+
+def test_cylinder_sample_positions_and_L1_midpoint(orc):
+    """Q11 / P:252: z_l = z0 + (l + 1/2)(z1 - z0)/L; L = 1 puts the one sample at
+    the cylinder midpoint."""
+    sc = _line_scene()
+    z0, z1 = 0.37, 1.57
+    for L in (1, 2, 5, 10):
+        c = _tower(sc, L, z0, z1)
+        zs = c["samples"][0, :, 2].astype(np.float64)
+        f0, f1 = float(np.float32(z0)), float(np.float32(z1))
+        want = np.array([f0 + (l + 0.5) * (f1 - f0) / L for l in range(L)], np.float32)
+        assert np.array_equal(c["samples"][0, :, 2], want)
+        assert np.all(np.diff(zs) > 0) and zs[0] > f0 and zs[-1] < f1
+        # evenly spread: constant gaps H/L, half a gap from each end
+        assert np.allclose(np.diff(zs), (f1 - f0) / L, atol=1e-6)
+        assert abs(zs[0] - f0 - 0.5 * (f1 - f0) / L) < 1e-6
+    c1 = _tower(sc, 1, z0, z1)
+    assert abs(float(c1["samples"][0, 0, 2]) - 0.5 * (z0 + z1)) < 1e-6
+
+
+def test_lamp_split_is_superposition_of_points(orc):
+    """P:252 (P/L per sample, summed): the L-sample entry equals the mean of the
+    L single-point (L = 1, P) entries, sample by sample visibility included — a
+    plate that shadows only the low samples removes exactly their share."""
+    base = _line_scene(h=0.75, zc=1.0)
+    V, F = base["vertices"], base["tris"]
+    # a horizontal plate between the patch and the lower part of the lamp column
+    Vp = np.array([[0.3, -0.3, 0.8], [0.5, -0.3, 0.8], [0.5, 0.3, 0.8], [0.3, 0.3, 0.8]], np.float32)
+    Fp = np.array([[0, 1, 2], [0, 2, 3]], np.int32) + len(V)
+    shadowed = dict(vertices=np.concatenate([V, Vp]), tris=np.concatenate([F, Fp]))
+    for sc in (base, shadowed):
+        p = orc.trimesh_patches(sc["vertices"], sc["tris"])
+        for L in (1, 3, 10):
+            c = _tower(sc, L, 0.37, 1.57)
+            col = int(np.argmin(np.abs(c["points"][:, 0] - 0.75) + np.abs(c["points"][:, 1])))
+            lam = c["samples"][col:col + 1]                       # (1, L, 3)
+            r = orc.irradiance_pairs(p, lam, [0], [0], P=P_W, want_margin=True)
+            singles = orc.irradiance_pairs(p, lam.reshape(L, 1, 3), [0] * L, list(range(L)), P=P_W)
+            assert not r["deg"].any() and not singles["deg"].any()
+            assert np.array_equal(r["vis"][0], singles["vis"][:, 0])
+            want = singles["A"].sum() / L
+            assert abs(r["A"][0] - want) <= 1e-15 * want
+        if sc is shadowed:  # the plate blocks some, not all, of the 10 samples
+            assert 0 < r["vis"][0].sum() < L
+
+
+def test_cylinder_converges_to_line_source(orc):
+    """L evenly distributed samples of P/L approximate a uniform line
+    source of power P on z ∈ [z0, z1].  For a patch at the origin of the plane
+    x = 0 (normal +x) and the line at x = h, the line source gives
+    E = P/(4πH) · [ (z - zc) / (h √(h² + (z - zc)²)) ]_{z0}^{z1}
+    (∫ h dz / (h² + u²)^{3/2} = u/(h√(h²+u²))); the midpoint rule converges to it
+    at O(1/L²).  A missing /L or shifted samples break both the limit and the
+    rate."""
+    h, zc, z0, z1 = 0.75, 1.0, 0.37, 1.57
+    sc = _line_scene(h, zc)
+    p = orc.trimesh_patches(sc["vertices"], sc["tris"])
+    assert p["centroid"][0].tolist() == [0.0, 0.0, zc] and p["normal"][0].tolist() == [1.0, 0.0, 0.0]
+    f0, f1 = float(np.float32(z0)), float(np.float32(z1))
+    H = f1 - f0
+
+    def prim(z):
+        u = z - zc
+        return u / (h * math.sqrt(h * h + u * u))
+    exact = P_W / (4 * math.pi * H) * (prim(f1) - prim(f0))
+    errs = []
+    for L in (4, 8, 16, 32, 64):
+        c = _tower(sc, L, z0, z1)
+        col = int(np.argmin(np.abs(c["points"][:, 0] - h) + np.abs(c["points"][:, 1])))
+        assert abs(c["points"][col, 0] - h) < 1e-7 and c["points"][col, 1] == 0.0
+        r = orc.irradiance_pairs(p, c["samples"][col:col + 1], [0], [0], P=P_W)
+        assert r["vis"].all() and not r["deg"].any()
+        errs.append(abs(r["A"][0] - exact) / exact)
+    # second-order convergence (ratio -> 4) down to the fp32 rounding of the samples
+    for a, b in zip(errs[:-2], errs[1:-1]):
+        assert 3.5 < a / b < 4.5, errs
+    assert errs[-1] < 2e-4, errs
+
+
+# ------------------------------------------------- point–triangle distance ---
+def _dist_via_vantage(orc, tri9, pts):
+    """min distance of each point to the triangle(s), through the oracle's
+    vantage evaluation (the routine the clearance decision uses)."""
+    tri9 = np.ascontiguousarray(np.asarray(tri9, np.float32).reshape(-1, 9))
+    pts = np.ascontiguousarray(np.asarray(pts, np.float32).reshape(-1, 3))
+    R = len(pts)
+    feas = np.zeros(R, np.uint8)
+    amb = np.zeros(R, np.uint8)
+    md = np.zeros(R, np.float64)
+    orc.lib().orc_vantage_eval_3d(tri9, len(tri9), pts.reshape(-1), R, 1, 0.05, 0, feas, amb, md, 0)
+    return md, feas.astype(bool)
+
+
+def test_point_triangle_distance_every_region(orc):
+    """Closed forms on the right triangle a=(0,0,0), b=(1,0,0), c=(0,1,0), a
+    point at height z above each Voronoi region: the face (distance |z|), the
+    three vertices and the three edges (the hypotenuse x + y = 1 at horizontal
+    distance (x + y - 1)/√2)."""
+    tri = [0, 0, 0, 1, 0, 0, 0, 1, 0]
+    cases = []
+    for z in (0.0, 0.25, -0.5):
+        z2 = z * z
+        cases += [((0.25, 0.25, z), abs(z)),                                  # face
+                  ((-0.5, -0.75, z), math.sqrt(0.25 + 0.5625 + z2)),         # vertex a
+                  ((1.5, -0.5, z), math.sqrt(0.25 + 0.25 + z2)),             # vertex b
+                  ((-0.25, 1.75, z), math.sqrt(0.0625 + 0.5625 + z2)),       # vertex c
+                  ((0.5, -0.5, z), math.sqrt(0.25 + z2)),                    # edge ab (y = 0)
+                  ((-0.75, 0.5, z), math.sqrt(0.5625 + z2)),                 # edge ac (x = 0)
+                  ((1.0, 0.5, z), math.sqrt(0.125 + z2)),                    # edge bc: (1+.5-1)/√2
+                  ((0.0, 0.0, z), abs(z)), ((1.0, 0.0, z), abs(z))]          # on a vertex
+    pts = [c[0] for c in cases]
+    md, _ = _dist_via_vantage(orc, tri, pts)
+    for (p, want), got in zip(cases, md):
+        assert abs(got - want) <= 1e-15 * max(1.0, want), (p, got, want)
+
+
+def _ref_point_tri(p, a, b, c):
+    """Independent formula: projection onto the plane if it falls inside the
+    triangle (barycentric solve), else the nearest of the three edge segments."""
+    n = np.cross(b - a, c - a)
+    n = n / np.linalg.norm(n)
+    q = p - np.dot(p - a, n) * n
+    M = np.stack([b - a, c - a], 1)
+    uv, *_ = np.linalg.lstsq(M, q - a, rcond=None)
+    if uv[0] >= 0 and uv[1] >= 0 and uv.sum() <= 1:
+        return abs(np.dot(p - a, n))
+
+    def seg(x, y):
+        t = np.clip(np.dot(p - x, y - x) / np.dot(y - x, y - x), 0.0, 1.0)
+        return np.linalg.norm(p - (x + t * (y - x)))
+    return min(seg(a, b), seg(b, c), seg(c, a))
+
+
+def test_point_triangle_distance_random_triangles(orc):
+    """Random triangles and points (some near the plane, some far): the oracle's
+    distance equals the projection/segment formula and never exceeds the
+    minimum over a dense barycentric sampling of the triangle, which it
+    approaches within the sampling step."""
+    rng = np.random.default_rng(7)
+    tris, pts = [], []
+    for _ in range(300):
+        a, b, c = rng.normal(0, 1, (3, 3)).astype(np.float32)
+        if np.linalg.norm(np.cross(b - a, c - a)) < 1e-2:
+            continue
+        tris.append(np.concatenate([a, b, c]))
+        p = rng.normal(0, 1.5, 3).astype(np.float32)
+        if rng.uniform() < 0.3:  # near the plane
+            n = np.cross(b - a, c - a)
+            p = (p - np.dot(p - a, n) / np.dot(n, n) * n + rng.normal(0, 1e-3) * n).astype(np.float32)
+        pts.append(p)
+    g = 200
+    u, v = np.meshgrid(np.arange(g + 1) / g, np.arange(g + 1) / g, indexing="ij")
+    keep = (u + v) <= 1
+    u, v = u[keep], v[keep]
+    for tri, p in zip(tris, pts):
+        md, _ = _dist_via_vantage(orc, tri, p)
+        a, b, c = (tri[3 * k:3 * k + 3].astype(np.float64) for k in range(3))
+        p64 = p.astype(np.float64)
+        ref = _ref_point_tri(p64, a, b, c)
+        assert abs(md[0] - ref) <= 1e-9 * max(1.0, ref)
+        S = a[None] + u[:, None] * (b - a)[None] + v[:, None] * (c - a)[None]
+        smin = np.sqrt(((S - p64) ** 2).sum(1)).min()
+        step = max(np.linalg.norm(b - a), np.linalg.norm(c - a), np.linalg.norm(c - b)) / g
+        assert md[0] <= smin + 1e-12 and smin - md[0] <= step
+
+
+def clearance_scene():
+    """Room [0,2]³ (inward shell) with three boxes placed so FLOAT3D grid points
+    (cell centres 0.125 + 0.25 a) sit 0.05 ± 1e-3 m from a face (box A), from a
+    corner (box B, vertex region) and from an edge (box C)."""
+    e, f = 0.049, 0.051
+    boxes = [((0.0, 0.0, 0.0), (2.0, 2.0, 2.0), True),
+             ((0.875 + e, 0.875 + f, 0.875 + e), (1.375 - f, 1.375 - e, 1.375 - f), False),   # A
+             ((0.375 + e / math.sqrt(3),) * 3, (0.375 + e / math.sqrt(3) + 0.15,) * 3, False),   # B
+             ((1.625 + f / math.sqrt(2), 0.375 + f / math.sqrt(2), 0.3),
+              (1.625 + f / math.sqrt(2) + 0.15, 0.375 + f / math.sqrt(2) + 0.15, 0.45), False)]  # C
+    V, F = _mesh(boxes)
+    return dict(vertices=V, tris=F), len(boxes)
+
+
+def clearance_expected(sc, n_boxes, pts):
+    """Closed-form distance of each point to the room shell and the boxes, from
+    the fp32 vertices (12 triangles per box in generation order), and whether
+    it lies inside an obstacle."""
+    V = sc["vertices"].astype(np.float64)
+    P = np.asarray(pts, np.float64)
+    per = len(V) // n_boxes
+    d = np.full(len(P), np.inf)
+    inside = np.zeros(len(P), bool)
+    for k in range(n_boxes):
+        B = V[k * per:(k + 1) * per]
+        lo, hi = B.min(0), B.max(0)
+        if k == 0:   # shell: points are inside the room
+            d = np.minimum(d, np.minimum(P - lo, hi - P).min(1))
+        else:
+            dd = np.sqrt((np.maximum(np.maximum(lo - P, P - hi), 0.0) ** 2).sum(1))
+            ins = ((P > lo) & (P < hi)).all(1)
+            inside |= ins
+            d = np.minimum(d, np.where(ins, np.minimum(P - lo, hi - P).min(1), dd))
+    return d, inside
+
+
+def test_clearance_threshold_flips_feasibility(orc):
+    """P:199 (5 cm dilation), Q10: on the clearance scene every grid point's
+    oracle feasibility equals [closed-form distance ≥ 0.05 and free], the
+    oracle's minimum distance equals the closed form (faces, edges, corners),
+    and the hand-placed points at 0.049 / 0.051 m fall on the expected side."""
+    sc, nb = clearance_scene()
+    opts = configs.vopts(configs.FLOAT3D, 0.25, 0.05)
+    v = orc.vantage(sc, opts)
+    P = v["points"]
+    d, inside = clearance_expected(sc, nb, P)
+    tri = np.ascontiguousarray(sc["vertices"][sc["tris"]].reshape(-1, 9))
+    md, _ = _dist_via_vantage(orc, tri, P)
+    assert np.allclose(md, d, rtol=0, atol=1e-7)
+    want = (d >= 0.05) & ~inside
+    assert np.array_equal(v["feasible"], want)
+    assert not v["ambiguous"].any()
+    # the threshold cases are really there
+    near = np.abs(d - 0.05) < 1.5e-3
+    assert near.sum() >= 6
+    assert v["feasible"][near].any() and (~v["feasible"][near]).any()
+    for q, dist in (((0.875, 1.125, 1.125), 0.049), ((1.375, 1.125, 1.125), 0.051),
+                    ((1.125, 0.875, 1.125), 0.051), ((1.125, 1.375, 1.125), 0.049),
+                    ((0.375, 0.375, 0.375), 0.049), ((1.625, 0.375, 0.375), 0.051)):
+        k = int(np.argmin(np.abs(P - np.array(q, np.float32)).sum(1)))
+        assert np.abs(P[k] - q).max() == 0.0
+        assert abs(d[k] - dist) < 2e-7, (q, d[k])
+        assert v["feasible"][k] == (dist > 0.05)
+
+
+# ------------------------------------------------------------ reach proxy ---
+def corridor_scene():
+    """Corridor room x ∈ [0,1], y ∈ [0,0.75], z ∈ [0,2.5] (inward shell) and a
+    small plate hanging 0.25 m above base b2.  With ρ = 0.25, base_z = 0.4 and
+    base clearance 0.325 (Q10/Q12) the floor grid (x, y ∈ {0.125, 0.375, ...})
+    has exactly two bases clear of the walls, b1 = (0.375, 0.375, 0.4) and
+    b2 = (0.625, 0.375, 0.4); the plate is 0.25 m from b2 (blocked) and
+    √(0.245² + 0.25²) = 0.35 m from b1 (free)."""
+    boxes = [((0.0, 0.0, 0.0), (1.0, 0.75, 2.5), True),
+             ((0.62, 0.35, 0.65), (0.70, 0.40, 0.70), False)]
+    V, F = _mesh(boxes)
+    return dict(vertices=V, tris=F)
+
+
+ARM_CORRIDOR = configs.vopts(configs.ARM, 0.25, 0.05, zmin=0.3, zmax=1.9, reach=0.85,
+                             base_clearance=0.325, base_z=0.4)
+B1 = np.array([0.375, 0.375, np.float32(0.4)], np.float64)   # fp32 grid values, exact in fp64
+B2 = np.array([0.625, 0.375, np.float32(0.4)], np.float64)
+
+
+def test_reach_proxy_bases(orc):
+    sc = corridor_scene()
+    b = orc.arm_bases(sc, ARM_CORRIDOR)
+    got = b["points"][b["feasible"]].astype(np.float64)
+    assert got.tolist() == [B1.tolist()]
+    assert not b["ambiguous"].any()
+
+
+def test_reach_proxy_hand_placed_lamps(orc):
+    """Q12: a lamp is reachable iff within 0.85 m of a FEASIBLE base; points at
+    0.85 ∓ 1e-3 from b1 in several directions flip; points within reach of the
+    blocked base b2 only are not reachable."""
+    sc = corridor_scene()
+    rng = np.random.default_rng(3)
+    dirs = [np.array([0, 0, 1.0]), np.array([0.6, 0, 0.8]), np.array([-0.28, 0.0, 0.96])]
+    dirs += [u / np.linalg.norm(u) for u in rng.normal(0, 1, (5, 3)) if u[2] > 0]
+    pts, want = [], []
+    for u in dirs:
+        for r, ok in ((0.849, True), (0.851, False)):
+            pts.append(B1 + r * u)
+            want.append(ok)
+    for dz in (0.70, 0.75, 0.80):   # within reach of b2 but > 0.85 from b1
+        q = B2 + np.array([0.24, 0, dz])
+        assert np.linalg.norm(q - B2) < 0.85 < np.linalg.norm(q - B1)
+        pts.append(q)
+        want.append(False)
+    pts = np.asarray(pts, np.float32)
+    ok, amb = orc.arm_reach(sc, ARM_CORRIDOR, pts)
+    # fp32 storage moves a point by <= 1e-7 m: far from the 1e-3 margins
+    assert ok.tolist() == want
+    assert not amb.any()
+
+
+def test_arm_vantage_matches_hand_derivation(orc):
+    """Full Armbot feasibility on the corridor (Q12): grid over x, y of the bbox
+    × z ∈ [0.3, 1.9]; feasible iff ≥ 0.05 m from every surface (closed-form box
+    distances), free (inside the room, outside the plate) and within 0.85 m of
+    b1 — derived here without the oracle's clearance or reach code."""
+    sc = corridor_scene()
+    v = orc.vantage(sc, ARM_CORRIDOR)
+    P = v["points"].astype(np.float64)
+    d, inside = clearance_expected(sc, 2, P)
+    reach = np.linalg.norm(P - B1, axis=1) <= np.float32(0.85)
+    want = (d >= 0.05) & ~inside & reach
+    assert np.array_equal(v["feasible"], want)
+    assert not v["ambiguous"].any()
+    assert 0 < want.sum() < len(want)
+    # the blocked base matters: b2 would add points
+    reach2 = np.linalg.norm(P - B2, axis=1) <= 0.85
+    assert ((d >= 0.05) & ~inside & reach2 & ~reach).any()
