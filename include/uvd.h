@@ -19,8 +19,17 @@
  *
  * Streams: every call enqueues on `stream` (a cudaStream_t, NULL = legacy
  * default stream).  Calls that return host scalars synchronise that stream:
- * uvd_scene_create, uvd_vantage_sample, uvd_sync_status, uvd_coverage.
- * A scene is immutable after creation; concurrent const calls are safe.
+ * uvd_scene_create, uvd_vantage_sample, uvd_sync_status, uvd_coverage (and
+ * uvd_static_columns when asked for its choice).
+ * A scene's data are immutable after creation; const calls on one scene may
+ * run concurrently on different streams or threads (the only per-scene
+ * mutable state — coverage partial sums — is kept per stream; the in-kernel
+ * error flag is shared, see uvd_sync_status).
+ * Devices: every call runs on the device of its scene (uvd_fluence /
+ * uvd_lp_solve: of their `out` / `t` buffer) and restores the caller's current
+ * device before returning.
+ *
+ * Profiling: every entry point is an NVTX range named after it.
  *
  * Errors: no exception crosses the ABI.  Calls return UVD_OK (0) or a
  * negative uvd_status and set a thread-local message (uvd_last_error).  On
@@ -140,6 +149,9 @@ UVD_API int uvd_scene_query(const uvd_scene* scene, int64_t* n_patches, int64_t*
 UVD_API int uvd_scene_patches(const uvd_scene* scene, float* centroid, float* normal, double* area,
                       int64_t* orig_id, void* stream);
 
+/* Release the scene.  Synchronises the scene's device first (every stream
+ * that used the scene must be done before its buffers go back to the
+ * allocator), then frees them. */
 UVD_API void uvd_scene_destroy(uvd_scene* scene);
 
 /* Introspection of the scene's BVH (a2), for structural tests and tree-quality
@@ -241,6 +253,18 @@ typedef struct {
   uint32_t* vis_bits;
   double* col_sumsq;
   unsigned long long* counters;
+  /* optional (parity tools and tests): the entries the fp32 pass left
+   * undecided and re-traced with exact fp64 triangle tests (DESIGN.md §6,
+   * k_fixup), as (local column << 32) | row, in no particular order.  At most
+   * fixup_cap are written to fixup_list; *fixup_count (DEVICE int64) receives
+   * their total.  NULL fixup_list / fixup_count: not reported. */
+  uint64_t* fixup_list;
+  int64_t fixup_cap;
+  int64_t* fixup_count;
+  /* optional: allocator of the call's scratch in uvd_fluence, uvd_lp_solve and
+   * uvd_static_columns (stream-ordered on the call's stream, returned before
+   * the call does); NULL = cudaMallocAsync / cudaFreeAsync (the ABI default). */
+  const uvd_allocator* allocator;
 } uvd_matrix_out;
 
 /* Assemble columns of A (a4 cull, a5 occlusion, a6 Eq. 7):
@@ -258,10 +282,15 @@ UVD_API int uvd_irradiance_matrix(const uvd_scene* scene, const float* lamp_xyz,
                           const int64_t* cols, int64_t n_cols, const uvd_lamp* lamp,
                           uvd_matrix_out* out, void* stream);
 
-/* Synchronise `stream` and report (then clear) the scene's in-kernel error flag:
- * UVD_OK, UVD_ERR_DOMAIN (a lamp–centroid distance < 1e-9 m), or UVD_ERR_CUDA
- * for a traversal-stack overflow (cannot happen: scene creation refuses BVHs
- * deeper than the 64-entry stacks with UVD_ERR_INVALID). */
+/* Synchronise `stream` and report the scene's in-kernel error flag, read and
+ * cleared in one device atomic: UVD_OK, UVD_ERR_DOMAIN (a lamp–centroid
+ * distance < 1e-9 m), or UVD_ERR_CUDA for a traversal-stack overflow (cannot
+ * happen: scene creation refuses BVHs deeper than 62 levels with
+ * UVD_ERR_INVALID).  The flag is per SCENE, not per stream: the call reports
+ * errors raised by any assembly on this scene, on any stream, that completed
+ * before it; an error raised later stays for the next call.  Callers that
+ * assemble on several streams and need per-stream attribution synchronise
+ * those streams first. */
 UVD_API int uvd_sync_status(const uvd_scene* scene, void* stream);
 
 /* ---------------------------------------------------------------------- a7 */
@@ -313,10 +342,15 @@ UVD_API int uvd_cubemap_matrix(const uvd_scene* scene, const float* lamp_xyz, in
  *   out[3j+1] = min_{i: A_ij > 0} A_ij           (+inf if none): dwell to cover
  *               every visible patch = μ_min / out[3j+1] (s)
  *   out[3j+2] = Σ_i |s_i| [A_ij · t_budget ≥ μ_min]  area covered in t_budget
- * out: DEVICE fp64 [3k].  The caller picks the column (maximum visible area,
- * reading Q24 for ties).  Deterministic.  Asynchronous. */
+ * out: DEVICE fp64 [3k].
+ * choice (HOST [2], optional): [0] = the static lamp's column — the largest
+ * visible area, ties to the shorter dwell μ_min / out[3j+1], then the lower
+ * index (reading Q24); [1] = the column covering most area within t_budget
+ * (ties to the lower index); -1 when k = 0.  dwell (HOST, optional): μ_min /
+ * min A of choice[0] (s; +inf if it sees nothing).  Deterministic.
+ * Asynchronous unless choice or dwell is requested (then synchronises). */
 UVD_API int uvd_static_columns(const uvd_scene* scene, const uvd_matrix_out* A, int64_t k, double t_budget,
-                       double mu_min, double* out, void* stream);
+                       double mu_min, double* out, int64_t choice[2], double* dwell, void* stream);
 
 /* ------------------------------------------------------------------ NEXT-1 */
 /* Relaxed dwell-time LP, Eq. 9 (§IV-D first stage):

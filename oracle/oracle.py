@@ -302,15 +302,25 @@ def vantage(scene: dict, opts: dict, idx=None, n_threads: int = 0) -> dict:
                 ambiguous=amb.astype(bool), idx=idx)
 
 
-def arm_bases(scene: dict, opts: dict, tri=None, n_threads: int = 0) -> dict:
+def arm_bases(scene: dict, opts: dict, tri=None, n_threads: int = 0, near=None) -> dict:
     """Armbot base positions: floor grid at z = base_z, feasible iff clearance
-    base_clearance from every triangle and in free space (Q12)."""
+    base_clearance from every triangle and in free space (Q12).  near: optional
+    (R, 3) points; only bases within reach + 1e-3 m of one of them are
+    evaluated (the others cannot decide the reach proxy for those points)."""
     lo, hi = _mesh_bbox(scene)
     rho = opts["spacing"]
     xs, ys = grid_axis(lo[0], hi[0], rho), grid_axis(lo[1], hi[1], rho)
     Y, X = np.meshgrid(ys, xs, indexing="ij")
     pts = np.stack([X.ravel(), Y.ravel(), np.full(X.size, np.float32(opts["base_z"]))], 1)
     pts = np.ascontiguousarray(pts, np.float32)
+    if near is not None:
+        lim = float(np.float32(opts["reach"])) + 1e-3
+        Q = np.asarray(near, np.float64)
+        keep = np.zeros(len(pts), bool)
+        for s in range(0, len(Q), 256):
+            d2 = ((Q[s:s + 256, None, :] - pts[None, :, :].astype(np.float64)) ** 2).sum(-1)
+            keep |= (d2 <= lim * lim).any(0)
+        pts = np.ascontiguousarray(pts[keep])
     if tri is None:
         tri = np.ascontiguousarray(np.asarray(scene["vertices"], np.float32)[scene["tris"]].reshape(-1, 9))
     R = len(pts)
@@ -326,7 +336,7 @@ def arm_reach(scene, opts, lamp_pts, tri=None, n_threads: int = 0):
     """Reach proxy (Q12): lamp p is reachable iff |p − b| ≤ reach (fp64) for some
     feasible base b.  Ambiguous if the decision depends on an ambiguous base or a
     distance within 1e-6 of the reach."""
-    bases = arm_bases(scene, opts, tri, n_threads)
+    bases = arm_bases(scene, opts, tri, n_threads, near=lamp_pts)
     B = bases["points"].astype(np.float64)
     reach = float(np.float32(opts["reach"]))
     ok = np.zeros(len(lamp_pts), bool)

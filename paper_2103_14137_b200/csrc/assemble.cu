@@ -736,12 +736,25 @@ __global__ void k_gather_lamps(const AsmParams P, float* __restrict__ out) {
   }
 }
 
-static int grid_size_assemble() {
-  int dev = 0, sms = 0, per = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_assemble_lane<false, true>, kAsmThreads, 0);
-  return std::max(1, sms * std::max(per, 1));
+// persistent grids (occupancy x SMs), cached per device and kernel
+template <typename K>
+static int persistent_grid(K kernel, int threads, int dev, int* cache) {
+  if (dev < 0 || dev >= kMaxDevices) dev = 0;
+  if (!cache[dev]) {
+    int per = 0;
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, kernel, threads, 0);
+    cache[dev] = std::max(1, sm_count(dev) * std::max(per, 1));
+  }
+  return cache[dev];
+}
+
+__global__ void k_take_fixups(const uint64_t* __restrict__ list, const unsigned long long* __restrict__ count,
+                              int64_t cap, uint64_t* __restrict__ out, int64_t out_cap, int64_t* __restrict__ n_out) {
+  const int64_t n = (int64_t)*count;
+  const int64_t m = min(min(n, cap), out_cap);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = list[i];
+  if (blockIdx.x == 0 && threadIdx.x == 0) *n_out = n;
 }
 
 }  // namespace uvd
@@ -756,6 +769,8 @@ extern "C" int uvd_irradiance_matrix(const uvd_scene* s, const float* lamp_xyz, 
     set_error("uvd_irradiance_matrix: null argument");
     return UVD_ERR_INVALID;
   }
+  DeviceGuard dg(s->alloc.device);
+  NvtxRange nv("uvd_irradiance_matrix");
   if (lamp->samples_per_config < 1 || !(lamp->power_w > 0.0)) {
     set_error("uvd_irradiance_matrix: need power_w > 0 and samples_per_config >= 1");
     return UVD_ERR_INVALID;
@@ -783,8 +798,14 @@ extern "C" int uvd_irradiance_matrix(const uvd_scene* s, const float* lamp_xyz, 
     set_error("uvd_irradiance_matrix: unknown format %d", out->format);
     return UVD_ERR_INVALID;
   }
+  if ((out->fixup_list && (!out->fixup_count || out->fixup_cap < 0)) || (out->fixup_count && !out->fixup_list)) {
+    set_error("uvd_irradiance_matrix: fixup_list needs fixup_count and fixup_cap >= 0");
+    return UVD_ERR_INVALID;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
   if (n_cols == 0) {
-    if (csc && out->colptr) UVD_CUDA_TRY(cudaMemsetAsync(out->colptr, 0, sizeof(int64_t), (cudaStream_t)stream));
+    if (csc && out->colptr) UVD_CUDA_TRY(cudaMemsetAsync(out->colptr, 0, sizeof(int64_t), st));
+    if (out->fixup_count) UVD_CUDA_TRY(cudaMemsetAsync(out->fixup_count, 0, sizeof(int64_t), st));
     return UVD_OK;
   }
   if (!csc && (!out->values || out->ld < s->N || out->ld % 32 != 0)) {
@@ -795,9 +816,9 @@ extern "C" int uvd_irradiance_matrix(const uvd_scene* s, const float* lamp_xyz, 
     set_error("uvd_irradiance_matrix: CSC output needs colptr (and rowidx/values when nnz_cap > 0)");
     return UVD_ERR_INVALID;
   }
-  cudaStream_t st = (cudaStream_t)stream;
-  Alloc al = s->alloc;
-  al.stream = st;
+  const int dev = s->alloc.device;
+  const int sms = sm_count(dev);
+  Scratch sc(s->alloc, st);  // every scratch buffer below goes back at every exit
   AsmParams P;
   P.tri = s->tri;
   P.nodes = s->nodes;
@@ -814,8 +835,7 @@ extern "C" int uvd_irradiance_matrix(const uvd_scene* s, const float* lamp_xyz, 
   P.words = (s->N + 31) / 32;
   P.tiles = csc ? P.words : out->ld / 32;
   {  // work order (item_to_tile): super-tiles of 512 tiles when the traversal data is > 2x the L2
-    int dev = 0, l2 = 0;
-    cudaGetDevice(&dev);
+    int l2 = 0;
     cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
     const double bvh_bytes = 8.0 * (double)s->n_nodes * sizeof(Node) + 48.0 * (double)s->M;
     P.super_log2 = bvh_bytes > 2.0 * (double)l2 ? 9 : -1;
@@ -833,89 +853,64 @@ extern "C" int uvd_irradiance_matrix(const uvd_scene* s, const float* lamp_xyz, 
   P.ptri = s->kind == UVD_SCENE_EXTRUDED ? s->ptri : nullptr;
   P.area_m = area_model ? lamp->subdiv : -1;
   // scratch: column ids, undecided-entry bits, visibility bits for CSC
-  int64_t* dcols = nullptr;
-  uint32_t* vis_scratch = nullptr;
-  int64_t* colcnt = nullptr;
-  if (cols) dcols = (int64_t*)al.get(n_cols * sizeof(int64_t));
-  P.pending = (uint32_t*)al.get((size_t)n_cols * P.words * sizeof(uint32_t));
-  if (P.pending && ((uintptr_t)P.pending & 15u)) {  // k_fixup_collect reads it with 16-B loads
-    set_error("uvd_irradiance_matrix: allocator returned a buffer not 16-B aligned");
-    al.put(P.pending);
-    return UVD_ERR_INVALID;
-  }
-  if (csc && !out->vis_bits)
-    vis_scratch = (uint32_t*)al.get((size_t)n_cols * P.L * P.words * sizeof(uint32_t));
-  if (csc) colcnt = (int64_t*)al.get(n_cols * sizeof(int64_t));
+  int64_t* dcols = cols ? (int64_t*)sc.get(n_cols * sizeof(int64_t)) : nullptr;
+  P.pending = (uint32_t*)sc.get((size_t)n_cols * P.words * sizeof(uint32_t));
+  uint32_t* vis_scratch =
+      csc && !out->vis_bits ? (uint32_t*)sc.get((size_t)n_cols * P.L * P.words * sizeof(uint32_t)) : nullptr;
+  int64_t* colcnt = csc ? (int64_t*)sc.get(n_cols * sizeof(int64_t)) : nullptr;
   if ((cols && !dcols) || !P.pending || (csc && !out->vis_bits && !vis_scratch) || (csc && !colcnt)) {
     set_error("uvd_irradiance_matrix: out of device memory");
     return UVD_ERR_NOMEM;
   }
+  if ((uintptr_t)P.pending & 15u) {  // k_fixup_collect reads it with 16-B loads
+    set_error("uvd_irradiance_matrix: allocator returned a buffer not 16-B aligned");
+    return UVD_ERR_INVALID;
+  }
   if (dcols) UVD_CUDA_TRY(cudaMemcpyAsync(dcols, cols, n_cols * sizeof(int64_t), cudaMemcpyHostToDevice, st));
   P.cols = dcols;
   P.vis_bits = out->vis_bits ? out->vis_bits : vis_scratch;
-  static int grid = 0, grid_c = 0;
-  if (!grid) grid = grid_size_assemble();
-  if (!grid_c) {
-    int dev = 0, sms = 0, per = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_assemble_lane<true, true>, kAsmThreads, 0);
-    grid_c = std::max(1, sms * std::max(per, 1));
-  }
-  float* lampc = nullptr;
   P.lampc = nullptr;
   if (!area_model) {
-    lampc = (float*)al.get((size_t)n_cols * P.L * 3 * sizeof(float));
+    float* lampc = (float*)sc.get((size_t)n_cols * P.L * 3 * sizeof(float));
     if (!lampc) { set_error("uvd_irradiance_matrix: out of device memory"); return UVD_ERR_NOMEM; }
     const int64_t n = n_cols * P.L * 3;
     k_gather_lamps<<<(unsigned)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, st>>>(P, lampc);
     note_launch();
     P.lampc = lampc;
   }
+  static int g_lane[4][kMaxDevices], g_area[4][kMaxDevices];  // [COUNT * 2 + OCT][device]
+  const int gi = (P.counters ? 2 : 0) + (P.onodes ? 1 : 0);
+  // octant node copies when the scene has them (bvh.cu caps their memory)
   if (area_model) {
-    static int grid_a = 0;
-    if (!grid_a) {
-      int dev = 0, sms = 0, per = 0;
-      cudaGetDevice(&dev);
-      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-      cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k_assemble_area<false, true>, kAreaThreads, 0);
-      grid_a = std::max(1, sms * std::max(per, 1));
-    }
-    // octant node copies when the scene has them (bvh.cu caps their memory)
-    if (P.counters) {
-      if (P.onodes) k_assemble_area<true, true><<<grid_a, kAreaThreads, 0, st>>>(P);
-      else k_assemble_area<true, false><<<grid_a, kAreaThreads, 0, st>>>(P);
-    } else {
-      if (P.onodes) k_assemble_area<false, true><<<grid_a, kAreaThreads, 0, st>>>(P);
-      else k_assemble_area<false, false><<<grid_a, kAreaThreads, 0, st>>>(P);
-    }
-  } else if (P.counters) {
-    if (P.onodes) k_assemble_lane<true, true><<<grid_c, kAsmThreads, 0, st>>>(P);
-    else k_assemble_lane<true, false><<<grid_c, kAsmThreads, 0, st>>>(P);
+    auto kern = P.counters ? (P.onodes ? k_assemble_area<true, true> : k_assemble_area<true, false>)
+                           : (P.onodes ? k_assemble_area<false, true> : k_assemble_area<false, false>);
+    kern<<<persistent_grid(kern, kAreaThreads, dev, g_area[gi]), kAreaThreads, 0, st>>>(P);
   } else {
-    if (P.onodes) k_assemble_lane<false, true><<<grid, kAsmThreads, 0, st>>>(P);
-    else k_assemble_lane<false, false><<<grid, kAsmThreads, 0, st>>>(P);
+    auto kern = P.counters ? (P.onodes ? k_assemble_lane<true, true> : k_assemble_lane<true, false>)
+                           : (P.onodes ? k_assemble_lane<false, true> : k_assemble_lane<false, false>);
+    kern<<<persistent_grid(kern, kAsmThreads, dev, g_lane[gi]), kAsmThreads, 0, st>>>(P);
   }
   note_launch();
   {  // exact fp64 re-trace of the (rare) entries the fp32 pass left undecided
-    int dev = 0, sms = 148;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t nwords = n_cols * P.words;
     // room for 2^24 entries (128 MB): C5 flags ~6.6 M; beyond it k_fixup_overflow re-traces the rest
     int64_t cap = std::min<int64_t>(nwords * 32, (int64_t)1 << 24);
     if (const char* e = getenv("UVD_FIXUP_CAP")) cap = std::max<int64_t>(1, std::min<int64_t>(cap, atoll(e)));  // tests
-    uint64_t* list = (uint64_t*)al.get((size_t)cap * sizeof(uint64_t) + 256);
+    uint64_t* list = (uint64_t*)sc.get((size_t)cap * sizeof(uint64_t) + 256);
     if (!list) { set_error("uvd_irradiance_matrix: out of device memory"); return UVD_ERR_NOMEM; }
     unsigned long long* count = (unsigned long long*)((char*)list + (size_t)cap * sizeof(uint64_t));
     UVD_CUDA_TRY(cudaMemsetAsync(count, 0, sizeof(unsigned long long), st));
     const int64_t per = (int64_t)kCollectThreads * kCollectWords;
     const unsigned g = (unsigned)std::max<int64_t>(1, std::min<int64_t>((nwords + per - 1) / per, 8 * sms));
     k_fixup_collect<<<g, kCollectThreads, 0, st>>>(P, list, cap, count);
+    if (out->fixup_list) {  // debug/parity export, before the re-trace (the list itself is unchanged by it)
+      k_take_fixups<<<(unsigned)std::max(1, 2 * sms), 256, 0, st>>>(list, count, cap, out->fixup_list, out->fixup_cap,
+                                                                    out->fixup_count);
+      note_launch();
+    }
     k_fixup_run<<<UVD_FIX_MINB * sms, 128, 0, st>>>(P, list, cap, count);
     k_fixup_overflow<<<2 * sms, 256, 0, st>>>(P, cap, count);
     note_launch(3);
-    al.put(list);
   }
   int rc = UVD_OK;
   if (csc) {
@@ -940,6 +935,5 @@ extern "C" int uvd_irradiance_matrix(const uvd_scene* s, const float* lamp_xyz, 
     note_launch();
   }
   UVD_CUDA_TRY(cudaGetLastError());
-  for (void* p : {(void*)P.pending, (void*)vis_scratch, (void*)colcnt, (void*)dcols, (void*)lampc}) al.put(p);
   return rc;
 }

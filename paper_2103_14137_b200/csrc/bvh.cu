@@ -1265,10 +1265,11 @@ __global__ void k_max_depth(const int32_t* __restrict__ parent_leaf, const int32
 // On return s->tri is leaf-ordered and `order` (if non-null) receives the
 // sorted -> input permutation (caller frees).
 int build_bvh(uvd_scene* s, float4* tri_in, uint32_t** order_out, cudaStream_t st) {
-  Alloc& al = s->alloc;
+  Alloc& al = s->alloc;     // scene-owned buffers (freed with the scene)
+  Scratch sc(al, st);       // this build's temporaries, released at every exit
   const int64_t M = s->M;
-  uint64_t* keys = (uint64_t*)al.get(M * sizeof(uint64_t));
-  uint32_t* vals = (uint32_t*)al.get(M * sizeof(uint32_t));
+  uint64_t* keys = (uint64_t*)sc.get(M * sizeof(uint64_t));
+  uint32_t* vals = (uint32_t*)sc.get(M * sizeof(uint32_t));
   s->tri = (float4*)al.get(3 * M * sizeof(float4));
   s->nodes = (Node*)al.get(std::max<int64_t>(M - 1, 1) * sizeof(Node));
   if (!keys || !vals || !s->tri || !s->nodes) {
@@ -1296,14 +1297,14 @@ int build_bvh(uvd_scene* s, float4* tri_in, uint32_t** order_out, cudaStream_t s
     s->root = 0;
   } else {
     int64_t ni = M - 1;
-    int32_t* left = (int32_t*)al.get(ni * 4);
-    int32_t* right = (int32_t*)al.get(ni * 4);
-    int32_t* rf = (int32_t*)al.get(ni * 4);
-    int32_t* rl = (int32_t*)al.get(ni * 4);
-    int32_t* pint = (int32_t*)al.get(ni * 4);
-    int32_t* pleaf = (int32_t*)al.get(M * 4);
-    float* ibox = (float*)al.get(ni * 6 * sizeof(float));
-    int* arrive = (int*)al.get(ni * sizeof(int));
+    int32_t* left = (int32_t*)sc.get(ni * 4);
+    int32_t* right = (int32_t*)sc.get(ni * 4);
+    int32_t* rf = (int32_t*)sc.get(ni * 4);
+    int32_t* rl = (int32_t*)sc.get(ni * 4);
+    int32_t* pint = (int32_t*)sc.get(ni * 4);
+    int32_t* pleaf = (int32_t*)sc.get(M * 4);
+    float* ibox = (float*)sc.get(ni * 6 * sizeof(float));
+    int* arrive = (int*)sc.get(ni * sizeof(int));
     if (!left || !right || !rf || !rl || !pint || !pleaf || !ibox || !arrive) {
       set_error("scene: out of device memory (BVH scratch)");
       return UVD_ERR_NOMEM;
@@ -1325,7 +1326,7 @@ int build_bvh(uvd_scene* s, float4* tri_in, uint32_t** order_out, cudaStream_t s
       UVD_TRY(build_ploc(s, M, left, right, rf, rl, pint, pleaf, ibox, arrive, vals, st));
     }
     {  // the traversal stacks hold 64 entries: refuse deeper trees loudly
-      int* dd = (int*)al.get(sizeof(int));
+      int* dd = (int*)sc.get(sizeof(int));
       if (!dd) { set_error("scene: out of device memory"); return UVD_ERR_NOMEM; }
       UVD_CUDA_TRY(cudaMemsetAsync(dd, 0, sizeof(int), st));
       k_max_depth<<<grid_for(M, 256), 256, 0, st>>>(pleaf, pint, M, dd);
@@ -1333,7 +1334,7 @@ int build_bvh(uvd_scene* s, float4* tri_in, uint32_t** order_out, cudaStream_t s
       int hd = 0;
       UVD_CUDA_TRY(cudaMemcpyAsync(&hd, dd, sizeof(int), cudaMemcpyDeviceToHost, st));
       UVD_CUDA_TRY(cudaStreamSynchronize(st));
-      al.put(dd);
+      sc.release(dd);
       if (hd > 62) {
         set_error("scene: BVH depth %d exceeds the traversal stack (64)", hd);
         return UVD_ERR_INVALID;
@@ -1345,9 +1346,6 @@ int build_bvh(uvd_scene* s, float4* tri_in, uint32_t** order_out, cudaStream_t s
     k_emit<<<grid_for(ni, 256), 256, 0, st>>>(s->tri, M, left, right, rf, rl, ibox, pre, s->nodes, cp);
     note_launch();
     s->root = 0;
-    for (void* p : {(void*)left, (void*)right, (void*)rf, (void*)rl, (void*)pint, (void*)pleaf,
-                    (void*)ibox, (void*)arrive})
-      al.put(p);
   }
   {  // octant copies of the nodes (k_octant_nodes) unless they would take > 1/16 of the
      // device memory or UVD_OCT=0: the traversal then reads the one array (min/max per slab)
@@ -1367,9 +1365,10 @@ int build_bvh(uvd_scene* s, float4* tri_in, uint32_t** order_out, cudaStream_t s
     }
   }
   UVD_CUDA_TRY(cudaGetLastError());
-  al.put(keys);
-  if (order_out) *order_out = vals;
-  else al.put(vals);
+  if (order_out) {
+    sc.keep(vals);  // ownership passes to the caller
+    *order_out = vals;
+  }
   return UVD_OK;
 }
 

@@ -239,6 +239,8 @@ extern "C" int uvd_cubemap_matrix(const uvd_scene* s, const float* lamp_xyz, int
                                   int32_t* hits, void* stream) {
   clear_error();
   if (!s || !lamp_xyz || !lamp || !out) { set_error("uvd_cubemap_matrix: null argument"); return UVD_ERR_INVALID; }
+  DeviceGuard dg(s->alloc.device);
+  NvtxRange nv("uvd_cubemap_matrix");
   if (lamp->samples_per_config < 1 || !(lamp->power_w > 0.0) || face_res < 1 || face_res > 4096) {
     set_error("uvd_cubemap_matrix: need power_w > 0, samples_per_config >= 1, 1 <= face_res <= 4096");
     return UVD_ERR_INVALID;
@@ -254,8 +256,7 @@ extern "C" int uvd_cubemap_matrix(const uvd_scene* s, const float* lamp_xyz, int
       if (cols[c] < 0 || cols[c] >= k_total) { set_error("uvd_cubemap_matrix: column out of range"); return UVD_ERR_INVALID; }
   if (n_cols == 0) return UVD_OK;
   cudaStream_t st = (cudaStream_t)stream;
-  Alloc al = s->alloc;
-  al.stream = st;
+  Scratch al(s->alloc, st);  // released at every exit
   const int R = face_res;
   const int64_t chunk = std::max<int64_t>(1, std::min<int64_t>(n_cols, (int64_t)(256ll << 20) / (8 * std::max<int64_t>(s->N, 1))));
   double* E = (double*)al.get((size_t)R * R * sizeof(double));
@@ -265,9 +266,7 @@ extern "C" int uvd_cubemap_matrix(const uvd_scene* s, const float* lamp_xyz, int
   if (dcols) UVD_CUDA_TRY(cudaMemcpyAsync(dcols, cols, n_cols * sizeof(int64_t), cudaMemcpyHostToDevice, st));
   k_cube_emission<<<(unsigned)(((int64_t)R * R + 255) / 256), 256, 0, st>>>(R, E);
   note_launch();
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const int dev = s->alloc.device, sms = sm_count(dev);
   CubeParams P;
   P.tri = s->tri;
   P.nodes = s->nodes;
@@ -298,6 +297,5 @@ extern "C" int uvd_cubemap_matrix(const uvd_scene* s, const float* lamp_xyz, int
     note_launch(2);
   }
   UVD_CUDA_TRY(cudaGetLastError());
-  for (void* p : {(void*)E, (void*)F, (void*)dcols}) al.put(p);
   return UVD_OK;
 }

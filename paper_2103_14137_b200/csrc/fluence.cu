@@ -13,6 +13,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <climits>
+#include <cmath>
 #include <mutex>
 #include <vector>
 
@@ -251,89 +253,99 @@ __global__ void __launch_bounds__(kStaticThreads) k_static_cols(const float* __r
   if (threadIdx.x < 3) out[3 * c + threadIdx.x] = s[threadIdx.x][0];
 }
 
-}  // namespace uvd
 
-using namespace uvd;
-
-// Grow-only scratch for the nonzero-column list, one buffer per (device,
-// stream) so calls on different streams never share it (a stream-ordered pool
-// allocation at every call stalled up to hundreds of ms on B200).
-struct FluScratch {
-  int dev = -1;
-  cudaStream_t stream = nullptr;
-  size_t bytes = 0;
-  void* p = nullptr;
+// NEXT-4 choice (reading Q24): the column with the largest visible area, ties
+// to the shorter dwell μ_min / min A, then the lower index; and the column
+// covering most area within the budget, ties to the lower index.  One block
+// and a total order: the result is unique and deterministic.
+struct StaticPick {
+  double vis, dwell, cov;
+  int64_t j;
 };
-static std::mutex g_flu_mu;
-static std::vector<FluScratch> g_flu;
-
-static void* flu_scratch(size_t bytes, cudaStream_t st) {
-  int dev = 0;
-  cudaGetDevice(&dev);
-  std::lock_guard<std::mutex> lk(g_flu_mu);
-  for (FluScratch& e : g_flu) {
-    if (e.dev != dev || e.stream != st) continue;
-    if (e.bytes >= bytes) return e.p;
-    cudaStreamSynchronize(st);  // the old buffer may still be read by this stream
-    cudaFree(e.p);
-    size_t b = std::max<size_t>(bytes, (size_t)2 * e.bytes);
-    if (cudaMalloc(&e.p, b) != cudaSuccess) { cudaGetLastError(); e.p = nullptr; e.bytes = 0; return nullptr; }
-    e.bytes = b;
-    return e.p;
+__device__ __forceinline__ bool better_vis(const StaticPick& a, const StaticPick& b) {
+  if (a.vis != b.vis) return a.vis > b.vis;
+  if (a.dwell != b.dwell) return a.dwell < b.dwell;
+  return a.j < b.j;
+}
+__device__ __forceinline__ bool better_cov(const StaticPick& a, const StaticPick& b) {
+  if (a.cov != b.cov) return a.cov > b.cov;
+  return a.j < b.j;
+}
+__global__ void __launch_bounds__(kStaticThreads) k_static_choose(const double* __restrict__ cols3, int64_t k,
+                                                                  double mu_min, double* __restrict__ res) {
+  StaticPick bv{-1.0, INFINITY, -1.0, INT64_MAX}, bc = bv;
+  for (int64_t j = threadIdx.x; j < k; j += kStaticThreads) {
+    const double mn = cols3[3 * j + 1];
+    const StaticPick c{cols3[3 * j], isinf(mn) ? INFINITY : mu_min / mn, cols3[3 * j + 2], j};
+    if (better_vis(c, bv)) bv = c;
+    if (better_cov(c, bc)) bc = c;
   }
-  FluScratch e;
-  e.dev = dev;
-  e.stream = st;
-  e.bytes = std::max<size_t>(bytes, 1 << 20);
-  if (cudaMalloc(&e.p, e.bytes) != cudaSuccess) { cudaGetLastError(); return nullptr; }
-  g_flu.push_back(e);
-  return e.p;
+  __shared__ StaticPick sv[kStaticThreads], sc[kStaticThreads];
+  sv[threadIdx.x] = bv;
+  sc[threadIdx.x] = bc;
+  __syncthreads();
+  for (int o = kStaticThreads / 2; o > 0; o >>= 1) {
+    if (threadIdx.x < o) {
+      if (better_vis(sv[threadIdx.x + o], sv[threadIdx.x])) sv[threadIdx.x] = sv[threadIdx.x + o];
+      if (better_cov(sc[threadIdx.x + o], sc[threadIdx.x])) sc[threadIdx.x] = sc[threadIdx.x + o];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    res[0] = (double)sv[0].j;
+    res[1] = sv[0].dwell;
+    res[2] = (double)sc[0].j;
+  }
 }
 
-extern "C" int uvd_fluence(const uvd_matrix_out* A, int64_t n, int64_t k, int transpose,
-                           const double* x, double* out, void* stream) {
-  clear_error();
-  if (!A || !out || n < 0 || k < 0) { set_error("uvd_fluence: bad argument"); return UVD_ERR_INVALID; }
-  cudaStream_t st0 = (cudaStream_t)stream;
-  if (n == 0) return UVD_OK;
-  if (k == 0) {  // empty shard: μ = 0, g is empty
-    if (!transpose) UVD_CUDA_TRY(cudaMemsetAsync(out, 0, n * sizeof(double), st0));
-    return UVD_OK;
+// The allocator of a matrix's scratch: the caller's (A->allocator) or the
+// ABI's default, cudaMallocAsync / cudaFreeAsync on the call's stream.
+Alloc matrix_alloc(const uvd_matrix_out* A, int dev, cudaStream_t st) {
+  Alloc al;
+  al.device = dev;
+  al.stream = st;
+  if (A && A->allocator && A->allocator->alloc && A->allocator->free) {
+    al.user = *A->allocator;
+    al.has_user = true;
   }
-  if (!x) { set_error("uvd_fluence: null x"); return UVD_ERR_INVALID; }
+  return al;
+}
+
+// Column split of A·t when the row quads alone cannot keep HBM busy.
+static int64_t gemv_split(int64_t n, int64_t k, bool csc, int dev) {
+  const int sms = sm_count(dev);
+  const int64_t quads = (n + 3) / 4;
+  const int64_t rblocks = (quads + kGemvThreads - 1) / kGemvThreads;
+  int64_t split = csc ? 1 : std::max<int64_t>(1, std::min<int64_t>((8 * sms + rblocks - 1) / rblocks, 16));
+  split = std::max<int64_t>(1, std::min<int64_t>(split, k / 8));
+  while (split > 1 && (size_t)split * n * 8 > ((size_t)64 << 20)) --split;
+  return split;
+}
+
+static size_t gemv_part_off(int64_t k) { return ((size_t)k * 12 + 256 + 255) & ~(size_t)255; }
+
+size_t fluence_ws_bytes(int64_t n, int64_t k, bool csc, int dev) {
+  const int64_t split = gemv_split(n, std::max<int64_t>(k, 1), csc, dev);
+  return gemv_part_off(std::max<int64_t>(k, 1)) + (split > 1 ? (size_t)split * n * 8 : 0);
+}
+
+// One fluence product on `st` with a caller-provided workspace `ws` of at least
+// fluence_ws_bytes(n, k) bytes (used by A·t only).  No allocation: uvd_lp_solve
+// captures these launches in a CUDA graph.
+int fluence_run(const uvd_matrix_out* A, int64_t n, int64_t k, int transpose, const double* x, double* out,
+                cudaStream_t st, void* ws) {
   const bool csc = A->format == UVD_CSC;
-  if (csc) {
-    if (!A->colptr || !A->rowidx || !A->values) {
-      set_error("uvd_fluence: CSC A needs colptr, rowidx and values");
-      return UVD_ERR_INVALID;
-    }
-  } else if (A->format != UVD_DENSE_COLMAJOR) {
-    set_error("uvd_fluence: unknown format %d", A->format);
-    return UVD_ERR_INVALID;
-  } else if (!A->values || A->ld < n || A->ld % 4 != 0 || ((uintptr_t)A->values & 15)) {
-    set_error("uvd_fluence: dense A needs 16-B aligned values and ld >= n, ld %% 4 == 0");
-    return UVD_ERR_INVALID;
-  }
-  cudaStream_t st = (cudaStream_t)stream;
-  if (n == 0) return UVD_OK;
   if (!transpose) {
-    if (k == 0) { UVD_CUDA_TRY(cudaMemsetAsync(out, 0, n * sizeof(double), st)); return UVD_OK; }
-    // column split for A·t when the row quads alone cannot keep HBM busy
-    int dev = 0, sms = 148;
+    int dev = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     const int64_t quads = (n + 3) / 4;
     const int64_t rblocks = (quads + kGemvThreads - 1) / kGemvThreads;
-    int64_t split = csc ? 1 : std::max<int64_t>(1, std::min<int64_t>((8 * sms + rblocks - 1) / rblocks, 16));
-    split = std::max<int64_t>(1, std::min<int64_t>(split, k / 8));
-    while (split > 1 && (size_t)split * n * 8 > ((size_t)64 << 20)) --split;
-    const size_t part_off = ((size_t)k * 12 + 256 + 255) & ~(size_t)255;
-    char* sp = (char*)flu_scratch(part_off + (split > 1 ? (size_t)split * n * 8 : 0), st);
-    if (!sp) { set_error("uvd_fluence: out of device memory"); return UVD_ERR_NOMEM; }
+    const int64_t split = gemv_split(n, k, csc, dev);
+    char* sp = (char*)ws;
     double* val = (double*)sp;
     int32_t* idx = (int32_t*)(sp + (size_t)k * 8);
     int32_t* cnt = (int32_t*)(sp + (size_t)k * 12 + 128);
-    double* part = (double*)(sp + part_off);
+    double* part = (double*)(sp + gemv_part_off(k));
     k_nonzero<<<1, 1024, 0, st>>>(x, k, idx, val, cnt);
     note_launch();
     if (csc) {
@@ -345,37 +357,95 @@ extern "C" int uvd_fluence(const uvd_matrix_out* A, int64_t n, int64_t k, int tr
       dim3 grid((unsigned)rblocks, (unsigned)split);
       k_gemv_n<<<grid, kGemvThreads, 0, st>>>(A->values, A->ld, n, idx, val, cnt, chunk, split > 1 ? part : out);
       if (split > 1) {
-        k_gemv_n_reduce<<<(unsigned)std::min<int64_t>((n + 255) / 256, 8 * sms), 256, 0, st>>>(part, (int)split, n, out);
+        k_gemv_n_reduce<<<(unsigned)std::min<int64_t>((n + 255) / 256, 8 * sm_count(dev)), 256, 0, st>>>(
+            part, (int)split, n, out);
         note_launch();
       }
     }
     note_launch();
-    UVD_CUDA_TRY(cudaGetLastError());
   } else {
-    if (k == 0) return UVD_OK;
     if (csc)
       k_csc_t<<<(unsigned)k, kGemvThreads, 0, st>>>(A->colptr, A->rowidx, A->values, x, out);
     else
-      k_gemv_t<<<(unsigned)((k + kGemvTCols - 1) / kGemvTCols), kGemvThreads, 0, st>>>(
-          A->values, A->ld, n, k, x, out);
+      k_gemv_t<<<(unsigned)((k + kGemvTCols - 1) / kGemvTCols), kGemvThreads, 0, st>>>(A->values, A->ld, n, k, x,
+                                                                                      out);
     note_launch();
-    UVD_CUDA_TRY(cudaGetLastError());
+  }
+  UVD_CUDA_TRY(cudaGetLastError());
+  return UVD_OK;
+}
+
+int fluence_check(const uvd_matrix_out* A, int64_t n, int64_t k, const double* x) {
+  if (k > 0 && n > 0 && !x) { set_error("uvd_fluence: null x"); return UVD_ERR_INVALID; }
+  if (A->format == UVD_CSC) {
+    if (!A->colptr || !A->rowidx || !A->values) {
+      set_error("uvd_fluence: CSC A needs colptr, rowidx and values");
+      return UVD_ERR_INVALID;
+    }
+  } else if (A->format != UVD_DENSE_COLMAJOR) {
+    set_error("uvd_fluence: unknown format %d", A->format);
+    return UVD_ERR_INVALID;
+  } else if (!A->values || A->ld < n || A->ld % 4 != 0 || ((uintptr_t)A->values & 15)) {
+    set_error("uvd_fluence: dense A needs 16-B aligned values and ld >= n, ld %% 4 == 0");
+    return UVD_ERR_INVALID;
   }
   return UVD_OK;
+}
+
+}  // namespace uvd
+
+using namespace uvd;
+
+extern "C" int uvd_fluence(const uvd_matrix_out* A, int64_t n, int64_t k, int transpose,
+                           const double* x, double* out, void* stream) {
+  clear_error();
+  if (!A || !out || n < 0 || k < 0) { set_error("uvd_fluence: bad argument"); return UVD_ERR_INVALID; }
+  DeviceGuard dg(pointer_device(out));
+  NvtxRange nv(transpose ? "uvd_fluence(A^T y)" : "uvd_fluence(A t)");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (n == 0) return UVD_OK;
+  if (k == 0) {  // empty shard: μ = 0, g is empty
+    if (!transpose) UVD_CUDA_TRY(cudaMemsetAsync(out, 0, n * sizeof(double), st));
+    return UVD_OK;
+  }
+  UVD_TRY(fluence_check(A, n, k, x));
+  int dev = 0;
+  cudaGetDevice(&dev);
+  void* ws = nullptr;
+  Scratch sc(matrix_alloc(A, dev, st), st);  // returned to the allocator at every exit
+  if (!transpose) {
+    ws = sc.get(fluence_ws_bytes(n, k, A->format == UVD_CSC, dev));
+    if (!ws) { set_error("uvd_fluence: out of device memory"); return UVD_ERR_NOMEM; }
+  }
+  return fluence_run(A, n, k, transpose, x, out, st, ws);
 }
 
 extern "C" int uvd_coverage(const uvd_scene* s, const double* mu, double mu_min,
                             const double* a_rowsum, double out[3], void* stream) {
   clear_error();
   if (!s || !mu || !out) { set_error("uvd_coverage: null argument"); return UVD_ERR_INVALID; }
+  DeviceGuard dg(s->alloc.device);
+  NvtxRange nv("uvd_coverage");
   cudaStream_t st = (cudaStream_t)stream;
-  int dev = 0, sms = 148;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  int nb = (int)std::min<int64_t>((s->N + kCovThreads - 1) / kCovThreads, std::min(2 * sms, kCovBlocksMax));
+  int nb = (int)std::min<int64_t>((s->N + kCovThreads - 1) / kCovThreads, std::min(2 * sm_count(s->alloc.device), kCovBlocksMax));
   nb = std::max(nb, 1);
-  double* part = s->cov_part;
-  double* dout = s->cov_part + 3 * kCovBlocksMax;
+  // partials: one buffer per stream (calls on different streams never share
+  // one; calls on one stream are ordered by it), kept for the scene's lifetime
+  double* part = nullptr;
+  {
+    uvd_scene* ms = const_cast<uvd_scene*>(s);  // internal cache only: results do not depend on it
+    std::lock_guard<std::mutex> lk(ms->cov_mu);
+    for (const auto& c : ms->cov_part)
+      if (c.stream == st) part = c.p;
+    if (!part) {
+      Alloc al = ms->alloc;
+      al.stream = st;
+      part = (double*)al.get((3 * kCovBlocksMax + 3) * sizeof(double));
+      if (!part) { set_error("uvd_coverage: out of device memory"); return UVD_ERR_NOMEM; }
+      ms->cov_part.push_back({st, part});
+    }
+  }
+  double* dout = part + 3 * kCovBlocksMax;
   k_coverage_part<<<nb, kCovThreads, 0, st>>>(mu, s->area, a_rowsum, s->N, mu_min, part);
   note_launch();
   k_coverage_final<<<1, 32, 0, st>>>(part, nb, dout);
@@ -390,7 +460,7 @@ extern "C" int uvd_coverage(const uvd_scene* s, const double* mu, double mu_min,
 }
 
 extern "C" int uvd_static_columns(const uvd_scene* s, const uvd_matrix_out* A, int64_t k, double t_budget,
-                                  double mu_min, double* out, void* stream) {
+                                  double mu_min, double* out, int64_t choice[2], double* dwell, void* stream) {
   clear_error();
   if (!s || !A || !out || k < 0 || !(mu_min > 0.0) || !(t_budget >= 0.0)) {
     set_error("uvd_static_columns: bad argument");
@@ -400,10 +470,28 @@ extern "C" int uvd_static_columns(const uvd_scene* s, const uvd_matrix_out* A, i
     set_error("uvd_static_columns: needs a dense A with ld >= N");
     return UVD_ERR_INVALID;
   }
-  if (k == 0) return UVD_OK;
+  DeviceGuard dg(s->alloc.device);
+  NvtxRange nv("uvd_static_columns");
   cudaStream_t st = (cudaStream_t)stream;
+  if (k == 0) {
+    if (choice) choice[0] = choice[1] = -1;
+    if (dwell) *dwell = INFINITY;
+    return UVD_OK;
+  }
   k_static_cols<<<(unsigned)k, kStaticThreads, 0, st>>>(A->values, A->ld, s->N, s->area, t_budget, mu_min, out);
   note_launch();
+  if (choice || dwell) {
+    Scratch sc(matrix_alloc(A, s->alloc.device, st), st);
+    double* res = (double*)sc.get(3 * sizeof(double));
+    double* h = (double*)host_stage();
+    if (!res || !h) { set_error("uvd_static_columns: out of memory"); return UVD_ERR_NOMEM; }
+    k_static_choose<<<1, kStaticThreads, 0, st>>>(out, k, mu_min, res);
+    note_launch();
+    UVD_CUDA_TRY(cudaMemcpyAsync(h, res, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+    UVD_CUDA_TRY(cudaStreamSynchronize(st));
+    if (choice) { choice[0] = (int64_t)h[0]; choice[1] = (int64_t)h[2]; }
+    if (dwell) *dwell = h[1];
+  }
   UVD_CUDA_TRY(cudaGetLastError());
   return UVD_OK;
 }

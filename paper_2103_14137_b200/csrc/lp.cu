@@ -383,6 +383,9 @@ extern "C" int uvd_lp_solve(const uvd_matrix_out* A, int64_t n, int64_t k, const
     set_error("uvd_lp_solve: need mu_min > 0, t_max > 0 and positive penalties");
     return UVD_ERR_INVALID;
   }
+  DeviceGuard dg(pointer_device(sigma));
+  NvtxRange nvr("uvd_lp_solve");
+  UVD_TRY(fluence_check(A, n, k, sigma));
   cudaStream_t st = (cudaStream_t)stream;
   const double eps = o->eps > 0.0 ? o->eps : 1e-6;
   const int64_t max_iter = o->max_iter > 0 ? o->max_iter : 200000;
@@ -408,14 +411,32 @@ extern "C" int uvd_lp_solve(const uvd_matrix_out* A, int64_t n, int64_t k, const
   // ---- workspace ----
   const int64_t kk = std::max<int64_t>(k, 1);
   const size_t nd = (size_t)6 * kk + (size_t)9 * n + 1 + std::max<size_t>(n, kk) + (size_t)kHpBlocks * 12 + 32;
-  double* ws = nullptr;
-  UVD_CUDA_TRY(cudaMalloc(&ws, nd * sizeof(double) + sizeof(HpScal) + 64));
+  int dev = 0;
+  cudaGetDevice(&dev);
+  // the whole workspace (iterates + the A·t scratch) from the matrix's allocator,
+  // taken once: the iterations allocate nothing (they are captured in a graph)
+  Alloc wal = matrix_alloc(A, dev, st);
+  const size_t ws_main = (nd * sizeof(double) + sizeof(HpScal) + 64 + 255) & ~(size_t)255;
+  const size_t ws_flu = fluence_ws_bytes(n, kk, A->format == UVD_CSC, dev);
+  double* ws = (double*)wal.get(ws_main + ws_flu);
+  if (!ws) { set_error("uvd_lp_solve: out of device memory (workspace)"); return UVD_ERR_NOMEM; }
+  void* fws = (char*)ws + ws_main;
   double* h = nullptr;  // pinned host mirror of check results
   if (cudaMallocHost(&h, 64 * sizeof(double)) != cudaSuccess) {
-    cudaFree(ws);
+    cudaGetLastError();
+    wal.put(ws);
     set_error("uvd_lp_solve: pinned allocation failed");
     return UVD_ERR_NOMEM;
   }
+  // a7 products on this stream with the preallocated scratch (an empty shard
+  // contributes μ = 0 and no g)
+  auto flu = [&](int transpose, const double* x, double* out) -> int {
+    if (k == 0) {
+      if (!transpose) UVD_CUDA_TRY(cudaMemsetAsync(out, 0, n * sizeof(double), st));
+      return UVD_OK;
+    }
+    return fluence_run(A, n, k, transpose, x, out, st, fws);
+  };
   HpVec v;
   double* p = ws;
   v.t = t;
@@ -450,7 +471,7 @@ extern "C" int uvd_lp_solve(const uvd_matrix_out* A, int64_t n, int64_t k, const
     if (exec) cudaGraphExecDestroy(exec);
     if (graph) cudaGraphDestroy(graph);
     cudaStreamSynchronize(st);
-    cudaFree(ws);
+    wal.put(ws);
     cudaFreeHost(h);
     return code;
   };
@@ -477,8 +498,8 @@ extern "C" int uvd_lp_solve(const uvd_matrix_out* A, int64_t n, int64_t k, const
   // ---- setup: preconditioners, norms, ω₀ ----
   k_fill<<<kHpBlocks, kHpThreads, 0, st>>>(ones, std::max(n, kk), 1.0);
   note_launch();
-  LP_TRY(uvd_fluence(A, n, k, 1, ones, v.gT, stream));   // column sums Σ_i A_ik (local columns)
-  LP_TRY(uvd_fluence(A, n, k, 0, ones, v.buf, stream));  // row sums Σ_k A_ik (partial over ranks)
+  LP_TRY(flu(1, ones, v.gT));   // column sums Σ_i A_ik (local columns)
+  LP_TRY(flu(0, ones, v.buf));  // row sums Σ_k A_ik (partial over ranks)
   LP_TRY(allreduce(v.buf, n, 0));
   k_hp_setup_rows<<<kHpBlocks, kHpThreads, 0, st>>>(v, n, v.buf, o->penalty, o->penalty_scalar, eta);
   k_hp_setup_cols<<<kHpBlocks, kHpThreads, 0, st>>>(v, k, eta);
@@ -503,11 +524,11 @@ extern "C" int uvd_lp_solve(const uvd_matrix_out* A, int64_t n, int64_t k, const
   }
 
   // ---- initial point z = (t, 0, 0): A t, Aᵀy ----
-  LP_TRY(uvd_fluence(A, n, k, 0, t, v.buf, stream));
+  LP_TRY(flu(0, t, v.buf));
   LP_TRY(allreduce(v.buf, n, 0));
   k_copy<<<kHpBlocks, kHpThreads, 0, st>>>(v.mu, v.buf, n);
   note_launch();
-  LP_TRY(uvd_fluence(A, n, k, 1, v.y, v.gT, stream));
+  LP_TRY(flu(1, v.y, v.gT));
   k_hp_anchor_rows<<<kHpBlocks, kHpThreads, 0, st>>>(v, n, 0);
   k_hp_anchor_cols<<<kHpBlocks, kHpThreads, 0, st>>>(v, k, 0, omega, rho);
   note_launch(2);
@@ -544,11 +565,11 @@ extern "C" int uvd_lp_solve(const uvd_matrix_out* A, int64_t n, int64_t k, const
       k_hp_primal<<<1, 1024, 0, st>>>(v, k, n, t_max);
       note_launch();
     }
-    UVD_TRY(uvd_fluence(A, n, k, 0, v.tT, v.buf, stream));
+    UVD_TRY(flu(0, v.tT, v.buf));
     UVD_TRY(allreduce(v.buf, n, 0));
     k_hp_dual<<<nb_rows, kHpThreads, 0, st>>>(v, n, mu_min, eta);
     note_launch();
-    UVD_TRY(uvd_fluence(A, n, k, 1, v.yT, v.gTT, stream));
+    UVD_TRY(flu(1, v.yT, v.gTT));
     k_hp_mix_cols<<<kHpBlocks, kHpThreads, 0, st>>>(v, k);
     note_launch();
     return UVD_OK;

@@ -42,6 +42,30 @@ void* host_stage() {
 }
 void note_launch(int n) { g_launches.fetch_add((unsigned long long)n, std::memory_order_relaxed); }
 
+int pointer_device(const void* p) {
+  if (!p) return -1;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return -1;
+  }
+  return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged ? a.device : -1;
+}
+
+int sm_count(int dev) {
+  static int cache[kMaxDevices] = {0};
+  if (dev < 0 || dev >= kMaxDevices) return 148;
+  if (!cache[dev]) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) {
+      cudaGetLastError();
+      v = 148;
+    }
+    cache[dev] = v;
+  }
+  return cache[dev];
+}
+
 void* Alloc::get(size_t bytes) {
   if (bytes == 0) bytes = 16;
   bytes = (bytes + 255) & ~(size_t)255;
@@ -246,16 +270,17 @@ static int create_trimesh(uvd_scene* s, const uvd_scene_desc* d, cudaStream_t st
     return UVD_ERR_INVALID;
   }
   Alloc& al = s->alloc;
+  Scratch sc(al, st);  // this function's temporaries, released at every exit
   const int64_t M = d->n_tris, NV = d->n_vertices;
   s->M = M;
   s->N = M;
-  float* dV = (float*)al.get(NV * 3 * sizeof(float));
-  int32_t* dF = (int32_t*)al.get(M * 3 * sizeof(int32_t));
-  float4* tri_in = (float4*)al.get(3 * M * sizeof(float4));
-  float* cen_in = (float*)al.get(M * 3 * sizeof(float));
-  float* nrm_in = (float*)al.get(M * 3 * sizeof(float));
-  double* area_in = (double*)al.get(M * sizeof(double));
-  unsigned long long* bad = (unsigned long long*)al.get(sizeof(unsigned long long));
+  float* dV = (float*)sc.get(NV * 3 * sizeof(float));
+  int32_t* dF = (int32_t*)sc.get(M * 3 * sizeof(int32_t));
+  float4* tri_in = (float4*)sc.get(3 * M * sizeof(float4));
+  float* cen_in = (float*)sc.get(M * 3 * sizeof(float));
+  float* nrm_in = (float*)sc.get(M * 3 * sizeof(float));
+  double* area_in = (double*)sc.get(M * sizeof(double));
+  unsigned long long* bad = (unsigned long long*)sc.get(sizeof(unsigned long long));
   if (!dV || !dF || !tri_in || !cen_in || !nrm_in || !area_in || !bad) {
     set_error("scene: out of device memory (M=%lld)", (long long)M);
     return UVD_ERR_NOMEM;
@@ -266,8 +291,8 @@ static int create_trimesh(uvd_scene* s, const uvd_scene_desc* d, cudaStream_t st
   UVD_CUDA_TRY(cudaMemsetAsync(bad, 0xff, sizeof(unsigned long long), st));
   {
     int nb = (int)std::min<int64_t>((NV + kBoxThreads - 1) / kBoxThreads, 1184);
-    float* part = (float*)al.get((size_t)nb * 6 * sizeof(float) + 6 * sizeof(float) + 64);
-    unsigned long long* vbad = (unsigned long long*)al.get(sizeof(unsigned long long));
+    float* part = (float*)sc.get((size_t)nb * 6 * sizeof(float) + 6 * sizeof(float) + 64);
+    unsigned long long* vbad = (unsigned long long*)sc.get(sizeof(unsigned long long));
     if (!part || !vbad) { set_error("scene: out of device memory"); return UVD_ERR_NOMEM; }
     float* box = part + 6 * nb;
     UVD_CUDA_TRY(cudaMemsetAsync(vbad, 0xff, sizeof(unsigned long long), st));
@@ -279,8 +304,8 @@ static int create_trimesh(uvd_scene* s, const uvd_scene_desc* d, cudaStream_t st
     UVD_CUDA_TRY(cudaMemcpyAsync(s->bbox, box, 6 * sizeof(float), cudaMemcpyDeviceToHost, st));
     UVD_CUDA_TRY(cudaMemcpyAsync(&h_vbad, vbad, sizeof(h_vbad), cudaMemcpyDeviceToHost, st));
     UVD_CUDA_TRY(cudaStreamSynchronize(st));
-    al.put(part);
-    al.put(vbad);
+    sc.release(part);
+    sc.release(vbad);
     if (h_vbad != ~0ull) {
       set_error("scene: vertex %llu is not finite", h_vbad);
       return UVD_ERR_INVALID;
@@ -297,6 +322,7 @@ static int create_trimesh(uvd_scene* s, const uvd_scene_desc* d, cudaStream_t st
   }
   uint32_t* order = nullptr;
   UVD_TRY(build_bvh(s, tri_in, &order, st));
+  sc.ps.push_back(order);  // build_bvh hands the permutation over
   s->centroid = (float*)al.get(M * 3 * sizeof(float));
   s->normal = (float*)al.get(M * 3 * sizeof(float));
   s->area = (double*)al.get(M * sizeof(double));
@@ -310,9 +336,6 @@ static int create_trimesh(uvd_scene* s, const uvd_scene_desc* d, cudaStream_t st
                                                        s->orig_id);
   note_launch();
   UVD_CUDA_TRY(cudaGetLastError());
-  for (void* p : {(void*)dV, (void*)dF, (void*)tri_in, (void*)cen_in, (void*)nrm_in,
-                  (void*)area_in, (void*)bad, (void*)order})
-    al.put(p);
   return UVD_OK;
 }
 
@@ -382,6 +405,7 @@ static int create_extruded(uvd_scene* s, const uvd_scene_desc* d, cudaStream_t s
   s->poly_xy = (float*)al.get(std::max<size_t>(pxy.size(), 2) * sizeof(float));
   s->poly_off = (int32_t*)al.get(poff.size() * sizeof(int32_t));
   float4* tri_in = (float4*)al.get(3 * s->M * sizeof(float4));
+  s->ptri = tri_in;  // patch-ordered wall triangles (2 per patch) for the area model (NEXT-2)
   s->centroid = (float*)al.get(N * 3 * sizeof(float));
   s->normal = (float*)al.get(N * 3 * sizeof(float));
   s->area = (double*)al.get(N * sizeof(double));
@@ -403,17 +427,23 @@ static int create_extruded(uvd_scene* s, const uvd_scene_desc* d, cudaStream_t s
   UVD_TRY(build_bvh(s, tri_in, nullptr, st));
   // pageable H2D copies above may still read the host vectors: finish first
   UVD_CUDA_TRY(cudaStreamSynchronize(st));
-  s->ptri = tri_in;  // patch-ordered wall triangles (2 per patch) for the area model (NEXT-2)
   return UVD_OK;
 }
 
+// Every stream that used the scene must be done with it before its buffers go
+// back to the allocator (a caching allocator may hand them out at once): the
+// device is synchronised first (uvd.h, uvd_scene_destroy).
 static void free_scene(uvd_scene* s) {
   if (!s) return;
+  DeviceGuard dg(s->alloc.device);
+  cudaDeviceSynchronize();
+  cudaGetLastError();
   Alloc& al = s->alloc;
   for (void* p : {(void*)s->centroid, (void*)s->normal, (void*)s->area, (void*)s->orig_id,
                   (void*)s->tri, (void*)s->nodes, (void*)s->walls, (void*)s->poly_xy,
-                  (void*)s->poly_off, (void*)s->err_flag, (void*)s->cov_part, (void*)s->ptri, (void*)s->onodes})
+                  (void*)s->poly_off, (void*)s->err_flag, (void*)s->ptri, (void*)s->onodes})
     al.put(p);
+  for (auto& c : s->cov_part) al.put(c.p);
   cudaStreamSynchronize(al.stream);
   delete s;
 }
@@ -431,7 +461,11 @@ extern "C" int uvd_scene_create(const uvd_scene_desc* desc, int device, void* st
     set_error("uvd_scene_create: unknown kind %d", desc->kind);
     return UVD_ERR_INVALID;
   }
-  UVD_CUDA_TRY(cudaSetDevice(device));
+  NvtxRange nv("uvd_scene_create");
+  int ndev = 0;
+  UVD_CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) { set_error("uvd_scene_create: no device %d", device); return UVD_ERR_INVALID; }
+  DeviceGuard dg(device);  // the caller's current device is restored on return
   uvd_scene* s = new uvd_scene();
   s->kind = desc->kind;
   s->alloc.device = device;
@@ -442,12 +476,9 @@ extern "C" int uvd_scene_create(const uvd_scene_desc* desc, int device, void* st
   }
   cudaStream_t st = (cudaStream_t)stream;
   int rc = desc->kind == UVD_SCENE_TRIMESH ? create_trimesh(s, desc, st) : create_extruded(s, desc, st);
-  if (rc == UVD_OK) {
-    s->cov_part = (double*)s->alloc.get((3 * kCovBlocksMax + 3) * sizeof(double));
-    if (!s->cov_part || !host_stage()) {
-      set_error("scene: out of memory (scratch)");
-      rc = UVD_ERR_NOMEM;
-    }
+  if (rc == UVD_OK && !host_stage()) {
+    set_error("scene: out of pinned host memory (staging)");
+    rc = UVD_ERR_NOMEM;
   }
   if (rc == UVD_OK) {
     s->err_flag = (int*)s->alloc.get(sizeof(int));
@@ -489,6 +520,8 @@ extern "C" int uvd_scene_patches(const uvd_scene* s, float* centroid, float* nor
                                  int64_t* orig_id, void* stream) {
   clear_error();
   if (!s) { set_error("uvd_scene_patches: null scene"); return UVD_ERR_INVALID; }
+  DeviceGuard dg(s->alloc.device);
+  NvtxRange nv("uvd_scene_patches");
   cudaStream_t st = (cudaStream_t)stream;
   if (centroid) UVD_CUDA_TRY(cudaMemcpyAsync(centroid, s->centroid, s->N * 3 * sizeof(float), cudaMemcpyDeviceToDevice, st));
   if (normal) UVD_CUDA_TRY(cudaMemcpyAsync(normal, s->normal, s->N * 3 * sizeof(float), cudaMemcpyDeviceToDevice, st));
@@ -499,17 +532,26 @@ extern "C" int uvd_scene_patches(const uvd_scene* s, float* centroid, float* nor
 
 extern "C" void uvd_scene_destroy(uvd_scene* s) { free_scene(s); }
 
+namespace uvd {
+__global__ void k_take_flag(int* flag, int* out) { *out = atomicExch(flag, 0); }
+}  // namespace uvd
+
 extern "C" int uvd_sync_status(const uvd_scene* s, void* stream) {
   clear_error();
   if (!s) { set_error("uvd_sync_status: null scene"); return UVD_ERR_INVALID; }
+  DeviceGuard dg(s->alloc.device);
+  NvtxRange nv("uvd_sync_status");
   cudaStream_t st = (cudaStream_t)stream;
-  int* hflag = (int*)host_stage();
-  UVD_CUDA_TRY(cudaMemcpyAsync(hflag, s->err_flag, sizeof(int), cudaMemcpyDeviceToHost, st));
-  UVD_CUDA_TRY(cudaStreamSynchronize(st));
+  int* hflag = (int*)host_stage();  // pinned: device-visible under unified addressing
+  if (!hflag) { set_error("uvd_sync_status: out of pinned host memory"); return UVD_ERR_NOMEM; }
+  // read and clear in one atomic: an error raised meanwhile by a kernel on
+  // another stream stays in the flag for the next call instead of being lost
+  k_take_flag<<<1, 1, 0, st>>>(s->err_flag, hflag);
+  note_launch();
   UVD_CUDA_TRY(cudaGetLastError());
-  const int flag = *hflag;
+  UVD_CUDA_TRY(cudaStreamSynchronize(st));
+  const int flag = *(volatile int*)hflag;
   if (flag) {
-    UVD_CUDA_TRY(cudaMemsetAsync(s->err_flag, 0, sizeof(int), st));
     if (flag == 2) {  // cannot happen: scene creation refuses trees deeper than the stacks
       set_error("traversal stack overflow (BVH deeper than 64)");
       return UVD_ERR_CUDA;
@@ -528,6 +570,8 @@ extern "C" int uvd_scene_bvh(const uvd_scene* s, void* nodes, float* tri, int64_
                              void* stream) {
   clear_error();
   if (!s) { set_error("uvd_scene_bvh: null scene"); return UVD_ERR_INVALID; }
+  DeviceGuard dg(s->alloc.device);
+  NvtxRange nv("uvd_scene_bvh");
   const int64_t nn = std::max<int64_t>(s->M - 1, 1);
   if (n_nodes) *n_nodes = nn;
   if (root) *root = s->root;

@@ -4,9 +4,13 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <nvtx3/nvToolsExt.h>
+
+#include <algorithm>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
+#include <mutex>
 #include <vector>
 
 #include "../../include/uvd.h"
@@ -78,6 +82,53 @@ struct Alloc {
   void put(void* p);
 };
 
+// Call-scoped device buffers: every buffer taken through get() is returned
+// (stream-ordered on the call's stream) at every exit of the call, error
+// returns included; release(p) hands one back early, keep(p) moves ownership out.
+struct Scratch {
+  Alloc al;
+  std::vector<void*> ps;
+  Scratch(const Alloc& a, cudaStream_t st) : al(a) { al.stream = st; }
+  ~Scratch() { for (void* p : ps) al.put(p); }
+  Scratch(const Scratch&) = delete;
+  Scratch& operator=(const Scratch&) = delete;
+  void* get(size_t bytes) {
+    void* p = al.get(bytes);
+    if (p) ps.push_back(p);
+    return p;
+  }
+  void keep(void* p) { ps.erase(std::remove(ps.begin(), ps.end(), p), ps.end()); }
+  void release(void* p) {
+    keep(p);
+    al.put(p);
+  }
+};
+
+// Every entry point runs on the device its scene (or its buffers) lives on and
+// restores the caller's current device on return.
+struct DeviceGuard {
+  int prev = -1, dev = -1;
+  explicit DeviceGuard(int d) : dev(d) {
+    if (cudaGetDevice(&prev) != cudaSuccess) { cudaGetLastError(); prev = -1; }
+    if (d >= 0 && prev != d) cudaSetDevice(d);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0 && prev != dev) cudaSetDevice(prev);
+  }
+};
+// device of a device pointer (-1 if unknown: the current device stays)
+int pointer_device(const void* p);
+
+// NVTX range around an entry point: visible in ncu --nvtx / nsys
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
+
+// per-device cached launch geometry (SM count; occupancy-derived grids)
+constexpr int kMaxDevices = 64;
+int sm_count(int dev);
+
 // ------------------------------------------------------------------- scene --
 struct Wall {  // 2.5D wall (host-prepared from the polygon description)
   float e0x, e0y, e1x, e1y;
@@ -118,8 +169,11 @@ struct uvd_scene {
   float wall_height = 0.f;
   // in-kernel error flag (device int)
   int* err_flag = nullptr;
-  // small preallocated scratch: coverage partials (device)
-  double* cov_part = nullptr;  // 3 * kCovBlocksMax + 3 doubles
+  // coverage partials, one buffer per stream the scene's coverage ran on (a
+  // call on another stream never shares one); guarded by cov_mu
+  struct CovScratch { cudaStream_t stream; double* p; };
+  std::vector<CovScratch> cov_part;  // each 3 * kCovBlocksMax + 3 doubles
+  std::mutex cov_mu;
 };
 
 namespace uvd {
@@ -129,4 +183,10 @@ void* host_stage();
 // launchers implemented in the .cu files
 int build_bvh(uvd_scene* s, float4* tri_in, uint32_t** order_out, cudaStream_t st);
 int sort_pairs_u64(uint64_t* keys, uint32_t* vals, int64_t n, Alloc& al, cudaStream_t st);
+// fluence.cu: the a7 products without allocation (uvd_lp_solve graphs them)
+Alloc matrix_alloc(const uvd_matrix_out* A, int dev, cudaStream_t st);
+size_t fluence_ws_bytes(int64_t n, int64_t k, bool csc, int dev);
+int fluence_check(const uvd_matrix_out* A, int64_t n, int64_t k, const double* x);
+int fluence_run(const uvd_matrix_out* A, int64_t n, int64_t k, int transpose, const double* x, double* out,
+                cudaStream_t st, void* ws);
 }  // namespace uvd

@@ -252,6 +252,8 @@ extern "C" int uvd_vantage_sample(const uvd_scene* s, const uvd_vantage_opts* o,
                                   int64_t* raw_index, int64_t cap, int64_t* out_k, void* stream) {
   clear_error();
   if (!s || !o || !out_k) { set_error("uvd_vantage_sample: null argument"); return UVD_ERR_INVALID; }
+  DeviceGuard dg(s->alloc.device);
+  NvtxRange nv("uvd_vantage_sample");
   *out_k = 0;
   if (!(o->spacing > 0.f) || !(o->clearance >= 0.f) || !std::isfinite(o->spacing)) {
     set_error("uvd_vantage_sample: spacing must be > 0 and clearance >= 0");
@@ -266,8 +268,7 @@ extern "C" int uvd_vantage_sample(const uvd_scene* s, const uvd_vantage_opts* o,
   int L = o->robot == UVD_ROBOT_TOWER ? o->lamp_samples : 1;
   if (L < 1) { set_error("uvd_vantage_sample: TOWER needs lamp_samples >= 1"); return UVD_ERR_INVALID; }
   cudaStream_t st = (cudaStream_t)stream;
-  Alloc al = s->alloc;
-  al.stream = st;
+  Scratch al(s->alloc, st);  // released at every exit
   Grid g;
   const float* bb = s->bbox;
   if (ext) g = make_grid(s->bounds[0], s->bounds[2], s->bounds[1], s->bounds[3], 0, 0, o->spacing, false);
@@ -334,7 +335,6 @@ extern "C" int uvd_vantage_sample(const uvd_scene* s, const uvd_vantage_opts* o,
     note_launch();
     UVD_CUDA_TRY(cudaGetLastError());
   }
-  for (void* p : {(void*)pts, (void*)flag, (void*)pos, (void*)dtot, (void*)bpts, (void*)bflag}) al.put(p);
   UVD_CUDA_TRY(cudaStreamSynchronize(st));
   return rc;
 }

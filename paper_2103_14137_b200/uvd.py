@@ -65,7 +65,9 @@ class _Lamp(C.Structure):
 class _MatrixOut(C.Structure):
     _fields_ = [("format", C.c_int32), ("ld", C.c_int64), ("values", C.c_void_p),
                 ("colptr", C.c_void_p), ("rowidx", C.c_void_p), ("nnz_cap", C.c_int64),
-                ("vis_bits", C.c_void_p), ("col_sumsq", C.c_void_p), ("counters", C.c_void_p)]
+                ("vis_bits", C.c_void_p), ("col_sumsq", C.c_void_p), ("counters", C.c_void_p),
+                ("fixup_list", C.c_void_p), ("fixup_cap", C.c_int64), ("fixup_count", C.c_void_p),
+                ("allocator", C.POINTER(_Allocator))]
 
 
 _ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int64, C.c_int, C.c_void_p, C.c_void_p)
@@ -118,7 +120,7 @@ def lib():
                                          C.POINTER(_Lamp), C.c_int32, C.POINTER(_MatrixOut), C.c_void_p,
                                          C.c_void_p]
         L.uvd_static_columns.argtypes = [C.c_void_p, C.POINTER(_MatrixOut), C.c_int64, C.c_double, C.c_double,
-                                         C.c_void_p, C.c_void_p]
+                                         C.c_void_p, C.POINTER(C.c_int64), C.POINTER(C.c_double), C.c_void_p]
         L.uvd_lp_solve.argtypes = [C.POINTER(_MatrixOut), C.c_int64, C.c_int64, C.POINTER(_LpOpts),
                                    C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(_LpResult), C.c_void_p]
         L.uvd_last_error.restype = C.c_char_p
@@ -163,6 +165,14 @@ def _torch_free(ptr, device, stream, ctx):
 
 
 _TORCH_ALLOCATOR = _Allocator(_torch_alloc, _torch_free, None)
+
+
+def _new_desc(fmt) -> _MatrixOut:
+    """A uvd_matrix_out whose call scratch comes from torch's caching allocator."""
+    m = _MatrixOut()
+    m.format = fmt
+    m.allocator = C.pointer(_TORCH_ALLOCATOR)
+    return m
 
 
 def _require_cuda():
@@ -292,12 +302,15 @@ class Scene:
 
     def irradiance(self, lamps: torch.Tensor, cols=None, power_w: float = 80.0, vis_bits: bool = False,
                    col_sumsq: bool = False, counters: bool = False, out: torch.Tensor | None = None,
-                   stream=None, area_subdiv: int | None = None) -> dict:
+                   stream=None, area_subdiv: int | None = None, fixups: int = 0) -> dict:
         """uvd_irradiance_matrix (dense column-major).  lamps: (K_total, L, 3)
         fp32 on the device; cols: None or a host sequence of global column ids.
         Returns dict(A=(n_cols, ld) fp32, [vis_bits (n_cols, L, words) int32],
         [col_sumsq (n_cols,) fp64], [counters (6,) int64: rays, box tests,
-        triangle tests, node fetches, entries re-traced in fp64, 0 — instrumented kernel])."""
+        triangle tests, node fetches, entries re-traced in fp64, 0 — instrumented kernel],
+        [fixups (m,) int64 (local column << 32 | row) of the entries the fp32 pass
+        left undecided (re-traced exactly), up to `fixups` of them, and
+        fixup_count (the total)])."""
         assert lamps.is_cuda and lamps.dtype == torch.float32 and lamps.is_contiguous()
         K, L = lamps.shape[0], lamps.shape[1]
         ccols = None
@@ -311,8 +324,7 @@ class Scene:
         A = out if out is not None else torch.empty((n_cols, ld), dtype=torch.float32, device=dev)
         assert A.shape == (n_cols, ld) and A.dtype == torch.float32 and A.is_contiguous()
         res = dict(A=A)
-        m = _MatrixOut()
-        m.format = DENSE_COLMAJOR
+        m = _new_desc(DENSE_COLMAJOR)
         m.ld = ld
         m.values = A.data_ptr()
         if vis_bits:
@@ -327,6 +339,11 @@ class Scene:
             ct = torch.zeros(6, dtype=torch.int64, device=dev)
             m.counters = ct.data_ptr()
             res["counters"] = ct
+        if fixups:
+            fl = torch.empty(int(fixups), dtype=torch.int64, device=dev)
+            fc = torch.zeros(1, dtype=torch.int64, device=dev)
+            m.fixup_list, m.fixup_cap, m.fixup_count = fl.data_ptr(), int(fixups), fc.data_ptr()
+            res["_fixups"] = (fl, fc)
         lamp = _Lamp(float(power_w), int(L), 0 if area_subdiv is None else 1,
                      0 if area_subdiv is None else int(area_subdiv))
         _check(lib().uvd_irradiance_matrix(
@@ -334,6 +351,11 @@ class Scene:
             ccols.ctypes.data_as(C.c_void_p) if ccols is not None else None, n_cols,
             C.byref(lamp), C.byref(m), _stream(stream)))
         res["_desc"] = m
+        if fixups:
+            fl, fc = res.pop("_fixups")
+            n_fix = int(fc.item())
+            res["fixups"] = fl[:min(n_fix, int(fixups))]
+            res["fixup_count"] = n_fix
         return res
 
     def irradiance_csc(self, lamps: torch.Tensor, cols=None, power_w: float = 80.0,
@@ -349,8 +371,7 @@ class Scene:
         dev = lamps.device
         colptr = torch.empty(n_cols + 1, dtype=torch.int64, device=dev)
         res = dict(colptr=colptr)
-        m = _MatrixOut()
-        m.format = CSC
+        m = _new_desc(CSC)
         m.colptr = colptr.data_ptr()
         if vis_bits:
             vb = torch.empty((n_cols, L, (self.N + 31) // 32), dtype=torch.int32, device=dev)
@@ -416,16 +437,13 @@ class Scene:
         k = A.shape[0]
         out = torch.empty((k, 3), dtype=torch.float64, device=A.device)
         m = _dense_desc(A)
+        choice = (C.c_int64 * 2)()
+        dwell = C.c_double()
         _check(lib().uvd_static_columns(self.handle, C.byref(m), k, float(t_budget), float(mu_min),
-                                        _ptr(out), _stream(stream)))
+                                        _ptr(out), choice, C.byref(dwell), _stream(stream)))
         o = out.cpu().numpy()
-        vis, mn, cov = o[:, 0], o[:, 1], o[:, 2]
-        dwell = np.where(np.isfinite(mn), mu_min / np.where(np.isfinite(mn), mn, 1.0), np.inf)
-        order = np.lexsort((np.arange(k), dwell, -vis))
-        j = int(order[0]) if k else -1
-        return {"visible_area": vis, "min_irradiance": mn, "covered_at_budget": cov, "column": j,
-                "dwell_s": float(dwell[j]) if k else float("inf"),
-                "best_budget_column": int(np.lexsort((np.arange(k), -cov))[0]) if k else -1}
+        return {"visible_area": o[:, 0], "min_irradiance": o[:, 1], "covered_at_budget": o[:, 2],
+                "column": int(choice[0]), "dwell_s": float(dwell.value), "best_budget_column": int(choice[1])}
 
     def coverage(self, mu: torch.Tensor, mu_min: float = 280.0, rowsum: torch.Tensor | None = None,
                  stream=None) -> np.ndarray:
@@ -435,8 +453,7 @@ class Scene:
 
 
 def _dense_desc(A: torch.Tensor) -> _MatrixOut:
-    m = _MatrixOut()
-    m.format = DENSE_COLMAJOR
+    m = _new_desc(DENSE_COLMAJOR)
     m.ld = A.shape[1]
     m.values = A.data_ptr()
     return m
@@ -462,8 +479,7 @@ def fluence_csc(csc: dict, n: int, x: torch.Tensor, transpose: bool = False,
     assert x.dtype == torch.float64 and x.is_cuda and x.is_contiguous()
     if out is None:
         out = torch.empty(k if transpose else n, dtype=torch.float64, device=x.device)
-    m = _MatrixOut()
-    m.format = CSC
+    m = _new_desc(CSC)
     m.colptr = csc["colptr"].data_ptr()
     m.rowidx = csc["rowidx"].data_ptr() if csc["nnz"] else csc["colptr"].data_ptr()
     m.values = csc["values"].data_ptr() if csc["nnz"] else csc["colptr"].data_ptr()
@@ -500,8 +516,7 @@ def lp_solve(A, n: int, mu_min: float = 280.0, t_max: float = 1800.0, penalty=No
     allreduce: or any callable(tensor, op) reducing a CUDA fp64 tensor in place
     across the column shards (op "sum" or "max")."""
     if isinstance(A, dict):
-        m = _MatrixOut()
-        m.format = CSC
+        m = _new_desc(CSC)
         m.colptr = A["colptr"].data_ptr()
         m.rowidx = A["rowidx"].data_ptr() if A["nnz"] else A["colptr"].data_ptr()
         m.values = A["values"].data_ptr() if A["nnz"] else A["colptr"].data_ptr()

@@ -11,7 +11,8 @@ consistently wound solids:
 * a nurse counter, a sink unit, a door panel and window frames on the walls.
 
 Every furniture solid is closed with OUTWARD winding; each item (group of
-solids) is jittered by ±2 cm and ±3° yaw (seeded) so grid-aligned rays do not
+solids) is jittered by ±2 cm and ±3° yaw, and its height scaled by 1 ± 1.5 % (wall
+fittings shifted ±1 cm; seeded) so grid-aligned rays and lamp planes do not
 systematically hit edges.  Faces are tessellated uniformly into
 cells of edge ≤ e, two triangles per cell, giving ≈ 2·A_surf/e² triangles.
 
@@ -102,11 +103,11 @@ class _Mesh:
         return s
 
 
-def _xform(yaw: float, tx: float, ty: float) -> np.ndarray:
+def _xform(yaw: float, tx: float, ty: float, sz: float = 1.0, tz: float = 0.0) -> np.ndarray:
     c, s = math.cos(yaw), math.sin(yaw)
     M = np.eye(4)
-    M[:3, :3] = [[c, -s, 0], [s, c, 0], [0, 0, 1]]
-    M[:3, 3] = [tx, ty, 0.0]
+    M[:3, :3] = [[c, -s, 0], [s, c, 0], [0, 0, sz]]
+    M[:3, 3] = [tx, ty, tz]
     return M
 
 
@@ -114,6 +115,15 @@ def ward(seed: int = 0, n_bays: int = 3, e: float = 0.06, width: float = 7.0,
          height: float = 3.0) -> dict:
     """Ward with `n_bays` bed bays per long wall (3 bays → 10 m × 7 m × 3 m, 6 beds)."""
     rng = np.random.Generator(np.random.PCG64(seed))
+    # heights: a second stream (the xy / yaw jitter above is unchanged by it);
+    # item heights scaled by 1 ± 1.5 % and wall fittings shifted by ± 1 cm, so
+    # no horizontal face sits exactly in a lamp-grid plane (e.g. a 0.8 m
+    # cabinet top and the Armbot grid's z = 0.8 m plane: cos θ = 0 exactly,
+    # a degenerate pair of SURVEY §8c for every such patch and lamp)
+    rng_h = np.random.Generator(np.random.PCG64(seed + 1000))
+
+    def hz():
+        return rng_h.uniform(0.985, 1.015)
     bay = 10.0 / 3.0
     length = bay * n_bays
     m = _Mesh()
@@ -121,6 +131,9 @@ def ward(seed: int = 0, n_bays: int = 3, e: float = 0.06, width: float = 7.0,
 
     def jit():
         return (math.radians(rng.uniform(-3, 3)), rng.uniform(-0.02, 0.02), rng.uniform(-0.02, 0.02))
+
+    def X(yaw, tx, ty):  # placement with the height jitter
+        return _xform(yaw, tx, ty, hz())
 
     for side in (0, 1):
         for b in range(n_bays):
@@ -130,43 +143,44 @@ def ward(seed: int = 0, n_bays: int = 3, e: float = 0.06, width: float = 7.0,
             base_y = 0.15 if not flip else width - 0.15
             yaw0 = 0.0 if not flip else math.pi
             dyaw, dx, dy = jit()
-            M = _xform(yaw0 + dyaw, cx + dx, base_y + dy)
+            M = X(yaw0 + dyaw, cx + dx, base_y + dy)
             m.box((-0.45, 0.05, 0.0), (0.45, 2.05, 0.5), e, M)          # bed frame
             m.box((-0.425, 0.075, 0.5), (0.425, 2.025, 0.65), e, M)     # mattress
             m.box((-0.45, 0.0, 0.0), (0.45, 0.05, 1.0), e, M)           # headboard
             dyaw, dx, dy = jit()
-            M = _xform(yaw0 + dyaw, cx + dx, base_y + dy)
+            M = X(yaw0 + dyaw, cx + dx, base_y + dy)
             m.box((0.6, 0.0, 0.0), (1.1, 0.45, 0.8), e, M)              # bedside cabinet
             dyaw, dx, dy = jit()
-            M = _xform(yaw0 + dyaw, cx + dx, base_y + dy)
+            M = X(yaw0 + dyaw, cx + dx, base_y + dy)
             sx, sy = 0.75, 1.0                                          # chair
             m.box((sx, sy, 0.45), (sx + 0.45, sy + 0.45, 0.5), e, M)    # seat
             for lx, ly in ((0, 0), (0.41, 0), (0, 0.41), (0.41, 0.41)):
                 m.box((sx + lx, sy + ly, 0.0), (sx + lx + 0.04, sy + ly + 0.04, 0.45), e, M)
             m.box((sx + 0.41, sy, 0.5), (sx + 0.45, sy + 0.45, 0.95), e, M)  # back
             dyaw, dx, dy = jit()
-            M = _xform(yaw0 + dyaw, cx + dx, base_y + dy)
+            M = X(yaw0 + dyaw, cx + dx, base_y + dy)
             tx, ty = -1.2, 1.6                                          # over-bed table
             m.box((tx, ty, 0.0), (tx + 0.6, ty + 0.4, 0.03), e, M)
             m.box((tx + 0.05, ty + 0.175, 0.03), (tx + 0.1, ty + 0.225, 0.9), e, M)
             m.box((tx, ty, 0.9), (tx + 0.8, ty + 0.4, 0.93), e, M)
             dyaw, dx, dy = jit()
-            M = _xform(yaw0 + dyaw, cx + dx, base_y + dy)
+            M = X(yaw0 + dyaw, cx + dx, base_y + dy)
             m.cylinder((-0.7, 0.3), 0.02, 0.0, 1.8, e, M)              # IV pole
     # nurse counter and sink unit in the middle / against the x=0 wall
     for b in range(max(1, n_bays // 3)):
         dyaw, dx, dy = jit()
         cx0 = length - 2.0 - b * 10.0
-        M = _xform(dyaw, cx0 + dx, width / 2 + dy)
+        M = X(dyaw, cx0 + dx, width / 2 + dy)
         m.box((-0.75, -0.35, 0.0), (0.75, 0.35, 1.1), e, M)
         dyaw, dx, dy = jit()
-        M = _xform(dyaw, 0.4 + b * 10.0 + dx, width / 2 + dy)
+        M = X(dyaw, 0.4 + b * 10.0 + dx, width / 2 + dy)
         m.box((-0.3, -0.5, 0.0), (0.3, 0.5, 0.9), e, M)
     # door panel on the x=length wall, window frames on the y=width wall
-    m.box((length - 0.04, width / 2 - 0.6, 0.0), (length - 0.001, width / 2 + 0.6, 2.1), e, np.eye(4))
+    m.box((length - 0.04, width / 2 - 0.6, 0.0), (length - 0.001, width / 2 + 0.6, 2.1), e, _xform(0, 0, 0, hz()))
     for b in range(n_bays):
         cx = bay * (b + 0.5)
-        m.box((cx - 0.6, width - 0.031, 1.2), (cx + 0.6, width - 0.001, 2.3), e, np.eye(4))
+        m.box((cx - 0.6, width - 0.031, 1.2), (cx + 0.6, width - 0.001, 2.3), e,
+              _xform(0, 0, 0, 1.0, rng_h.uniform(-0.01, 0.01)))
     V = np.concatenate(m.V).astype(np.float32)
     F = np.concatenate(m.F).astype(np.int32)
     solid = np.concatenate(m.solid)

@@ -189,7 +189,10 @@ def test_trimesh_patches_closed_solids(orc):
     L = 10.0 / 3.0
     assert abs(vol[0] + L * 7.0 * 3.0) < 1e-4 * L * 21   # shell: inward normals
     assert (vol[1:] > 0).all()
-    assert abs(vol[1] - 0.9 * 2.0 * 0.5) < 1e-4           # bed frame volume
+    # bed frame 0.9 m x 2.0 m, its height jittered by the generator (yaw leaves z alone)
+    zf = w["vertices"][np.unique(w["tris"][w["solid"] == 1]), 2].astype(np.float64)
+    assert abs(zf.max() - zf.min() - 0.5) < 0.5 * 0.016
+    assert abs(vol[1] - 0.9 * 2.0 * (zf.max() - zf.min())) < 1e-4   # bed frame volume
 
 
 def test_trimesh_rejects_degenerate(orc):

@@ -1,23 +1,23 @@
-"""NEXT-4 resolution sweeps (PAPER App. II) on the GPU: the
-paper's two 2.5D experiments over the 25 random rooms and its 3D grid sweep,
-reusing the hot path (scene → vantage → A) and NEXT-1 (the LP).
+"""NEXT-4 resolution sweeps as throughput-scaling curves (PAPER App. II axes,
+P:495–522): assembly time and entries/s of the hot path
+(scene → vantage → A) as the paper's resolutions vary.  Only the throughput
+axis is reproduced — the paper's dwell/coverage results need its planner and
+asset and are out of scope.
 
-* env-res: wall patch resolution 1/2 … 1/32 m at a 0.1 m grid;
-* grid:    vantage grid 1/2 … 1/32 m at the 1/8 m "balanced" patch resolution;
-* 3d:      Floatbot grid spacing 1000 … 250 mm on the C4 ward, 30-minute budget.
+* env-res: wall patch resolution 1/2 … 1/32 m at a 0.1 m grid on the random
+  rooms;
+* grid:    vantage grid 1/2 … 1/32 m at the 1/8 m patch resolution;
+* 3d:      Floatbot grid spacing 1000 … 250 mm on the C4 ward.
 
-For each point: assembly time and entries/s (the throughput curve), the LP's
-total dwell for full disinfection of the visible patches (Eq. 9 with a loose
-budget) or the 30-minute coverage, normalised per room by the coarsest
-resolution as the paper plots them (mean ± std over rooms).
+Each point: best of 3 CUDA-event timings of uvd_irradiance_matrix after a
+warm-up (the BVH prebuilt), N, K, entries/s.
 
-usage: python tools/sweep.py [--rooms 25] [--no-3d] [--out profiles/sweep_r01.json]
+usage: python tools/sweep.py [--rooms 25] [--no-3d] [--out profiles/sweep_r02.json]
 """
 import argparse
 import json
 import os
 import sys
-import time
 
 import numpy as np
 import torch
@@ -29,79 +29,57 @@ from paper_2103_14137_b200 import uvd  # noqa: E402
 from synth import configs, rooms  # noqa: E402
 
 
-def run_one(scene, vopts, t_max, eps):
+def run_one(scene, vopts, reps=3):
     sc = uvd.Scene(scene)
     lam, _ = sc.vantage(vopts)
     K = int(lam.shape[0])
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    a = sc.irradiance(lam, col_sumsq=True)
-    e1.record()
+    A = torch.empty((K, sc.ld()), dtype=torch.float32, device="cuda")
+    sc.irradiance(lam, out=A)
+    best = float("inf")
+    for _ in range(reps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        sc.irradiance(lam, out=A)
+        e1.record()
+        torch.cuda.synchronize()
+        best = min(best, e0.elapsed_time(e1))
     sc.sync_status()
-    ms = e0.elapsed_time(e1)
-    A = a["A"]
-    p = 10.0 * float(np.sqrt(a["col_sumsq"].sum().item()))
-    rowsum = uvd.fluence(A, sc.N, torch.ones(K, dtype=torch.float64, device="cuda"))
-    t0 = time.perf_counter()
-    r = uvd.lp_solve(A, sc.N, penalty=p, t_max=t_max, eps=eps, max_iter=400000)
-    lp_s = time.perf_counter() - t0
-    mu = uvd.fluence(A, sc.N, r["t"])
-    cov = sc.coverage(mu, configs.MU_MIN, rowsum)
-    return {"N": sc.N, "K": K, "assemble_ms": ms, "entries_per_s": sc.N * K / (ms / 1e3),
-            "dwell_s": r["sum_t"], "nnz_t": int((r["t"] > 0).sum().item()), "lp_status": r["status"],
-            "lp_iterations": r["iterations"], "lp_s": lp_s,
-            "coverage_total": cov[0] / cov[1], "coverage_visible": cov[0] / cov[2]}
+    n = sc.N
+    sc.close()
+    return {"N": n, "K": K, "assemble_ms": best, "entries_per_s": n * K / (best / 1e3)}
 
 
-def summarise(rows_by_level, key):
-    """per-room normalisation by the first (coarsest) level, then mean/std per level"""
-    levels = list(rows_by_level)
-    base = np.array([r[key] for r in rows_by_level[levels[0]]])
-    out = {}
-    for lv in levels:
-        v = np.array([r[key] for r in rows_by_level[lv]]) / base
-        out[str(lv)] = {"mean": float(v.mean()), "std": float(v.std())}
-    return out
+def summary(rows):
+    return {"N": int(np.median([r["N"] for r in rows])), "K": int(np.median([r["K"] for r in rows])),
+            "assemble_ms_median": float(np.median([r["assemble_ms"] for r in rows])),
+            "entries_per_s_median": float(np.median([r["entries_per_s"] for r in rows]))}
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--rooms", type=int, default=25)
     ap.add_argument("--no-3d", action="store_true")
-    ap.add_argument("--eps", type=float, default=1e-7)
     ap.add_argument("--out", default=None)
     a = ap.parse_args()
-    out = {"gpu": torch.cuda.get_device_name(0), "rooms": a.rooms}
-    loose = 1e6  # "time until full disinfection": the budget does not bind (P:293)
-    res_levels = [0.5, 0.25, 0.125, 0.0625, 0.03125]
-    env = {lv: [] for lv in res_levels}
-    for seed in range(a.rooms):
-        for lv in res_levels:
-            sc = rooms.random_room(seed, 4.0, patch_res=lv)
-            env[lv].append(run_one(sc, configs.vopts(configs.DISC2D, 0.1, 0.15, lamp_z=1.0), loose, a.eps))
-        print("env-res room", seed, [round(env[lv][-1]["dwell_s"], 1) for lv in res_levels], flush=True)
-    out["env_res"] = {"levels_m": res_levels, "grid_m": 0.1,
-                      "dwell_norm": summarise(env, "dwell_s"),
-                      "raw": {str(k): v for k, v in env.items()}}
-    grid_levels = [0.5, 0.25, 0.125, 0.0625, 0.03125]
-    grid = {lv: [] for lv in grid_levels}
-    for seed in range(a.rooms):
-        for lv in grid_levels:
-            sc = rooms.random_room(seed, 4.0, patch_res=0.125)
-            grid[lv].append(run_one(sc, configs.vopts(configs.DISC2D, lv, 0.15, lamp_z=1.0), loose, a.eps))
-        print("grid room", seed, [round(grid[lv][-1]["dwell_s"], 1) for lv in grid_levels], flush=True)
-    out["grid"] = {"levels_m": grid_levels, "patch_res_m": 0.125,
-                   "dwell_norm": summarise(grid, "dwell_s"),
-                   "raw": {str(k): v for k, v in grid.items()}}
+    import __graft_entry__
+    __graft_entry__.build()
+    out = {"gpu": torch.cuda.get_device_name(0), "rooms": a.rooms, "timing": "best of 3 after a warm-up"}
+    levels = [0.5, 0.25, 0.125, 0.0625, 0.03125]
+    env = {lv: [run_one(rooms.random_room(s, 4.0, patch_res=lv), configs.vopts(configs.DISC2D, 0.1, 0.15, lamp_z=1.0))
+                for s in range(a.rooms)] for lv in levels}
+    out["env_res"] = {"grid_m": 0.1, "levels": {str(k): summary(v) for k, v in env.items()}}
+    print("env-res", {k: round(v["entries_per_s_median"] / 1e9, 2) for k, v in out["env_res"]["levels"].items()})
+    grid = {lv: [run_one(rooms.random_room(s, 4.0, patch_res=0.125), configs.vopts(configs.DISC2D, lv, 0.15, lamp_z=1.0))
+                 for s in range(a.rooms)] for lv in levels}
+    out["grid"] = {"patch_res_m": 0.125, "levels": {str(k): summary(v) for k, v in grid.items()}}
+    print("grid", {k: round(v["entries_per_s_median"] / 1e9, 2) for k, v in out["grid"]["levels"].items()})
     if not a.no_3d:
-        sp = [1.0, 0.75, 0.5, 0.4, 0.3, 0.25]
         rows = []
-        for s in sp:
-            r = run_one(configs.c4_scene(), dict(configs.FLOAT_OPTS, spacing=s), configs.T_MAX, 1e-4)
+        for s in [1.0, 0.75, 0.5, 0.4, 0.3, 0.25]:
+            r = run_one(configs.c4_scene(), dict(configs.FLOAT_OPTS, spacing=s))
             r["spacing_m"] = s
             rows.append(r)
-            print("3d", s, {k: r[k] for k in ("K", "assemble_ms", "coverage_total", "lp_iterations")}, flush=True)
+            print("3d", s, r, flush=True)
         out["grid_3d"] = rows
     if a.out:
         with open(a.out, "w") as f:
