@@ -92,7 +92,7 @@ def parse():
 def workload(name):
     from synth import configs
     if name == "C5":
-        return dict(name="C5: synthetic ward ≥1M triangles × Armbot configs at 0.25 m",
+        return dict(name="C5: synthetic ward ≥1M triangles × Armbot configs (0.2 m grid)",
                     scene=configs.c5_scene(), vantage=configs.ARM_OPTS, L=1)
     if name == "C4-float":
         return dict(name="C4: synthetic ward ~216k triangles × Floatbot configs at 0.25 m",

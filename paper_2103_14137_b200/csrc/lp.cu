@@ -385,7 +385,7 @@ extern "C" int uvd_lp_solve(const uvd_matrix_out* A, int64_t n, int64_t k, const
   }
   DeviceGuard dg(pointer_device(sigma));
   NvtxRange nvr("uvd_lp_solve");
-  UVD_TRY(fluence_check(A, n, k, sigma));
+  if (k > 0) UVD_TRY(fluence_check(A, n, k, sigma));  // an empty shard has no A to check
   cudaStream_t st = (cudaStream_t)stream;
   const double eps = o->eps > 0.0 ? o->eps : 1e-6;
   const int64_t max_iter = o->max_iter > 0 ? o->max_iter : 200000;

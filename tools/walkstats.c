@@ -1,0 +1,200 @@
+/* walkstats.c — traversal statistics of the assembly's per-lane BVH walk on
+ * sampled work items (a development tool; not the oracle, not the product).
+ *
+ * Replays k_assemble_lane's walk on the CPU (fp32 slab tests bounded by the
+ * segment's t range, near child first, any hit ends the ray, the fp32
+ * triangle filter) on the scene's own BVH (dumped by tools/walkstats.py) and
+ * reports, per node depth: visits per ray, and for each work item (one lamp,
+ * 32 consecutive rows) the UNION of nodes its lanes visit — the work a
+ * warp-shared (beam) traversal of that depth range could not avoid.
+ *
+ * usage: walkstats nodes.bin tri.bin cen.bin nrm.bin lamps.bin items.bin N M nn K root n_items
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <stdlib.h>
+#include <string.h>
+
+typedef struct { float a[4], b[4], c[4]; uint32_t d[4]; } Node;
+#define MAXD 96
+#define STK 256
+
+static void* slurp(const char* path, size_t* n) {
+  FILE* f = fopen(path, "rb");
+  if (!f) { perror(path); exit(1); }
+  fseek(f, 0, SEEK_END);
+  *n = (size_t)ftell(f);
+  fseek(f, 0, SEEK_SET);
+  void* p = malloc(*n);
+  if (fread(p, 1, *n, f) != *n) { perror("read"); exit(1); }
+  fclose(f);
+  return p;
+}
+
+static int is_leaf(uint32_t r) { return (r & 0x80000000u) != 0; }
+
+/* fp32 filtered segment/triangle test as in traverse.cuh (0 miss, 1 hit, 2 undecided) */
+static int tri32(float ox, float oy, float oz, float dx, float dy, float dz, float nD, float tlo, float thi,
+                 const float* a, const float* b, const float* c) {
+  const float k = 16.0f * 5.9604645e-08f;
+  float e1x = b[0] - a[0], e1y = b[1] - a[1], e1z = b[2] - a[2];
+  float e2x = c[0] - a[0], e2y = c[1] - a[1], e2z = c[2] - a[2];
+  float tx = ox - a[0], ty = oy - a[1], tz = oz - a[2];
+  float px = dy * e2z - dz * e2y, py = dz * e2x - dx * e2z, pz = dx * e2y - dy * e2x;
+  float det = e1x * px + e1y * py + e1z * pz;
+  float nE1 = fabsf(e1x) + fabsf(e1y) + fabsf(e1z), nE2 = fabsf(e2x) + fabsf(e2y) + fabsf(e2z);
+  float nT = fabsf(tx) + fabsf(ty) + fabsf(tz);
+  float eDet = k * nE1 * nD * nE2, A = fabsf(det);
+  if (A <= eDet) return 2;
+  float s = det > 0.f ? 1.f : -1.f;
+  float U = s * (tx * px + ty * py + tz * pz), eU = k * nT * nD * nE2;
+  if (U < -eU) return 0;
+  float qx = ty * e1z - tz * e1y, qy = tz * e1x - tx * e1z, qz = tx * e1y - ty * e1x;
+  float V = s * (dx * qx + dy * qy + dz * qz), eV = k * nD * nT * nE1;
+  if (V < -eV) return 0;
+  float Wm = A - U - V, eWm = eDet + eU + eV;
+  if (Wm < -eWm) return 0;
+  float W = s * (e2x * qx + e2y * qy + e2z * qz), eW = k * nE2 * nT * nE1;
+  float m0 = W - tlo * A, e0 = eW + tlo * eDet, m1 = thi * A - W, e1 = eW + eDet;
+  if (m0 < -e0 || m1 < -e1) return 0;
+  if (U > eU && V > eV && Wm > eWm && m0 > e0 && m1 > e1) return 1;
+  return 2;
+}
+
+static float sinv(float d) { return fabsf(d) < 1e-30f ? copysignf(1e30f, d) : 1.0f / d; }
+
+/* simple open-addressing set of node ids (per item) */
+#define HSZ 65536
+static uint32_t hkey[HSZ];
+static uint16_t hstamp[HSZ];
+static uint16_t cur_stamp = 0;
+static int hset_add(uint32_t k) {  /* 1 if new */
+  uint32_t h = (k * 2654435761u) & (HSZ - 1);
+  while (hstamp[h] == cur_stamp) {
+    if (hkey[h] == k) return 0;
+    h = (h + 1) & (HSZ - 1);
+  }
+  hstamp[h] = cur_stamp;
+  hkey[h] = k;
+  return 1;
+}
+
+int main(int argc, char** argv) {
+  if (argc < 13) { fprintf(stderr, "usage\n"); return 1; }
+  size_t sz;
+  const Node* nodes = (const Node*)slurp(argv[1], &sz);
+  const float* tri = (const float*)slurp(argv[2], &sz);
+  const float* cen = (const float*)slurp(argv[3], &sz);
+  const float* nrm = (const float*)slurp(argv[4], &sz);
+  const float* lamps = (const float*)slurp(argv[5], &sz);
+  const int64_t* items = (const int64_t*)slurp(argv[6], &sz);
+  const int64_t N = atoll(argv[7]), nn = atoll(argv[9]);
+  const uint32_t root = (uint32_t)strtoul(argv[11], 0, 10);
+  const int64_t n_items = atoll(argv[12]);
+  (void)argv[8]; (void)argv[10];
+  /* node depths (preorder: parents before children) */
+  int* depth = (int*)calloc((size_t)nn, sizeof(int));
+  for (int64_t i = 0; i < nn; ++i)
+    for (int s = 0; s < 2; ++s)
+      if (!is_leaf(nodes[i].d[s])) depth[nodes[i].d[s]] = depth[i] + 1;
+  double uni_d[MAXD] = {0}, lanes_d[MAXD] = {0};
+  double rays[2] = {0, 0}, tri_tests[2] = {0, 0}, n_it = 0, und = 0;
+  double maxlane_sum = 0, nv_res[2] = {0, 0};
+  for (int64_t it = 0; it < n_items; ++it) {
+    const int64_t c = items[2 * it], tile = items[2 * it + 1];
+    const float* p = lamps + 3 * c;
+    const float ox = p[0], oy = p[1], oz = p[2];
+    ++cur_stamp;
+    if (cur_stamp == 0) { memset(hstamp, 0, sizeof(hstamp)); cur_stamp = 1; }
+    double item_vis[MAXD] = {0};
+    int any = 0, maxlane = 0;
+    for (int lane = 0; lane < 32; ++lane) {
+      const int64_t r = tile * 32 + lane;
+      if (r >= N) continue;
+      const float cx = cen[3 * r], cy = cen[3 * r + 1], cz = cen[3 * r + 2];
+      const double Dx = (double)cx - ox, Dy = (double)cy - oy, Dz = (double)cz - oz;
+      const double cosd = -(Dx * nrm[3 * r] + Dy * nrm[3 * r + 1] + Dz * nrm[3 * r + 2]);
+      if (!(cosd > 0.0)) continue;
+      any = 1;
+      const float dx = cx - ox, dy = cy - oy, dz = cz - oz;
+      const float ix = sinv(dx), iy = sinv(dy), iz = sinv(dz);
+      const float tlo = 1e-4f / sqrtf(dx * dx + dy * dy + dz * dz), thi = 1.0f - tlo;
+      const float nD = fabsf(dx) + fabsf(dy) + fabsf(dz);
+      uint32_t stk[STK];
+      int sp = 0, res = 0, undec = 0, nv = 0, ntri = 0;
+      uint32_t ref = root;
+      for (;;) {
+        while (!is_leaf(ref)) {
+          const Node* n = nodes + ref;
+          const int dep = depth[ref] < MAXD ? depth[ref] : MAXD - 1;
+          item_vis[dep] += 1;
+          if (hset_add(ref)) uni_d[dep] += 1;
+          ++nv;
+          const float* bx[2] = {n->a, n->b};
+          float an[2], af[2];
+          for (int s = 0; s < 2; ++s) {
+            float x0 = (bx[s][0] - ox) * ix, x1 = (bx[s][1] - ox) * ix;
+            float y0 = (bx[s][2] - oy) * iy, y1 = (bx[s][3] - oy) * iy;
+            float z0 = (n->c[2 * s] - oz) * iz, z1 = (n->c[2 * s + 1] - oz) * iz;
+            an[s] = fmaxf(fmaxf(fminf(x0, x1), fminf(y0, y1)), fmaxf(fminf(z0, z1), 0.f));
+            af[s] = fminf(fminf(fmaxf(x0, x1), fmaxf(y0, y1)), fminf(fmaxf(z0, z1), thi));
+          }
+          const int h0 = an[0] <= af[0], h1 = an[1] <= af[1];
+          if (h0 && h1) {
+            const int sw = an[1] < an[0];
+            ref = sw ? n->d[1] : n->d[0];
+            stk[sp++] = sw ? n->d[0] : n->d[1];
+          } else if (h0 || h1) {
+            ref = h0 ? n->d[0] : n->d[1];
+          } else {
+            ref = sp ? stk[--sp] : 0xffffffffu;
+          }
+        }
+        if (ref == 0xffffffffu) break;
+        const uint32_t st = (ref & 0x7fffffffu) >> 3, cnt = (ref & 7u) + 1u;
+        int hit = 0;
+        for (uint32_t k = 0; k < cnt; ++k) {
+          const float* tv = tri + 12 * (int64_t)(st + k);
+          int own;
+          memcpy(&own, tv + 3, 4);
+          if (own == (int)r) continue;
+          ++ntri;
+          const int cls = tri32(ox, oy, oz, dx, dy, dz, nD, tlo, thi, tv, tv + 4, tv + 8);
+          if (cls == 1) { hit = 1; break; }
+          if (cls == 2) undec = 1;
+        }
+        if (hit) { res = 1; break; }
+        ref = sp ? stk[--sp] : 0xffffffffu;
+        if (ref == 0xffffffffu) break;
+      }
+      rays[res] += 1;
+      tri_tests[res] += ntri;
+      nv_res[res] += nv;
+      und += undec;
+      if (nv > maxlane) maxlane = nv;
+    }
+    if (any) {
+      n_it += 1;
+      maxlane_sum += maxlane;
+      for (int d = 0; d < MAXD; ++d) lanes_d[d] += item_vis[d];
+    }
+  }
+  const double R = rays[0] + rays[1];
+  printf("{\"items\": %.0f, \"rays\": %.0f, \"occluded_fraction\": %.5f, \"undecided_fraction\": %.6f,\n", n_it, R,
+         rays[1] / R, und / R);
+  printf(" \"tri_tests_per_ray\": %.3f, \"max_lane_visits_per_item\": %.3f,\n", (tri_tests[0] + tri_tests[1]) / R,
+         maxlane_sum / n_it);
+  double tot = 0, totu = 0;
+  for (int d = 0; d < MAXD; ++d) { tot += lanes_d[d]; totu += uni_d[d]; }
+  printf(" \"visits_per_ray\": %.3f, \"visits_per_clear_ray\": %.3f, \"visits_per_occluded_ray\": %.3f, \"union_visits_per_item\": %.3f,\n",
+         tot / R, nv_res[0] / rays[0], nv_res[1] / rays[1], totu / n_it);
+  printf(" \"by_depth\": [");
+  for (int d = 0, first = 1; d < MAXD; ++d) {
+    if (lanes_d[d] == 0) continue;
+    printf("%s[%d, %.4f, %.4f]", first ? "" : ", ", d, lanes_d[d] / R, uni_d[d] / n_it);
+    first = 0;
+  }
+  printf("]}\n");
+  return 0;
+}
