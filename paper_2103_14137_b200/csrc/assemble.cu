@@ -180,31 +180,35 @@ __device__ __forceinline__ int lane_walk32(const AsmParams& P, float ox, float o
 // that many tiles, every column of a super-tile before the next one (rays from
 // ~9 lamps to the same 16 K patches in flight), chosen when the BVH is several
 // times the L2: the paths near the patches are then shared across lamps.
-__device__ __forceinline__ void item_to_tile(const AsmParams& P, int64_t item, int64_t& c, int64_t& tile) {
-  if (P.super_log2 < 0) {
+__device__ __forceinline__ void item_to_unit(const AsmParams& P, int64_t units, int super_log2, int64_t item,
+                                             int64_t& c, int64_t& tile) {
+  if (super_log2 < 0) {
     if (P.items32) {  // 32-bit division (a 64-bit one is a ~70-instruction sequence)
-      const uint32_t cc = (uint32_t)item / (uint32_t)P.tiles;
+      const uint32_t cc = (uint32_t)item / (uint32_t)units;
       c = cc;
-      tile = (int64_t)((uint32_t)item - cc * (uint32_t)P.tiles);
+      tile = (int64_t)((uint32_t)item - cc * (uint32_t)units);
     } else {
-      c = item / P.tiles;
-      tile = item - c * P.tiles;
+      c = item / units;
+      tile = item - c * units;
     }
     return;
   }
-  // super-tiles of T = 2^super_log2 tiles; items < 2^32 (checked on the host)
-  const uint32_t sh = (uint32_t)P.super_log2, T = 1u << sh, it = (uint32_t)item;
-  const uint32_t full = (uint32_t)P.tiles >> sh, per = (uint32_t)P.n_cols << sh, base = full * per;
+  // super-tiles of T = 2^super_log2 units; items < 2^32 (checked on the host)
+  const uint32_t sh = (uint32_t)super_log2, T = 1u << sh, it = (uint32_t)item;
+  const uint32_t full = (uint32_t)units >> sh, per = (uint32_t)P.n_cols << sh, base = full * per;
   if (it < base) {
     const uint32_t s = it / per, rem = it - s * per;
     c = rem >> sh;
     tile = (int64_t)((s << sh) + (rem & (T - 1u)));
   } else {
-    const uint32_t rem = it - base, tl = (uint32_t)P.tiles - (full << sh);
+    const uint32_t rem = it - base, tl = (uint32_t)units - (full << sh);
     const uint32_t cc = rem / tl;
     c = cc;
     tile = (int64_t)((full << sh) + rem - cc * tl);
   }
+}
+__device__ __forceinline__ void item_to_tile(const AsmParams& P, int64_t item, int64_t& c, int64_t& tile) {
+  item_to_unit(P, P.tiles, P.super_log2, item, c, tile);
 }
 
 template <bool COUNT, bool OCT>
@@ -212,6 +216,8 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmMinBlocks) k_assemble_lane(As
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   unsigned long long cnt[6] = {0, 0, 0, 0, 0, 0};  // per-lane tallies (COUNT only)
   const int64_t total = P.n_cols * P.tiles;
+  // static stride: warp w of block b takes items b·W + w, + G·W, ... (a per-block
+  // dynamic schedule keeping an SM's warps on one lamp was measured slower)
   for (int64_t item = (int64_t)blockIdx.x * kAsmWarps + warp; item < total;
        item += (int64_t)gridDim.x * kAsmWarps) {
     // tile fastest: concurrent warps trace adjacent patches from the same lamp

@@ -80,3 +80,5 @@ def test_fixup_list_overflow_bit_identical(uvd, cap, monkeypatch):
     sc.sync_status()
     assert torch.equal(ref["A"], got["A"])
     assert torch.equal(ref["vis_bits"], got["vis_bits"])
+
+

@@ -80,6 +80,95 @@ static int hset_add(uint32_t k) {  /* 1 if new */
   return 1;
 }
 
+
+/* Warp-packet replay of one work item: one DFS for all 32 lanes, each stack
+ * entry carrying the mask of lanes whose segment enters that node; a node is
+ * visited while some of its lanes are still undecided; at a leaf the lanes in
+ * its mask test the triangles (a certain hit retires the lane).  Near child:
+ * the one most of the lanes that hit both enter first. */
+typedef struct { double node_steps, leaf_steps, tri_steps, lane_tri; } Pk;
+static void packet_item(const Node* nodes, const float* tri, const float* cen, const float* nrm, int64_t N,
+                        uint32_t root, float ox, float oy, float oz, int64_t tile, Pk* pk) {
+  float ix[32], iy[32], iz[32], thi[32], tlo[32], dx[32], dy[32], dz[32], nD[32];
+  uint32_t live = 0;
+  for (int l = 0; l < 32; ++l) {
+    const int64_t r = tile * 32 + l;
+    if (r >= N) continue;
+    const float cx = cen[3 * r], cy = cen[3 * r + 1], cz = cen[3 * r + 2];
+    const double Dx = (double)cx - ox, Dy = (double)cy - oy, Dz = (double)cz - oz;
+    if (!(-(Dx * nrm[3 * r] + Dy * nrm[3 * r + 1] + Dz * nrm[3 * r + 2]) > 0.0)) continue;
+    dx[l] = cx - ox; dy[l] = cy - oy; dz[l] = cz - oz;
+    ix[l] = sinv(dx[l]); iy[l] = sinv(dy[l]); iz[l] = sinv(dz[l]);
+    tlo[l] = 1e-4f / sqrtf(dx[l] * dx[l] + dy[l] * dy[l] + dz[l] * dz[l]);
+    thi[l] = 1.0f - tlo[l];
+    nD[l] = fabsf(dx[l]) + fabsf(dy[l]) + fabsf(dz[l]);
+    live |= 1u << l;
+  }
+  if (!live) return;
+  uint32_t sref[STK], smask[STK];
+  int sp = 0;
+  uint32_t ref = root, mask = live, done = 0;
+  for (;;) {
+    const uint32_t act = mask & ~done;
+    if (act) {
+      if (!is_leaf(ref)) {
+        const Node* n = nodes + ref;
+        pk->node_steps += 1;
+        uint32_t m0 = 0, m1 = 0, nearer1 = 0;
+        for (int l = 0; l < 32; ++l) {
+          if (!((act >> l) & 1)) continue;
+          const float* bx[2] = {n->a, n->b};
+          float an[2], af[2];
+          for (int s2 = 0; s2 < 2; ++s2) {
+            float x0 = (bx[s2][0] - ox) * ix[l], x1 = (bx[s2][1] - ox) * ix[l];
+            float y0 = (bx[s2][2] - oy) * iy[l], y1 = (bx[s2][3] - oy) * iy[l];
+            float z0 = (n->c[2 * s2] - oz) * iz[l], z1 = (n->c[2 * s2 + 1] - oz) * iz[l];
+            an[s2] = fmaxf(fmaxf(fminf(x0, x1), fminf(y0, y1)), fmaxf(fminf(z0, z1), 0.f));
+            af[s2] = fminf(fminf(fmaxf(x0, x1), fmaxf(y0, y1)), fminf(fmaxf(z0, z1), thi[l]));
+          }
+          if (an[0] <= af[0]) m0 |= 1u << l;
+          if (an[1] <= af[1]) m1 |= 1u << l;
+          if (an[0] <= af[0] && an[1] <= af[1] && an[1] < an[0]) nearer1 |= 1u << l;
+        }
+        if (m0 && m1) {
+          const int both = __builtin_popcount(m0 & m1);
+          const int sw = 2 * __builtin_popcount(nearer1) > both;
+          sref[sp] = sw ? n->d[0] : n->d[1];
+          smask[sp++] = sw ? m0 : m1;
+          ref = sw ? n->d[1] : n->d[0];
+          mask = sw ? m1 : m0;
+          continue;
+        } else if (m0 || m1) {
+          ref = m0 ? n->d[0] : n->d[1];
+          mask = m0 ? m0 : m1;
+          continue;
+        }
+      } else {
+        pk->leaf_steps += 1;
+        const uint32_t st = (ref & 0x7fffffffu) >> 3, cnt = (ref & 7u) + 1u;
+        for (uint32_t k = 0; k < cnt; ++k) {
+          const float* tv = tri + 12 * (int64_t)(st + k);
+          int own;
+          memcpy(&own, tv + 3, 4);
+          const uint32_t a2 = mask & ~done;
+          if (!a2) break;
+          pk->tri_steps += 1;
+          for (int l = 0; l < 32; ++l) {
+            if (!((a2 >> l) & 1)) continue;
+            if (own == (int)(tile * 32 + l)) continue;
+            pk->lane_tri += 1;
+            if (tri32(ox, oy, oz, dx[l], dy[l], dz[l], nD[l], tlo[l], thi[l], tv, tv + 4, tv + 8) == 1)
+              done |= 1u << l;
+          }
+        }
+      }
+    }
+    if (!sp) break;
+    ref = sref[--sp];
+    mask = smask[sp];
+  }
+}
+
 int main(int argc, char** argv) {
   if (argc < 13) { fprintf(stderr, "usage\n"); return 1; }
   size_t sz;
@@ -100,7 +189,9 @@ int main(int argc, char** argv) {
       if (!is_leaf(nodes[i].d[s])) depth[nodes[i].d[s]] = depth[i] + 1;
   double uni_d[MAXD] = {0}, lanes_d[MAXD] = {0};
   double rays[2] = {0, 0}, tri_tests[2] = {0, 0}, n_it = 0, und = 0;
-  double maxlane_sum = 0, nv_res[2] = {0, 0};
+  double maxlane_sum = 0, nv_res[2] = {0, 0}, leaf_lane = 0;
+  Pk pk = {0, 0, 0, 0};
+  double uni_leaf = 0;
   for (int64_t it = 0; it < n_items; ++it) {
     const int64_t c = items[2 * it], tile = items[2 * it + 1];
     const float* p = lamps + 3 * c;
@@ -109,6 +200,7 @@ int main(int argc, char** argv) {
     if (cur_stamp == 0) { memset(hstamp, 0, sizeof(hstamp)); cur_stamp = 1; }
     double item_vis[MAXD] = {0};
     int any = 0, maxlane = 0;
+    packet_item(nodes, tri, cen, nrm, N, root, ox, oy, oz, tile, &pk);
     for (int lane = 0; lane < 32; ++lane) {
       const int64_t r = tile * 32 + lane;
       if (r >= N) continue;
@@ -154,6 +246,8 @@ int main(int argc, char** argv) {
         if (ref == 0xffffffffu) break;
         const uint32_t st = (ref & 0x7fffffffu) >> 3, cnt = (ref & 7u) + 1u;
         int hit = 0;
+        leaf_lane += 1;
+        if (hset_add(ref)) uni_leaf += 1;
         for (uint32_t k = 0; k < cnt; ++k) {
           const float* tv = tri + 12 * (int64_t)(st + k);
           int own;
@@ -189,6 +283,10 @@ int main(int argc, char** argv) {
   for (int d = 0; d < MAXD; ++d) { tot += lanes_d[d]; totu += uni_d[d]; }
   printf(" \"visits_per_ray\": %.3f, \"visits_per_clear_ray\": %.3f, \"visits_per_occluded_ray\": %.3f, \"union_visits_per_item\": %.3f,\n",
          tot / R, nv_res[0] / rays[0], nv_res[1] / rays[1], totu / n_it);
+  printf(" \"leaf_visits_per_ray\": %.3f, \"union_leaves_per_item\": %.3f,\n", leaf_lane / R, uni_leaf / n_it);
+  printf(" \"packet\": {\"node_steps_per_item\": %.3f, \"leaf_steps_per_item\": %.3f, \"tri_steps_per_item\": %.3f, \"lane_tri_tests_per_ray\": %.3f},\n",
+         pk.node_steps / n_it, pk.leaf_steps / n_it, pk.tri_steps / n_it, pk.lane_tri / R);
+  printf(" \"lanes_per_item\": %.3f,\n", R / n_it);
   printf(" \"by_depth\": [");
   for (int d = 0, first = 1; d < MAXD; ++d) {
     if (lanes_d[d] == 0) continue;
