@@ -51,6 +51,8 @@ struct AsmParams {
   int64_t N;
   const float* __restrict__ lamps;
   const float* __restrict__ lampc;  // [n_cols][L][3] lamps gathered per column (k_assemble_lane)
+  const float* __restrict__ lamp_free;   // [n_cols][L] lamp radius r_L (free.cu), or nullptr
+  const float* __restrict__ front_free;  // [N] front radius r_T (free.cu), or nullptr
   int L;
   double scale;  // P / (4π L)
   const int64_t* __restrict__ cols;  // device, nullptr = identity
@@ -91,7 +93,7 @@ enum { kClear = 0, kBlocked = 1, kUndecided = 2 };
 // decide some triangle (the caller flags the entry for exact re-tracing).
 template <bool COUNT, bool OCT>
 __device__ __forceinline__ int lane_walk32(const AsmParams& P, float ox, float oy, float oz,
-                                           float dx, float dy, float dz, int owner,
+                                           float dx, float dy, float dz, int owner, float rl, float rt,
                                            unsigned long long* cnt) {
   uint32_t stk[kLaneStack];
   int sp = 0;
@@ -101,8 +103,15 @@ __device__ __forceinline__ int lane_walk32(const AsmParams& P, float ox, float o
   // the segment's own extent t in (t_lo, t_hi) also bounds the box tests: boxes
   // the segment only enters within 0.1 mm of the target (e.g. the target's own
   // flat leaf and its flat ancestors) are never visited
-  const float tlo = (float)kSelfEps * rsqrtf(dx * dx + dy * dy + dz * dz);
+  const float inv_len = rsqrtf(dx * dx + dy * dy + dz * dz);
+  const float tlo = (float)kSelfEps * inv_len;
   const float thi = 1.0f - tlo;
+  // and by the empty regions at its ends (free.cu): nothing within r_L of the
+  // lamp, nothing in front of the patch within r_T; the box range shrinks to
+  // [tmin, tmax] (factors 1 - 1e-5 and the 2e-7 slack cover rsqrtf's and the
+  // products' rounding, so the bounds stay outside the true ones)
+  const float tmin = rl * inv_len * 0.99999f;
+  const float tmax = fminf(thi, 1.0f - fmaxf(rt * inv_len * 0.99999f - 2e-7f, 0.0f));
   // start in the copy of the nodes whose slabs are stored (near, far) for this
   // ray's octant; child refs stay inside that copy
   const uint32_t oct = (__float_as_uint(ix) >> 31) | ((__float_as_uint(iy) >> 31) << 1) |
@@ -133,15 +142,15 @@ __device__ __forceinline__ int lane_walk32(const AsmParams& P, float ox, float o
       const float bz0 = fmaf(nc.z, iz, -oiz), bz1 = fmaf(nc.w, iz, -oiz);
       float an, af, bn, bf;
       if (OCT) {
-        an = fmaxf(fmaxf(ax0, ay0), fmaxf(az0, 0.0f));
-        af = fminf(fminf(ax1, ay1), fminf(az1, thi));
-        bn = fmaxf(fmaxf(bx0, by0), fmaxf(bz0, 0.0f));
-        bf = fminf(fminf(bx1, by1), fminf(bz1, thi));
+        an = fmaxf(fmaxf(ax0, ay0), fmaxf(az0, tmin));
+        af = fminf(fminf(ax1, ay1), fminf(az1, tmax));
+        bn = fmaxf(fmaxf(bx0, by0), fmaxf(bz0, tmin));
+        bf = fminf(fminf(bx1, by1), fminf(bz1, tmax));
       } else {
-        an = fmaxf(fmaxf(fminf(ax0, ax1), fminf(ay0, ay1)), fmaxf(fminf(az0, az1), 0.0f));
-        af = fminf(fminf(fmaxf(ax0, ax1), fmaxf(ay0, ay1)), fminf(fmaxf(az0, az1), thi));
-        bn = fmaxf(fmaxf(fminf(bx0, bx1), fminf(by0, by1)), fmaxf(fminf(bz0, bz1), 0.0f));
-        bf = fminf(fminf(fmaxf(bx0, bx1), fmaxf(by0, by1)), fminf(fmaxf(bz0, bz1), thi));
+        an = fmaxf(fmaxf(fminf(ax0, ax1), fminf(ay0, ay1)), fmaxf(fminf(az0, az1), tmin));
+        af = fminf(fminf(fmaxf(ax0, ax1), fmaxf(ay0, ay1)), fminf(fmaxf(az0, az1), tmax));
+        bn = fmaxf(fmaxf(fminf(bx0, bx1), fminf(by0, by1)), fmaxf(fminf(bz0, bz1), tmin));
+        bf = fminf(fminf(fmaxf(bx0, bx1), fmaxf(by0, by1)), fminf(fmaxf(bz0, bz1), tmax));
       }
       const bool h0 = an <= af;
       const bool h1 = bn <= bf;
@@ -232,7 +241,7 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmMinBlocks) k_assemble_lane(As
       const float ox = pl[0], oy = pl[1], oz = pl[2];
       bool vis = false, front = false;
       float cx = 0.f, cy = 0.f, cz = 0.f;
-      double w = 0.0;
+      double w = 0.0, cosr = 0.0;
       if (valid) {
         cx = P.centroid[3 * r]; cy = P.centroid[3 * r + 1]; cz = P.centroid[3 * r + 2];
         const float nx = P.normal[3 * r], ny = P.normal[3 * r + 1], nz = P.normal[3 * r + 2];
@@ -247,12 +256,16 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmMinBlocks) k_assemble_lane(As
           front = false;
         }
         w = cosd / (dd * d);  // a6: Eq. 7 in fp64, added if the ray is clear
+        cosr = cosd - 1e-2 * d >= 0.0 ? 1.0 : 0.0;  // cos θ ≥ 1e-2 (no division)
       }
       const float dx = cx - ox, dy = cy - oy, dz = cz - oz;
       if (front) {
         if (COUNT) cnt[0] += 1;
+        // empty end regions (free.cu); the front one only away from grazing (cos θ ≥ 1e-2)
+        const float rl = P.lamp_free ? P.lamp_free[c * P.L + l] : 0.0f;
+        const float rt = P.front_free && cosr >= 1e-2 ? P.front_free[r] : 0.0f;
         // a5: occlusion of the open segment, t in (1e-4/d, 1 - 1e-4/d), fp32 decisions
-        const int res = lane_walk32<COUNT, OCT>(P, ox, oy, oz, dx, dy, dz, r, cnt);
+        const int res = lane_walk32<COUNT, OCT>(P, ox, oy, oz, dx, dy, dz, r, rl, rt, cnt);
         vis = res == kClear;
         pend |= res == kUndecided;
         if (vis) acc += w;
@@ -377,7 +390,7 @@ __global__ void __launch_bounds__(kAreaThreads, UVD_AREA_MINB) k_assemble_area(A
                 continue;
               }
               if (COUNT) cnt[0] += 1;
-              const int res = lane_walk32<COUNT, OCT>(P, ox, oy, oz, dx, dy, dz, r, cnt);
+              const int res = lane_walk32<COUNT, OCT>(P, ox, oy, oz, dx, dy, dz, r, 0.0f, 0.0f, cnt);
               if (COUNT && res == kBlocked) cnt[5] += 1;
               pend |= res == kUndecided;
               if (res == kClear) {
@@ -876,6 +889,9 @@ extern "C" int uvd_irradiance_matrix(const uvd_scene* s, const float* lamp_xyz, 
   P.cols = dcols;
   P.vis_bits = out->vis_bits ? out->vis_bits : vis_scratch;
   P.lampc = nullptr;
+  P.lamp_free = nullptr;
+  P.front_free = s->front_free;
+  if (const char* e = getenv("UVD_FREE")) if (atoi(e) == 0) P.front_free = nullptr;  // dev A/B
   if (!area_model) {
     float* lampc = (float*)sc.get((size_t)n_cols * P.L * 3 * sizeof(float));
     if (!lampc) { set_error("uvd_irradiance_matrix: out of device memory"); return UVD_ERR_NOMEM; }
@@ -883,6 +899,10 @@ extern "C" int uvd_irradiance_matrix(const uvd_scene* s, const float* lamp_xyz, 
     k_gather_lamps<<<(unsigned)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, st>>>(P, lampc);
     note_launch();
     P.lampc = lampc;
+    float* lfree = (float*)sc.get((size_t)n_cols * P.L * sizeof(float));
+    if (!lfree) { set_error("uvd_irradiance_matrix: out of device memory"); return UVD_ERR_NOMEM; }
+    UVD_TRY(lamp_radius(s, lampc, n_cols * P.L, lfree, st));
+    P.lamp_free = P.front_free ? lfree : nullptr;
   }
   static int g_lane[4][kMaxDevices], g_area[4][kMaxDevices];  // [COUNT * 2 + OCT][device]
   const int gi = (P.counters ? 2 : 0) + (P.onodes ? 1 : 0);

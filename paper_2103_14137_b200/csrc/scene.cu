@@ -441,7 +441,7 @@ static void free_scene(uvd_scene* s) {
   Alloc& al = s->alloc;
   for (void* p : {(void*)s->centroid, (void*)s->normal, (void*)s->area, (void*)s->orig_id,
                   (void*)s->tri, (void*)s->nodes, (void*)s->walls, (void*)s->poly_xy,
-                  (void*)s->poly_off, (void*)s->err_flag, (void*)s->ptri, (void*)s->onodes})
+                  (void*)s->poly_off, (void*)s->err_flag, (void*)s->ptri, (void*)s->onodes, (void*)s->front_free})
     al.put(p);
   for (auto& c : s->cov_part) al.put(c.p);
   cudaStreamSynchronize(al.stream);
@@ -476,6 +476,7 @@ extern "C" int uvd_scene_create(const uvd_scene_desc* desc, int device, void* st
   }
   cudaStream_t st = (cudaStream_t)stream;
   int rc = desc->kind == UVD_SCENE_TRIMESH ? create_trimesh(s, desc, st) : create_extruded(s, desc, st);
+  if (rc == UVD_OK) rc = front_radius(s, st);  // patches (row order) and BVH are final here
   if (rc == UVD_OK && !host_stage()) {
     set_error("scene: out of pinned host memory (staging)");
     rc = UVD_ERR_NOMEM;

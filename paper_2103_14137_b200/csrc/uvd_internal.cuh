@@ -158,6 +158,7 @@ struct uvd_scene {
   uvd::Node* onodes = nullptr; // 8 x max(M-1, 1): the nodes with each child box stored (near, far) per ray octant
   int64_t n_nodes = 0;
   uint32_t root = 0;          // root ref
+  float* front_free = nullptr; // [N] front radius of every patch (free.cu)
   // 2.5D description (device + host copies) for the floorplan vantage test
   uvd::Wall* walls = nullptr;  // device
   int64_t n_walls = 0;
@@ -183,6 +184,9 @@ void* host_stage();
 // launchers implemented in the .cu files
 int build_bvh(uvd_scene* s, float4* tri_in, uint32_t** order_out, cudaStream_t st);
 int sort_pairs_u64(uint64_t* keys, uint32_t* vals, int64_t n, Alloc& al, cudaStream_t st);
+// free.cu: empty regions at the segment ends (front radius per patch, lamp radius per sample)
+int front_radius(uvd_scene* s, cudaStream_t st);
+int lamp_radius(const uvd_scene* s, const float* lamps, int64_t n, float* out, cudaStream_t st);
 // fluence.cu: the a7 products without allocation (uvd_lp_solve graphs them)
 Alloc matrix_alloc(const uvd_matrix_out* A, int dev, cudaStream_t st);
 size_t fluence_ws_bytes(int64_t n, int64_t k, bool csc, int dev);

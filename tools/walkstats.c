@@ -81,6 +81,127 @@ static int hset_add(uint32_t k) {  /* 1 if new */
 }
 
 
+
+/* ---- free regions at the segment ends (what a shorter t range would save) ---- */
+typedef struct { double x, y, z; } V3;
+static V3 v3(double x, double y, double z) { V3 r = {x, y, z}; return r; }
+static V3 vsub(V3 a, V3 b) { return v3(a.x - b.x, a.y - b.y, a.z - b.z); }
+static double vdot(V3 a, V3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+static V3 vld(const float* p) { return v3(p[0], p[1], p[2]); }
+static V3 vmad(V3 a, V3 b, double s) { return v3(a.x + b.x * s, a.y + b.y * s, a.z + b.z * s); }
+static double pt_tri(V3 p, V3 a, V3 b, V3 c) {  /* closest-point distance (Voronoi regions) */
+  V3 ab = vsub(b, a), ac = vsub(c, a), ap = vsub(p, a);
+  double d1 = vdot(ab, ap), d2 = vdot(ac, ap);
+  if (d1 <= 0 && d2 <= 0) return sqrt(vdot(ap, ap));
+  V3 bp = vsub(p, b);
+  double d3 = vdot(ab, bp), d4 = vdot(ac, bp);
+  if (d3 >= 0 && d4 <= d3) return sqrt(vdot(bp, bp));
+  double vc = d1 * d4 - d3 * d2;
+  if (vc <= 0 && d1 >= 0 && d3 <= 0) { V3 q = vsub(p, vmad(a, ab, d1 / (d1 - d3))); return sqrt(vdot(q, q)); }
+  V3 cp = vsub(p, c);
+  double d5 = vdot(ab, cp), d6 = vdot(ac, cp);
+  if (d6 >= 0 && d5 <= d6) return sqrt(vdot(cp, cp));
+  double vb = d5 * d2 - d1 * d6;
+  if (vb <= 0 && d2 >= 0 && d6 <= 0) { V3 q = vsub(p, vmad(a, ac, d2 / (d2 - d6))); return sqrt(vdot(q, q)); }
+  double va = d3 * d6 - d5 * d4;
+  if (va <= 0 && (d4 - d3) >= 0 && (d5 - d6) >= 0) {
+    V3 q = vsub(p, vmad(b, vsub(c, b), (d4 - d3) / ((d4 - d3) + (d5 - d6))));
+    return sqrt(vdot(q, q));
+  }
+  double den = 1.0 / (va + vb + vc);
+  V3 q = vsub(p, vmad(vmad(a, ab, vb * den), ac, vc * den));
+  return sqrt(vdot(q, q));
+}
+static double box_d2(V3 p, float lx, float hx, float ly, float hy, float lz, float hz) {
+  double dx = fmax(fmax(lx - p.x, p.x - hx), 0), dy = fmax(fmax(ly - p.y, p.y - hy), 0), dz = fmax(fmax(lz - p.z, p.z - hz), 0);
+  return dx * dx + dy * dy + dz * dz;
+}
+/* distance from p to the nearest triangle (other than `own`) that has a vertex
+   strictly in front of the plane (n, p) when n != NULL; all triangles otherwise */
+static double nearest(const Node* nodes, const float* tri, uint32_t root, V3 p, const float* n, int own) {
+  uint32_t stk[STK];
+  int sp = 0;
+  double best = 1e30;
+  uint32_t ref = root;
+  for (;;) {
+    if (is_leaf(ref)) {
+      const uint32_t st = (ref & 0x7fffffffu) >> 3, cnt = (ref & 7u) + 1u;
+      for (uint32_t k = 0; k < cnt; ++k) {
+        const float* tv = tri + 12 * (int64_t)(st + k);
+        int o;
+        memcpy(&o, tv + 3, 4);
+        if (o == own) continue;
+        V3 a = vld(tv), b = vld(tv + 4), c = vld(tv + 8);
+        if (n) {
+          V3 nn = v3(n[0], n[1], n[2]);
+          const double e = 1e-6;
+          if (vdot(vsub(a, p), nn) <= e && vdot(vsub(b, p), nn) <= e && vdot(vsub(c, p), nn) <= e) continue;
+        }
+        double d = pt_tri(p, a, b, c);
+        if (d < best) best = d;
+      }
+    } else {
+      const Node* nd = nodes + ref;
+      double d0 = box_d2(p, nd->a[0], nd->a[1], nd->a[2], nd->a[3], nd->c[0], nd->c[1]);
+      double d1 = box_d2(p, nd->b[0], nd->b[1], nd->b[2], nd->b[3], nd->c[2], nd->c[3]);
+      uint32_t c0 = nd->d[0], c1 = nd->d[1];
+      if (d1 < d0) { double t = d0; d0 = d1; d1 = t; uint32_t u = c0; c0 = c1; c1 = u; }
+      if (d1 < best * best) stk[sp++] = c1;
+      if (d0 < best * best) { ref = c0; continue; }
+    }
+    if (!sp) break;
+    ref = stk[--sp];
+  }
+  return best;
+}
+
+/* the same walk with the box tests bounded to t in [tmin, thi] (a shorter segment); returns node visits */
+static int replay(const Node* nodes, const float* tri, uint32_t root, float ox, float oy, float oz, float dx, float dy,
+                  float dz, float tmin, float thi, float tlo, int own, double* ntri) {
+  const float ix = sinv(dx), iy = sinv(dy), iz = sinv(dz), nD = fabsf(dx) + fabsf(dy) + fabsf(dz);
+  uint32_t stk[STK];
+  int sp = 0, nv = 0;
+  uint32_t ref = root;
+  for (;;) {
+    while (!is_leaf(ref)) {
+      const Node* n = nodes + ref;
+      ++nv;
+      const float* bx[2] = {n->a, n->b};
+      float an[2], af[2];
+      for (int s = 0; s < 2; ++s) {
+        float x0 = (bx[s][0] - ox) * ix, x1 = (bx[s][1] - ox) * ix;
+        float y0 = (bx[s][2] - oy) * iy, y1 = (bx[s][3] - oy) * iy;
+        float z0 = (n->c[2 * s] - oz) * iz, z1 = (n->c[2 * s + 1] - oz) * iz;
+        an[s] = fmaxf(fmaxf(fminf(x0, x1), fminf(y0, y1)), fmaxf(fminf(z0, z1), tmin));
+        af[s] = fminf(fminf(fmaxf(x0, x1), fmaxf(y0, y1)), fminf(fmaxf(z0, z1), thi));
+      }
+      const int h0 = an[0] <= af[0], h1 = an[1] <= af[1];
+      if (h0 && h1) {
+        const int sw = an[1] < an[0];
+        ref = sw ? n->d[1] : n->d[0];
+        stk[sp++] = sw ? n->d[0] : n->d[1];
+      } else if (h0 || h1) {
+        ref = h0 ? n->d[0] : n->d[1];
+      } else {
+        ref = sp ? stk[--sp] : 0xffffffffu;
+      }
+    }
+    if (ref == 0xffffffffu) break;
+    const uint32_t st = (ref & 0x7fffffffu) >> 3, cnt = (ref & 7u) + 1u;
+    for (uint32_t k = 0; k < cnt; ++k) {
+      const float* tv = tri + 12 * (int64_t)(st + k);
+      int o;
+      memcpy(&o, tv + 3, 4);
+      if (o == own) continue;
+      *ntri += 1;
+      if (tri32(ox, oy, oz, dx, dy, dz, nD, tlo, thi, tv, tv + 4, tv + 8) == 1) return nv;
+    }
+    ref = sp ? stk[--sp] : 0xffffffffu;
+    if (ref == 0xffffffffu) break;
+  }
+  return nv;
+}
+
 /* Warp-packet replay of one work item: one DFS for all 32 lanes, each stack
  * entry carrying the mask of lanes whose segment enters that node; a node is
  * visited while some of its lanes are still undecided; at a leaf the lanes in
@@ -191,11 +312,13 @@ int main(int argc, char** argv) {
   double rays[2] = {0, 0}, tri_tests[2] = {0, 0}, n_it = 0, und = 0;
   double maxlane_sum = 0, nv_res[2] = {0, 0}, leaf_lane = 0;
   Pk pk = {0, 0, 0, 0};
+  double nv_free = 0, tri_free = 0, free_t_lo = 0, free_t_hi = 0;
   double uni_leaf = 0;
   for (int64_t it = 0; it < n_items; ++it) {
     const int64_t c = items[2 * it], tile = items[2 * it + 1];
     const float* p = lamps + 3 * c;
     const float ox = p[0], oy = p[1], oz = p[2];
+    const double rL = nearest(nodes, tri, root, v3(ox, oy, oz), NULL, -1);
     ++cur_stamp;
     if (cur_stamp == 0) { memset(hstamp, 0, sizeof(hstamp)); cur_stamp = 1; }
     double item_vis[MAXD] = {0};
@@ -212,6 +335,15 @@ int main(int argc, char** argv) {
       const float dx = cx - ox, dy = cy - oy, dz = cz - oz;
       const float ix = sinv(dx), iy = sinv(dy), iz = sinv(dz);
       const float tlo = 1e-4f / sqrtf(dx * dx + dy * dy + dz * dz), thi = 1.0f - tlo;
+      /* free regions: no triangle within rL of the lamp; none strictly in front of the target within rT */
+      {
+        const double len = sqrt((double)dx * dx + (double)dy * dy + (double)dz * dz);
+        const double rT = nearest(nodes, tri, root, v3(cx, cy, cz), nrm + 3 * r, (int)r);
+        free_t_lo += fmin(rL / len, 0.5);
+        free_t_hi += fmin(rT / len, 0.5);
+        const float tmin2 = (float)fmax(0.0, rL / len * 0.999), thi2 = (float)fmin(thi, 1.0 - rT / len * 0.999);
+        nv_free += replay(nodes, tri, root, ox, oy, oz, dx, dy, dz, tmin2, thi2, tlo, (int)r, &tri_free);
+      }
       const float nD = fabsf(dx) + fabsf(dy) + fabsf(dz);
       uint32_t stk[STK];
       int sp = 0, res = 0, undec = 0, nv = 0, ntri = 0;
@@ -287,6 +419,8 @@ int main(int argc, char** argv) {
   printf(" \"packet\": {\"node_steps_per_item\": %.3f, \"leaf_steps_per_item\": %.3f, \"tri_steps_per_item\": %.3f, \"lane_tri_tests_per_ray\": %.3f},\n",
          pk.node_steps / n_it, pk.leaf_steps / n_it, pk.tri_steps / n_it, pk.lane_tri / R);
   printf(" \"lanes_per_item\": %.3f,\n", R / n_it);
+  printf(" \"free_regions\": {\"visits_per_ray\": %.3f, \"tri_tests_per_ray\": %.3f, \"mean_t_cut_lamp\": %.4f, \"mean_t_cut_target\": %.4f},\n",
+         nv_free / R, tri_free / R, free_t_lo / R, free_t_hi / R);
   printf(" \"by_depth\": [");
   for (int d = 0, first = 1; d < MAXD; ++d) {
     if (lanes_d[d] == 0) continue;
