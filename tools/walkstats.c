@@ -202,6 +202,95 @@ static int replay(const Node* nodes, const float* tri, uint32_t root, float ox, 
   return nv;
 }
 
+/* any-hit walk returning the first certain-hit triangle (leaf order), -1 if none */
+static int64_t walk_hit(const Node* nodes, const float* tri, uint32_t root, float ox, float oy, float oz, float dx,
+                        float dy, float dz, int own) {
+  const float ix = sinv(dx), iy = sinv(dy), iz = sinv(dz), nD = fabsf(dx) + fabsf(dy) + fabsf(dz);
+  const float tlo = 1e-4f / sqrtf(dx * dx + dy * dy + dz * dz), thi = 1.0f - tlo;
+  uint32_t stk[STK];
+  int sp = 0;
+  uint32_t ref = root;
+  for (;;) {
+    while (!is_leaf(ref)) {
+      const Node* n = nodes + ref;
+      const float* bx[2] = {n->a, n->b};
+      float an[2], af[2];
+      for (int s = 0; s < 2; ++s) {
+        float x0 = (bx[s][0] - ox) * ix, x1 = (bx[s][1] - ox) * ix;
+        float y0 = (bx[s][2] - oy) * iy, y1 = (bx[s][3] - oy) * iy;
+        float z0 = (n->c[2 * s] - oz) * iz, z1 = (n->c[2 * s + 1] - oz) * iz;
+        an[s] = fmaxf(fmaxf(fminf(x0, x1), fminf(y0, y1)), fmaxf(fminf(z0, z1), 0.f));
+        af[s] = fminf(fminf(fmaxf(x0, x1), fmaxf(y0, y1)), fminf(fmaxf(z0, z1), thi));
+      }
+      const int h0 = an[0] <= af[0], h1 = an[1] <= af[1];
+      if (h0 && h1) {
+        const int sw = an[1] < an[0];
+        ref = sw ? n->d[1] : n->d[0];
+        stk[sp++] = sw ? n->d[0] : n->d[1];
+      } else if (h0 || h1) {
+        ref = h0 ? n->d[0] : n->d[1];
+      } else {
+        ref = sp ? stk[--sp] : 0xffffffffu;
+      }
+    }
+    if (ref == 0xffffffffu) return -1;
+    const uint32_t st = (ref & 0x7fffffffu) >> 3, cnt = (ref & 7u) + 1u;
+    for (uint32_t k = 0; k < cnt; ++k) {
+      const float* tv = tri + 12 * (int64_t)(st + k);
+      int o;
+      memcpy(&o, tv + 3, 4);
+      if (o == own) continue;
+      if (tri32(ox, oy, oz, dx, dy, dz, nD, tlo, thi, tv, tv + 4, tv + 8) == 1) return (int64_t)(st + k);
+    }
+    ref = sp ? stk[--sp] : 0xffffffffu;
+    if (ref == 0xffffffffu) return -1;
+  }
+}
+
+/* occluder hints: tiles processed for consecutive lamps; each patch remembers
+   the last occluder found for it (lag = how many lamps earlier it was found) */
+static void hint_sim(const Node* nodes, const float* tri, const float* cen, const float* nrm, const float* lamps,
+                     int64_t N, int64_t K, uint32_t root, int n_tiles, int n_cols, int lag) {
+  srand(12345);
+  double occl = 0, hit_lag = 0, tested = 0, clear_tested = 0;
+  for (int t = 0; t < n_tiles; ++t) {
+    const int64_t tile = (int64_t)(((double)rand() / RAND_MAX) * ((N + 31) / 32 - 1));
+    const int64_t c0 = (int64_t)(((double)rand() / RAND_MAX) * (K - n_cols - 1));
+    int64_t hist[64][32];  /* occluder found for lamp c (ring of 64), lane */
+    for (int a = 0; a < 64; ++a) for (int l = 0; l < 32; ++l) hist[a][l] = -1;
+    for (int64_t c = c0; c < c0 + n_cols; ++c) {
+      const float* p = lamps + 3 * c;
+      const float ox = p[0], oy = p[1], oz = p[2];
+      for (int l = 0; l < 32; ++l) {
+        const int64_t r = tile * 32 + l;
+        hist[c & 63][l] = -1;
+        if (r >= N) continue;
+        const float cx = cen[3 * r], cy = cen[3 * r + 1], cz = cen[3 * r + 2];
+        const double Dx = (double)cx - ox, Dy = (double)cy - oy, Dz = (double)cz - oz;
+        if (!(-(Dx * nrm[3 * r] + Dy * nrm[3 * r + 1] + Dz * nrm[3 * r + 2]) > 0.0)) continue;
+        const float dx = cx - ox, dy = cy - oy, dz = cz - oz;
+        const int64_t occ = walk_hit(nodes, tri, root, ox, oy, oz, dx, dy, dz, (int)r);
+        /* the most recent hint at least `lag` lamps old */
+        int64_t h = -1;
+        for (int64_t q = c - lag; q >= c0 && q > c - 64; --q)
+          if (hist[q & 63][l] >= 0) { h = hist[q & 63][l]; break; }
+        if (h >= 0) {
+          tested += 1;
+          const float* tv = tri + 12 * h;
+          const float tlo = 1e-4f / sqrtf(dx * dx + dy * dy + dz * dz), thi = 1.0f - tlo;
+          const int cls = tri32(ox, oy, oz, dx, dy, dz, fabsf(dx) + fabsf(dy) + fabsf(dz), tlo, thi, tv, tv + 4, tv + 8);
+          if (occ >= 0 && cls == 1) hit_lag += 1;
+          if (occ < 0) clear_tested += 1;
+        }
+        if (occ >= 0) occl += 1;
+        hist[c & 63][l] = occ;
+      }
+    }
+  }
+  printf(" \"hints_lag%d\": {\"occluded_rays\": %.0f, \"hint_hits\": %.0f, \"hint_hit_fraction_of_occluded\": %.4f, \"hint_tests\": %.0f, \"hint_tests_on_clear_rays\": %.0f},\n",
+         lag, occl, hit_lag, hit_lag / occl, tested, clear_tested);
+}
+
 /* Warp-packet replay of one work item: one DFS for all 32 lanes, each stack
  * entry carrying the mask of lanes whose segment enters that node; a node is
  * visited while some of its lanes are still undecided; at a leaf the lanes in
@@ -302,7 +391,7 @@ int main(int argc, char** argv) {
   const int64_t N = atoll(argv[7]), nn = atoll(argv[9]);
   const uint32_t root = (uint32_t)strtoul(argv[11], 0, 10);
   const int64_t n_items = atoll(argv[12]);
-  (void)argv[8]; (void)argv[10];
+  (void)argv[8];
   /* node depths (preorder: parents before children) */
   int* depth = (int*)calloc((size_t)nn, sizeof(int));
   for (int64_t i = 0; i < nn; ++i)
@@ -419,6 +508,11 @@ int main(int argc, char** argv) {
   printf(" \"packet\": {\"node_steps_per_item\": %.3f, \"leaf_steps_per_item\": %.3f, \"tri_steps_per_item\": %.3f, \"lane_tri_tests_per_ray\": %.3f},\n",
          pk.node_steps / n_it, pk.leaf_steps / n_it, pk.tri_steps / n_it, pk.lane_tri / R);
   printf(" \"lanes_per_item\": %.3f,\n", R / n_it);
+  {
+    const int64_t K = atoll(argv[10]);
+    hint_sim(nodes, tri, cen, nrm, lamps, N, K, root, 300, 48, 1);
+    hint_sim(nodes, tri, cen, nrm, lamps, N, K, root, 300, 48, 9);
+  }
   printf(" \"free_regions\": {\"visits_per_ray\": %.3f, \"tri_tests_per_ray\": %.3f, \"mean_t_cut_lamp\": %.4f, \"mean_t_cut_target\": %.4f},\n",
          nv_free / R, tri_free / R, free_t_lo / R, free_t_hi / R);
   printf(" \"by_depth\": [");
