@@ -86,6 +86,8 @@ def parse():
                     help="weak scaling: every rank assembles a fixed 1/8 of the C5 configurations "
                          "(total K = N x K/8), instead of a share of the fixed full problem")
     ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--no-bcast", action="store_true",
+                    help="N > 1: every rank builds the scene instead of rank 0 building and broadcasting it")
     return ap.parse_args()
 
 
@@ -326,7 +328,8 @@ def main():
         ev = ev_ph[i] if i is not None else None
         if ev:
             ev[0].record(stream)
-        sc = uvd.Scene(desc)                                  # a1, a2
+        # a1, a2: N > 1 builds once on rank 0 and broadcasts the scene image
+        sc = uvd.Scene(desc) if ws == 1 or args.no_bcast else shard.broadcast_scene(desc)
         if ev:
             ev[1].record(stream)
         lam, _ = sc.vantage(wl["vantage"])                    # a3
@@ -468,7 +471,9 @@ def main():
                            "precision": ("fp32 conservative box tests and fp32 triangle filter with forward "
                                          "error bounds; undecided rays re-traced with exact fp64 triangle tests; "
                                          "fp64 ray setup, front-face test and Eq. 7; A stored fp32"),
-                           "step": "scene_create+vantage+irradiance+fluence(A·t, A·1, Aᵀy)+coverage"},
+                           "step": "scene_create+vantage+irradiance+fluence(A·t, A·1, Aᵀy)+coverage",
+                           "scene_build": ("every rank" if ws == 1 or args.no_bcast else
+                                           "rank 0, broadcast as a uvd_scene_export image")},
                 "phases_ms": phases, "roofline": roofline, "roofline_a7": a7, "cpu_baseline": cpu,
                 "parity": parity_blk, "e2e": e2e, "gpu_launches": int(n_launch), "clocks": clk}
         print(json.dumps(line), flush=True)

@@ -154,6 +154,21 @@ UVD_API int uvd_scene_patches(const uvd_scene* scene, float* centroid, float* no
  * allocator), then frees them. */
 UVD_API void uvd_scene_destroy(uvd_scene* scene);
 
+/* Ship one scene build to other ranks (rank 0 builds, broadcasts).
+ * uvd_scene_export writes the scene into a flat DEVICE buffer of *bytes bytes
+ * on the scene's device (buf = NULL: *bytes receives the size; too small:
+ * UVD_ERR_CAPACITY with the size): patch attributes, leaf-ordered triangles,
+ * BVH nodes, front radii (and the 2.5D wall tables), not the octant node
+ * copies.  Synchronises `stream`.
+ * uvd_scene_import creates an independent scene on `device` from such a
+ * buffer (DEVICE memory on that device, e.g. after an NCCL broadcast): the
+ * same scene bit for bit (every call on it gives the results of the
+ * exporter), octant copies rebuilt locally.  INVALID for a buffer that is not
+ * a uvd_scene_export image.  Synchronises `stream`. */
+UVD_API int uvd_scene_export(const uvd_scene* scene, void* buf, size_t* bytes, void* stream);
+UVD_API int uvd_scene_import(const void* buf, size_t bytes, int device, void* stream,
+                             const uvd_allocator* allocator, uvd_scene** out);
+
 /* Introspection of the scene's BVH (a2), for structural tests and tree-quality
  * tools.  *n_nodes = max(M-1, 1), *root = the root reference (HOST).  nodes
  * (DEVICE, optional): n_nodes records of 64 B in depth-first preorder —

@@ -1258,6 +1258,30 @@ __global__ void k_max_depth(const int32_t* __restrict__ parent_leaf, const int32
   atomicMax(depth, d);
 }
 
+// Octant copies of the nodes (k_octant_nodes) unless they would take > 1/16 of
+// the device memory or UVD_OCT=0: the traversal then reads the one array
+// (min/max per slab).  Also used by uvd_scene_import (the copies are rebuilt
+// locally, not shipped).
+int build_octants(uvd_scene* s, cudaStream_t st) {
+  Alloc& al = s->alloc;
+  const int64_t nn = std::max<int64_t>(s->M - 1, 1);
+  if (s->onodes) al.put(s->onodes);
+  s->onodes = nullptr;
+  s->n_nodes = nn;
+  size_t free_b = 0, total_b = 0;
+  cudaMemGetInfo(&free_b, &total_b);
+  const char* e = getenv("UVD_OCT");
+  const bool want = !(e && atoi(e) == 0) && 8 * nn < ((int64_t)1 << 31) &&
+                    (double)(8 * nn * (int64_t)sizeof(Node)) <= (double)total_b / 16.0;
+  if (want) s->onodes = (Node*)al.get(8 * nn * sizeof(Node));  // nullptr (no memory): one array
+  if (s->onodes) {
+    k_octant_nodes<<<grid_for(8 * nn, 256), 256, 0, st>>>(s->nodes, nn, s->onodes);
+    note_launch();
+  }
+  UVD_CUDA_TRY(cudaGetLastError());
+  return UVD_OK;
+}
+
 #ifndef UVD_BVH_DEFAULT
 #define UVD_BVH_DEFAULT 2  // binned SAH; UVD_BVH=ploc / karras select the others
 #endif
@@ -1347,23 +1371,7 @@ int build_bvh(uvd_scene* s, float4* tri_in, uint32_t** order_out, cudaStream_t s
     note_launch();
     s->root = 0;
   }
-  {  // octant copies of the nodes (k_octant_nodes) unless they would take > 1/16 of the
-     // device memory or UVD_OCT=0: the traversal then reads the one array (min/max per slab)
-    const int64_t nn = std::max<int64_t>(M - 1, 1);
-    if (s->onodes) al.put(s->onodes);
-    s->onodes = nullptr;
-    s->n_nodes = nn;
-    size_t free_b = 0, total_b = 0;
-    cudaMemGetInfo(&free_b, &total_b);
-    const char* e = getenv("UVD_OCT");
-    const bool want = !(e && atoi(e) == 0) && 8 * nn < ((int64_t)1 << 31) &&
-                      (double)(8 * nn * (int64_t)sizeof(Node)) <= (double)total_b / 16.0;
-    if (want) s->onodes = (Node*)al.get(8 * nn * sizeof(Node));  // nullptr (no memory): one array
-    if (s->onodes) {
-      k_octant_nodes<<<grid_for(8 * nn, 256), 256, 0, st>>>(s->nodes, nn, s->onodes);
-      note_launch();
-    }
-  }
+  UVD_TRY(build_octants(s, st));
   UVD_CUDA_TRY(cudaGetLastError());
   if (order_out) {
     sc.keep(vals);  // ownership passes to the caller

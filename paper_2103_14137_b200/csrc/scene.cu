@@ -402,7 +402,9 @@ static int create_extruded(uvd_scene* s, const uvd_scene_desc* d, cudaStream_t s
   s->bbox[3] = b[2]; s->bbox[4] = b[3]; s->bbox[5] = d->wall_height;
   Alloc& al = s->alloc;
   s->walls = (Wall*)al.get(W.size() * sizeof(Wall));
-  s->poly_xy = (float*)al.get(std::max<size_t>(pxy.size(), 2) * sizeof(float));
+  s->n_poly_xy = (int64_t)std::max<size_t>(pxy.size(), 2);
+  s->poly_xy = (float*)al.get(s->n_poly_xy * sizeof(float));
+  s->n_poly_off = (int64_t)poff.size();
   s->poly_off = (int32_t*)al.get(poff.size() * sizeof(int32_t));
   float4* tri_in = (float4*)al.get(3 * s->M * sizeof(float4));
   s->ptri = tri_in;  // patch-ordered wall triangles (2 per patch) for the area model (NEXT-2)
@@ -579,5 +581,190 @@ extern "C" int uvd_scene_bvh(const uvd_scene* s, void* nodes, float* tri, int64_
   cudaStream_t st = (cudaStream_t)stream;
   if (nodes) UVD_CUDA_TRY(cudaMemcpyAsync(nodes, s->nodes, nn * sizeof(Node), cudaMemcpyDeviceToDevice, st));
   if (tri) UVD_CUDA_TRY(cudaMemcpyAsync(tri, s->tri, s->M * 3 * sizeof(float4), cudaMemcpyDeviceToDevice, st));
+  return UVD_OK;
+}
+
+// ------------------------------------------------------------ export/import --
+// One scene build shipped to the other ranks ("rank 0 builds and
+// runs ncclBroadcast of ≈112 MB").  A flat DEVICE buffer: a 256-B header, then
+// 256-B aligned sections (patch attributes, leaf-ordered triangles, BVH nodes,
+// front radii, and for 2.5D scenes the wall and polygon tables and the
+// patch-ordered wall triangles).  The octant node copies are rebuilt by the
+// importer (k_octant_nodes, ~0.2 ms on C5) instead of shipped (8x the nodes).
+namespace uvd {
+struct SceneHdr {
+  uint64_t magic;
+  int32_t version, kind;
+  int64_t N, M, n_nodes;
+  uint32_t root;
+  int32_t n_poly;
+  float bbox[6];
+  double total_area;
+  float bounds[4];
+  float wall_height;
+  int32_t has_ptri;
+  int64_t n_walls, n_poly_xy, n_poly_off;
+  uint64_t off[12];  // section offsets (bytes from the buffer start)
+  uint64_t total;
+};
+static_assert(sizeof(SceneHdr) <= 256, "scene header fits 256 B");
+constexpr uint64_t kSceneMagic = 0x3130646576557655ull;  // "UvUved01"
+enum { S_CEN, S_NRM, S_AREA, S_ORIG, S_TRI, S_NODES, S_FRONT, S_WALLS, S_PXY, S_POFF, S_PTRI, S_COUNT };
+
+static size_t al256(size_t x) { return (x + 255) & ~(size_t)255; }
+
+static void section_sizes(const SceneHdr& h, size_t sz[S_COUNT]) {
+  sz[S_CEN] = (size_t)h.N * 3 * sizeof(float);
+  sz[S_NRM] = (size_t)h.N * 3 * sizeof(float);
+  sz[S_AREA] = (size_t)h.N * sizeof(double);
+  sz[S_ORIG] = (size_t)h.N * sizeof(int64_t);
+  sz[S_TRI] = (size_t)h.M * 3 * sizeof(float4);
+  sz[S_NODES] = (size_t)h.n_nodes * sizeof(Node);
+  sz[S_FRONT] = (size_t)h.N * sizeof(float);
+  sz[S_WALLS] = (size_t)h.n_walls * sizeof(Wall);
+  sz[S_PXY] = (size_t)h.n_poly_xy * sizeof(float);
+  sz[S_POFF] = (size_t)h.n_poly_off * sizeof(int32_t);
+  sz[S_PTRI] = h.has_ptri ? (size_t)h.N * 2 * 3 * sizeof(float4) : 0;
+}
+
+static SceneHdr make_hdr(const uvd_scene* s) {
+  SceneHdr h;
+  memset(&h, 0, sizeof(h));
+  h.magic = kSceneMagic;
+  h.version = 1;
+  h.kind = s->kind;
+  h.N = s->N;
+  h.M = s->M;
+  h.n_nodes = s->n_nodes;
+  h.root = s->root;
+  h.n_poly = s->n_poly;
+  memcpy(h.bbox, s->bbox, sizeof(h.bbox));
+  h.total_area = s->total_area;
+  memcpy(h.bounds, s->bounds, sizeof(h.bounds));
+  h.wall_height = s->wall_height;
+  h.has_ptri = s->ptri != nullptr;
+  h.n_walls = s->walls ? s->n_walls : 0;
+  h.n_poly_xy = s->kind == UVD_SCENE_EXTRUDED ? s->n_poly_xy : 0;
+  h.n_poly_off = s->kind == UVD_SCENE_EXTRUDED ? s->n_poly_off : 0;
+  size_t sz[S_COUNT];
+  section_sizes(h, sz);
+  uint64_t o = 256;
+  for (int k = 0; k < S_COUNT; ++k) {
+    h.off[k] = o;
+    o += al256(sz[k]);
+  }
+  h.total = o;
+  return h;
+}
+}  // namespace uvd
+
+extern "C" int uvd_scene_export(const uvd_scene* s, void* buf, size_t* bytes, void* stream) {
+  clear_error();
+  if (!s || !bytes) { set_error("uvd_scene_export: null argument"); return UVD_ERR_INVALID; }
+  DeviceGuard dg(s->alloc.device);
+  NvtxRange nv("uvd_scene_export");
+  const SceneHdr h = make_hdr(s);
+  if (!buf) { *bytes = h.total; return UVD_OK; }
+  if (*bytes < h.total) {
+    set_error("uvd_scene_export: buffer of %zu bytes, need %llu", *bytes, (unsigned long long)h.total);
+    *bytes = h.total;
+    return UVD_ERR_CAPACITY;
+  }
+  cudaStream_t st = (cudaStream_t)stream;
+  char* b = (char*)buf;
+  size_t sz[S_COUNT];
+  section_sizes(h, sz);
+  const void* src[S_COUNT] = {s->centroid, s->normal, s->area, s->orig_id, s->tri, s->nodes, s->front_free,
+                              s->walls, s->poly_xy, s->poly_off, s->ptri};
+  UVD_CUDA_TRY(cudaMemcpyAsync(b, &h, sizeof(h), cudaMemcpyHostToDevice, st));
+  for (int k = 0; k < S_COUNT; ++k)
+    if (sz[k]) UVD_CUDA_TRY(cudaMemcpyAsync(b + h.off[k], src[k], sz[k], cudaMemcpyDeviceToDevice, st));
+  UVD_CUDA_TRY(cudaStreamSynchronize(st));  // the header is a stack variable
+  *bytes = h.total;
+  return UVD_OK;
+}
+
+extern "C" int uvd_scene_import(const void* buf, size_t bytes, int device, void* stream,
+                                const uvd_allocator* allocator, uvd_scene** out) {
+  clear_error();
+  if (!buf || !out) { set_error("uvd_scene_import: null argument"); return UVD_ERR_INVALID; }
+  *out = nullptr;
+  NvtxRange nv("uvd_scene_import");
+  int ndev = 0;
+  UVD_CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) { set_error("uvd_scene_import: no device %d", device); return UVD_ERR_INVALID; }
+  DeviceGuard dg(device);
+  cudaStream_t st = (cudaStream_t)stream;
+  SceneHdr h;
+  if (bytes < sizeof(h)) { set_error("uvd_scene_import: buffer too small"); return UVD_ERR_INVALID; }
+  UVD_CUDA_TRY(cudaMemcpyAsync(&h, buf, sizeof(h), cudaMemcpyDeviceToHost, st));
+  UVD_CUDA_TRY(cudaStreamSynchronize(st));
+  if (h.magic != kSceneMagic || h.version != 1 || h.total > bytes || h.N < 1 || h.M < 1 ||
+      (h.kind != UVD_SCENE_TRIMESH && h.kind != UVD_SCENE_EXTRUDED)) {
+    set_error("uvd_scene_import: not a uvd_scene_export buffer (or truncated)");
+    return UVD_ERR_INVALID;
+  }
+  const SceneHdr ref = [&] {  // the section layout the header must describe
+    SceneHdr r = h;
+    size_t sz[S_COUNT];
+    section_sizes(r, sz);
+    uint64_t o = 256;
+    for (int k = 0; k < S_COUNT; ++k) { r.off[k] = o; o += al256(sz[k]); }
+    r.total = o;
+    return r;
+  }();
+  if (memcmp(ref.off, h.off, sizeof(h.off)) != 0 || ref.total != h.total) {
+    set_error("uvd_scene_import: inconsistent section table");
+    return UVD_ERR_INVALID;
+  }
+  uvd_scene* s = new uvd_scene();
+  s->kind = h.kind;
+  s->alloc.device = device;
+  s->alloc.stream = st;
+  if (allocator && allocator->alloc && allocator->free) {
+    s->alloc.user = *allocator;
+    s->alloc.has_user = true;
+  }
+  s->N = h.N; s->M = h.M; s->n_nodes = h.n_nodes; s->root = h.root; s->n_poly = h.n_poly;
+  memcpy(s->bbox, h.bbox, sizeof(h.bbox));
+  s->total_area = h.total_area;
+  memcpy(s->bounds, h.bounds, sizeof(h.bounds));
+  s->wall_height = h.wall_height;
+  s->n_walls = h.n_walls;
+  s->n_poly_xy = h.n_poly_xy;
+  s->n_poly_off = h.n_poly_off;
+  size_t sz[S_COUNT];
+  section_sizes(h, sz);
+  void** dst[S_COUNT] = {(void**)&s->centroid, (void**)&s->normal, (void**)&s->area, (void**)&s->orig_id,
+                         (void**)&s->tri, (void**)&s->nodes, (void**)&s->front_free, (void**)&s->walls,
+                         (void**)&s->poly_xy, (void**)&s->poly_off, (void**)&s->ptri};
+  int rc = UVD_OK;
+  const char* b = (const char*)buf;
+  for (int k = 0; k < S_COUNT && rc == UVD_OK; ++k) {
+    if (!sz[k]) continue;
+    *dst[k] = s->alloc.get(sz[k]);
+    if (!*dst[k]) { set_error("uvd_scene_import: out of device memory"); rc = UVD_ERR_NOMEM; break; }
+    if (cudaMemcpyAsync(*dst[k], b + h.off[k], sz[k], cudaMemcpyDeviceToDevice, st) != cudaSuccess) {
+      set_error("uvd_scene_import: %s", cudaGetErrorString(cudaGetLastError()));
+      rc = UVD_ERR_CUDA;
+    }
+  }
+  if (rc == UVD_OK) rc = build_octants(s, st);
+  if (rc == UVD_OK) {
+    s->err_flag = (int*)s->alloc.get(sizeof(int));
+    if (!s->err_flag || !host_stage()) { set_error("uvd_scene_import: out of memory"); rc = UVD_ERR_NOMEM; }
+    else if (cudaMemsetAsync(s->err_flag, 0, sizeof(int), st) != cudaSuccess ||
+             cudaStreamSynchronize(st) != cudaSuccess) {
+      set_error("uvd_scene_import: %s", cudaGetErrorString(cudaGetLastError()));
+      rc = UVD_ERR_CUDA;
+    }
+  }
+  if (rc != UVD_OK) {
+    std::string msg = uvd_last_error();
+    free_scene(s);
+    set_error("%s", msg.c_str());
+    return rc;
+  }
+  *out = s;
   return UVD_OK;
 }

@@ -166,6 +166,7 @@ struct uvd_scene {
   float* poly_xy = nullptr;    // device, obstacles' vertices
   int32_t* poly_off = nullptr; // device, n_obstacles+1 offsets
   int32_t n_poly = 0;
+  int64_t n_poly_xy = 0, n_poly_off = 0;  // element counts of poly_xy / poly_off (export)
   float bounds[4] = {0, 0, 0, 0};
   float wall_height = 0.f;
   // in-kernel error flag (device int)
@@ -183,6 +184,7 @@ namespace uvd {
 void* host_stage();
 // launchers implemented in the .cu files
 int build_bvh(uvd_scene* s, float4* tri_in, uint32_t** order_out, cudaStream_t st);
+int build_octants(uvd_scene* s, cudaStream_t st);
 int sort_pairs_u64(uint64_t* keys, uint32_t* vals, int64_t n, Alloc& al, cudaStream_t st);
 // free.cu: empty regions at the segment ends (front radius per patch, lamp radius per sample)
 int front_radius(uvd_scene* s, cudaStream_t st);

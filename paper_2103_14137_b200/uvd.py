@@ -105,6 +105,9 @@ def lib():
                                         C.c_void_p]
         L.uvd_scene_bvh.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_int64),
                                     C.POINTER(C.c_uint32), C.c_void_p]
+        L.uvd_scene_export.argtypes = [C.c_void_p, C.c_void_p, C.POINTER(C.c_size_t), C.c_void_p]
+        L.uvd_scene_import.argtypes = [C.c_void_p, C.c_size_t, C.c_int, C.c_void_p, C.POINTER(_Allocator),
+                                       C.POINTER(C.c_void_p)]
         L.uvd_scene_destroy.argtypes = [C.c_void_p]
         L.uvd_scene_destroy.restype = None
         L.uvd_vantage_sample.argtypes = [C.c_void_p, C.POINTER(_VantageOpts), C.c_void_p, C.c_void_p,
@@ -131,6 +134,7 @@ def lib():
 
 
 EXPORTS = ("uvd_scene_create", "uvd_scene_query", "uvd_scene_patches", "uvd_scene_bvh", "uvd_scene_destroy",
+           "uvd_scene_export", "uvd_scene_import",
            "uvd_vantage_sample", "uvd_irradiance_matrix", "uvd_sync_status", "uvd_fluence",
            "uvd_coverage", "uvd_cubemap_matrix", "uvd_static_columns", "uvd_lp_solve", "uvd_last_error", "uvd_version", "uvd_launch_count")
 
@@ -187,9 +191,19 @@ class Scene:
     tris may be numpy arrays (host; the host->device copy is part of the call)
     or CUDA tensors (float32 (nv,3) / int32 (nt,3), already resident)."""
 
-    def __init__(self, desc: dict, device: int | None = None, stream=None, torch_allocator: bool = True):
+    def __init__(self, desc: dict | None, device: int | None = None, stream=None, torch_allocator: bool = True,
+                 _image: torch.Tensor | None = None):
         _require_cuda()
         self.device = torch.cuda.current_device() if device is None else device
+        if _image is not None:  # uvd_scene_import of a uvd_scene_export image
+            h = C.c_void_p()
+            self._alloc = _TORCH_ALLOCATOR if torch_allocator else None
+            with torch.cuda.device(self.device):
+                _check(lib().uvd_scene_import(_ptr(_image), _image.numel(), self.device, _stream(stream),
+                                              C.byref(self._alloc) if self._alloc else None, C.byref(h)))
+            self._h = h
+            self._query()
+            return
         d = _SceneDesc()
         keep = []
         if "vertices" in desc:
@@ -230,14 +244,32 @@ class Scene:
             _check(lib().uvd_scene_create(C.byref(d), self.device, _stream(stream),
                                           C.byref(self._alloc) if self._alloc else None, C.byref(h)))
         self._h = h
+        self._query()
+
+    def _query(self):
         n, m = C.c_int64(), C.c_int64()
         bb = (C.c_float * 6)()
         area = C.c_double()
-        _check(lib().uvd_scene_query(h, C.byref(n), C.byref(m), bb, C.byref(area)))
+        _check(lib().uvd_scene_query(self._h, C.byref(n), C.byref(m), bb, C.byref(area)))
         self.N, self.M = n.value, m.value
         self.bbox = np.array(bb[:], np.float32)
         self.total_area = area.value
-        self.kind = d.kind
+
+    def export(self, stream=None) -> torch.Tensor:
+        """uvd_scene_export: the scene as a flat uint8 CUDA tensor (for a broadcast)."""
+        nb = C.c_size_t()
+        _check(lib().uvd_scene_export(self.handle, None, C.byref(nb), _stream(stream)))
+        buf = torch.empty(nb.value, dtype=torch.uint8, device=f"cuda:{self.device}")
+        _check(lib().uvd_scene_export(self.handle, _ptr(buf), C.byref(nb), _stream(stream)))
+        return buf
+
+    @classmethod
+    def from_image(cls, image: torch.Tensor, device: int | None = None, stream=None,
+                   torch_allocator: bool = True) -> "Scene":
+        """uvd_scene_import: a scene from a Scene.export() image (uint8 CUDA tensor)."""
+        assert image.is_cuda and image.dtype == torch.uint8 and image.is_contiguous()
+        return cls(None, device=image.device.index if device is None else device, stream=stream,
+                   torch_allocator=torch_allocator, _image=image)
 
     @property
     def handle(self):

@@ -135,3 +135,42 @@ def test_fixup_list_export(uvd):
     r2 = sc.irradiance(lamps, cols=cols, fixups=5)
     assert r2["fixup_count"] == n and len(r2["fixups"]) == 5
     assert torch.equal(r2["A"], r["A"])
+
+
+@pytest.mark.parametrize("which", ["ward", "c2"])
+def test_scene_export_import_roundtrip(uvd, which):
+    """uvd_scene_export / uvd_scene_import (the multi-rank scene broadcast,
+    SURVEY §8e): the imported scene is the same scene — patches, BVH, vantage
+    samples, A, visibility bits and the fix-up list bit for bit — and a
+    corrupted image is refused."""
+    from synth import ward
+    if which == "ward":
+        desc, vo = ward.ward(seed=3, n_bays=1, e=0.2), configs.vopts(configs.FLOAT3D, 0.5, 0.05)
+    else:
+        c = configs.c2(6)
+        desc, vo = c["scene"], c["vantage"]
+    a = uvd.Scene(desc)
+    img = a.export()
+    b = uvd.Scene.from_image(img)
+    assert (a.N, a.M, a.total_area) == (b.N, b.M, b.total_area) and np.array_equal(a.bbox, b.bbox)
+    pa, pb = a.patches(), b.patches()
+    for k in pa:
+        assert torch.equal(pa[k], pb[k])
+    ba, bb = a.bvh(), b.bvh()
+    assert ba["root"] == bb["root"] and torch.equal(ba["nodes"], bb["nodes"]) and torch.equal(ba["tri"], bb["tri"])
+    la, ra = a.vantage(vo)
+    lb, rb = b.vantage(vo)
+    assert torch.equal(la, lb) and torch.equal(ra, rb)
+    xa = a.irradiance(la, vis_bits=True, fixups=1 << 16)
+    xb = b.irradiance(la, vis_bits=True, fixups=1 << 16)
+    a.sync_status()
+    b.sync_status()
+    assert torch.equal(xa["A"], xb["A"]) and torch.equal(xa["vis_bits"], xb["vis_bits"])
+    assert xa["fixup_count"] == xb["fixup_count"]
+    bad = img.clone()
+    bad[:8] = 0
+    with pytest.raises(uvd.UvdError) as e:
+        uvd.Scene.from_image(bad)
+    assert e.value.code == uvd.UVD_ERR_INVALID
+    with pytest.raises(uvd.UvdError):
+        uvd.Scene.from_image(img[:200].contiguous())

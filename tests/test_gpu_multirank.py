@@ -1,7 +1,8 @@
 """Multi-rank CUDA path: two processes on
 cuda:0 (the GPU pool is single-GPU) with a gloo process group, each calling
 libuvd on its block-cyclic column shard; the partial μ = A_r·t_r and A_r·𝟙 are
-summed by all_reduce.  Checks: every rank's A shard and visibility bits equal
+summed by all_reduce; the scene is built once (rank 0) and broadcast as a
+uvd_scene_export image (gloo broadcast of a CUDA tensor).  Checks: every rank's A shard and visibility bits equal
 the corresponding columns of a single-process assembly bit for bit, the
 reduced μ equals the single-process μ within 1e-12 relative (reduction order
 only), and coverage agrees.  Plus a torchrun dry run of bench.py's multi-rank
@@ -43,7 +44,7 @@ def _worker(rank, world, port, out):
     from paper_2103_14137_b200 import shard, uvd
     from synth import configs, vectors, ward
     desc = ward.ward(seed=2, n_bays=1, e=0.12)
-    sc = uvd.Scene(desc)
+    sc = shard.broadcast_scene(desc)  # rank 0 builds, the other rank imports the broadcast image
     lamps, _ = sc.vantage(configs.FLOAT_OPTS)
     K, N = lamps.shape[0], sc.N
     cols = shard.block_cyclic(K, world, rank, 32)
