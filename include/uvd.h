@@ -47,6 +47,9 @@
  *                             < 0 column-major (default: 9 when the traversal
  *                             data exceeds 2x the L2, else column-major)
  *   UVD_FIXUP_CAP=n           capacity of the exact re-trace list (tests only)
+ *   UVD_FREE=0                no empty end regions (free.cu) in the walk's box
+ *                             tests (dev A/B); UVD_FREE_CAP=r caps the front
+ *                             radius search at r m (default 0.1)
  *   UVD_LP_*                  PDHG tuning knobs of uvd_lp_solve (lp.cu; they
  *                             change the iterates, not the optimum)
  * The others never change a result: every setting gives bit-identical A and
