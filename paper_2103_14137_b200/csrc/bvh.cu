@@ -590,7 +590,7 @@ static inline unsigned grid_for(int64_t n, int t) { return (unsigned)((n + t - 1
 static int build_ploc(uvd_scene* s, int64_t M, int32_t* left, int32_t* right, int32_t* rf, int32_t* rl,
                       int32_t* pint, int32_t* pleaf, float* ibox, int* arrive, uint32_t* order,
                       cudaStream_t st) {
-  Alloc& al = s->alloc;
+  Scratch al(s->alloc, st);  // released at every exit
   float* cbA = (float*)al.get(M * 6 * sizeof(float));
   float* cbB = (float*)al.get(M * 6 * sizeof(float));
   int32_t* idA = (int32_t*)al.get(M * 4);
@@ -650,9 +650,6 @@ static int build_ploc(uvd_scene* s, int64_t M, int32_t* left, int32_t* right, in
   }
 #endif
   UVD_CUDA_TRY(cudaGetLastError());
-  for (void* p : {(void*)cbA, (void*)cbB, (void*)idA, (void*)idB, (void*)nn, (void*)keep, (void*)lead,
-                  (void*)ctr, (void*)tri2})
-    al.put(p);
   return UVD_OK;
 }
 
@@ -1105,7 +1102,7 @@ __global__ void k_gather_u32(const uint32_t* __restrict__ in, const int32_t* __r
 
 static int build_sah(uvd_scene* s, int64_t M, int32_t* left, int32_t* right, int32_t* rf, int32_t* rl,
                      int32_t* pint, int32_t* pleaf, float* ibox, int* arrive, uint32_t* order, cudaStream_t st) {
-  Alloc& al = s->alloc;
+  Scratch al(s->alloc, st);  // released at every exit
   // thresholds of the multi-CTA path; UVD_SAH_HUGE / UVD_SAH_CHUNK override them (tests
   // force the chunked path on small scenes with them)
   auto env_pos = [](const char* name, int dflt) {
@@ -1242,9 +1239,6 @@ static int build_sah(uvd_scene* s, int64_t M, int32_t* left, int32_t* right, int
   k_refit<<<grid_for(M, 256), 256, 0, st>>>(s->tri, M, left, right, pint, pleaf, ibox, arrive);
   note_launch();
   UVD_CUDA_TRY(cudaGetLastError());
-  for (void* p : {(void*)perm, (void*)tmp, (void*)la, (void*)lb, (void*)ba, (void*)bb, (void*)ha, (void*)hb,
-                  (void*)hs, (void*)ctr, (void*)tri2})
-    al.put(p);
   return UVD_OK;
 }
 

@@ -19,6 +19,18 @@
 typedef struct { float a[4], b[4], c[4]; uint32_t d[4]; } Node;
 #define MAXD 96
 #define STK 256
+#ifndef MARCH
+#define MARCH 24
+#endif
+#ifndef RT_CAP
+#define RT_CAP 0.1
+#endif
+#ifndef DEFICIT
+#define DEFICIT 0.0
+#endif
+#ifndef MARCH_EPS
+#define MARCH_EPS 0.02
+#endif
 
 static void* slurp(const char* path, size_t* n) {
   FILE* f = fopen(path, "rb");
@@ -291,6 +303,65 @@ static void hint_sim(const Node* nodes, const float* tri, const float* cen, cons
          lag, occl, hit_lag, hit_lag / occl, tested, clear_tested);
 }
 
+/* replay with a child ordering policy (for occluded rays the order decides how
+   soon a hit ends the walk): 0 near child first, 1 larger subtree first,
+   2 larger box surface area first, 3 far child first */
+static int replay_order(const Node* nodes, const int* nsub, const float* tri, uint32_t root, float ox, float oy, float oz,
+                        float dx, float dy, float dz, int own, int mode, int* hit_out) {
+  const float ix = sinv(dx), iy = sinv(dy), iz = sinv(dz), nD = fabsf(dx) + fabsf(dy) + fabsf(dz);
+  const float tlo = 1e-4f / sqrtf(dx * dx + dy * dy + dz * dz), thi = 1.0f - tlo;
+  uint32_t stk[STK];
+  int sp = 0, nv = 0;
+  uint32_t ref = root;
+  *hit_out = 0;
+  for (;;) {
+    while (!is_leaf(ref)) {
+      const Node* n = nodes + ref;
+      ++nv;
+      const float* bx[2] = {n->a, n->b};
+      float an[2], af[2], area[2];
+      for (int s = 0; s < 2; ++s) {
+        float x0 = (bx[s][0] - ox) * ix, x1 = (bx[s][1] - ox) * ix;
+        float y0 = (bx[s][2] - oy) * iy, y1 = (bx[s][3] - oy) * iy;
+        float z0 = (n->c[2 * s] - oz) * iz, z1 = (n->c[2 * s + 1] - oz) * iz;
+        an[s] = fmaxf(fmaxf(fminf(x0, x1), fminf(y0, y1)), fmaxf(fminf(z0, z1), 0.f));
+        af[s] = fminf(fminf(fmaxf(x0, x1), fmaxf(y0, y1)), fminf(fmaxf(z0, z1), thi));
+        const float ex = bx[s][1] - bx[s][0], ey = bx[s][3] - bx[s][2], ez = n->c[2 * s + 1] - n->c[2 * s];
+        area[s] = ex * ey + ey * ez + ez * ex;
+      }
+      const int h0 = an[0] <= af[0], h1 = an[1] <= af[1];
+      if (h0 && h1) {
+        int sw;
+        if (mode == 0) sw = an[1] < an[0];
+        else if (mode == 1) {
+          const int s0 = is_leaf(n->d[0]) ? (int)((n->d[0] & 7u) + 1u) : nsub[n->d[0]];
+          const int s1 = is_leaf(n->d[1]) ? (int)((n->d[1] & 7u) + 1u) : nsub[n->d[1]];
+          sw = s1 > s0;
+        } else if (mode == 2) sw = area[1] > area[0];
+        else sw = an[1] >= an[0];
+        ref = sw ? n->d[1] : n->d[0];
+        stk[sp++] = sw ? n->d[0] : n->d[1];
+      } else if (h0 || h1) {
+        ref = h0 ? n->d[0] : n->d[1];
+      } else {
+        ref = sp ? stk[--sp] : 0xffffffffu;
+      }
+    }
+    if (ref == 0xffffffffu) break;
+    const uint32_t st = (ref & 0x7fffffffu) >> 3, cnt = (ref & 7u) + 1u;
+    for (uint32_t k = 0; k < cnt; ++k) {
+      const float* tv = tri + 12 * (int64_t)(st + k);
+      int o;
+      memcpy(&o, tv + 3, 4);
+      if (o == own) continue;
+      if (tri32(ox, oy, oz, dx, dy, dz, nD, tlo, thi, tv, tv + 4, tv + 8) == 1) { *hit_out = 1; return nv; }
+    }
+    ref = sp ? stk[--sp] : 0xffffffffu;
+    if (ref == 0xffffffffu) break;
+  }
+  return nv;
+}
+
 /* Warp-packet replay of one work item: one DFS for all 32 lanes, each stack
  * entry carrying the mask of lanes whose segment enters that node; a node is
  * visited while some of its lanes are still undecided; at a leaf the lanes in
@@ -397,11 +468,18 @@ int main(int argc, char** argv) {
   for (int64_t i = 0; i < nn; ++i)
     for (int s = 0; s < 2; ++s)
       if (!is_leaf(nodes[i].d[s])) depth[nodes[i].d[s]] = depth[i] + 1;
+  int* nsub = (int*)calloc((size_t)nn, sizeof(int));
+  for (int64_t i = nn - 1; i >= 0; --i)
+    for (int s2 = 0; s2 < 2; ++s2) {
+      const uint32_t c = nodes[i].d[s2];
+      nsub[i] += is_leaf(c) ? (int)((c & 7u) + 1u) : nsub[c];
+    }
+  double ord_v[4][2] = {{0}}, ord_n[2] = {0, 0};
   double uni_d[MAXD] = {0}, lanes_d[MAXD] = {0};
   double rays[2] = {0, 0}, tri_tests[2] = {0, 0}, n_it = 0, und = 0;
   double maxlane_sum = 0, nv_res[2] = {0, 0}, leaf_lane = 0;
   Pk pk = {0, 0, 0, 0};
-  double nv_free = 0, tri_free = 0, free_t_lo = 0, free_t_hi = 0;
+  double nv_free = 0, tri_free = 0, free_t_lo = 0, free_t_hi = 0, march_steps = 0, march_free = 0, march_free_clear = 0, nv_march = 0, tri_march = 0;
   double uni_leaf = 0;
   for (int64_t it = 0; it < n_items; ++it) {
     const int64_t c = items[2 * it], tile = items[2 * it + 1];
@@ -485,6 +563,31 @@ int main(int argc, char** argv) {
       }
       rays[res] += 1;
       tri_tests[res] += ntri;
+      for (int mo = 0; mo < 4; ++mo) {
+        int h = 0;
+        ord_v[mo][res] += replay_order(nodes, nsub, tri, root, ox, oy, oz, dx, dy, dz, (int)r, mo, &h);
+      }
+      ord_n[res] += 1;
+      /* sphere tracing from the lamp with exact distances (upper bound of a distance-field march) */
+      {
+        const double len = sqrt((double)dx * dx + (double)dy * dy + (double)dz * dz);
+        const double rT2 = nearest(nodes, tri, root, v3(cx, cy, cz), nrm + 3 * r, (int)r);
+        double t = rL / len * 0.999;
+        const double tend = fmin((double)thi, 1.0 - fmin(rT2, RT_CAP) / len * 0.999);
+        int k = 0;
+        for (; k < MARCH && t < tend; ++k) {
+          const V3 x = v3(ox + t * dx, oy + t * dy, oz + t * dz);
+          const double dist = nearest(nodes, tri, root, x, NULL, -1) - DEFICIT;
+          if (dist < MARCH_EPS) break;
+          t += (dist - 1e-5) / len;
+        }
+        march_steps += k;
+        if (t >= tend) march_free += 1;
+        if (t >= tend && res == 0) march_free_clear += 1;
+        const float tm = (float)fmin(t, tend);
+        const float thi3 = (float)tend;
+        nv_march += t >= tend ? 0 : replay(nodes, tri, root, ox, oy, oz, dx, dy, dz, tm, thi3, tlo, (int)r, &tri_march);
+      }
       nv_res[res] += nv;
       und += undec;
       if (nv > maxlane) maxlane = nv;
@@ -508,6 +611,11 @@ int main(int argc, char** argv) {
   printf(" \"packet\": {\"node_steps_per_item\": %.3f, \"leaf_steps_per_item\": %.3f, \"tri_steps_per_item\": %.3f, \"lane_tri_tests_per_ray\": %.3f},\n",
          pk.node_steps / n_it, pk.leaf_steps / n_it, pk.tri_steps / n_it, pk.lane_tri / R);
   printf(" \"lanes_per_item\": %.3f,\n", R / n_it);
+  printf(" \"order_visits\": {\"near_first\": [%.2f, %.2f], \"larger_subtree\": [%.2f, %.2f], \"larger_area\": [%.2f, %.2f], \"far_first\": [%.2f, %.2f]},\n",
+         ord_v[0][0] / ord_n[0], ord_v[0][1] / ord_n[1], ord_v[1][0] / ord_n[0], ord_v[1][1] / ord_n[1],
+         ord_v[2][0] / ord_n[0], ord_v[2][1] / ord_n[1], ord_v[3][0] / ord_n[0], ord_v[3][1] / ord_n[1]);
+  printf(" \"march\": {\"max_steps\": %d, \"eps\": %.3f, \"steps_per_ray\": %.3f, \"fully_free_rays\": %.4f, \"fully_free_of_clear\": %.4f, \"visits_per_ray_after\": %.3f, \"tri_per_ray_after\": %.3f},\n",
+         MARCH, MARCH_EPS, march_steps / R, march_free / R, march_free_clear / rays[0], nv_march / R, tri_march / R);
   {
     const int64_t K = atoll(argv[10]);
     hint_sim(nodes, tri, cen, nrm, lamps, N, K, root, 300, 48, 1);

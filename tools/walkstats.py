@@ -40,7 +40,8 @@ def main():
     files["items"] = os.path.join(d, "items.bin")
     items.tofile(files["items"])
     exe = os.path.join(d, "walkstats")
-    subprocess.check_call(["gcc", "-O2", "-o", exe, os.path.join(ROOT, "tools", "walkstats.c"), "-lm"])
+    defs = [a for a in os.environ.get("WALKSTATS_DEFS", "").split() if a]
+    subprocess.check_call(["gcc", "-O2", *defs, "-o", exe, os.path.join(ROOT, "tools", "walkstats.c"), "-lm"])
     out = subprocess.check_output([exe, files["nodes"], files["tri"], files["cen"], files["nrm"], files["lamps"],
                                    files["items"], str(N), str(sc.M), str(b["nodes"].shape[0]), str(K),
                                    str(b["root"]), str(n_items)], text=True)
