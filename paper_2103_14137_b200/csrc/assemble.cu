@@ -248,15 +248,15 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmMinBlocks) k_assemble_lane(As
         // a4: ray p -> c in fp64 (exact differences of fp32 inputs), front-face cull
         const D3 D = d3((double)cx - (double)ox, (double)cy - (double)oy, (double)cz - (double)oz);
         const double dd = ddot3(D, D);
-        const double d = sqrt(dd);
         const double cosd = -(D.x * (double)nx + D.y * (double)ny + D.z * (double)nz);  // <p - c, n>
         front = cosd > 0.0;
-        if (d < kMinDist) {
+        if (dd < kMinDist * kMinDist) {
           atomicExch(P.err, 1);
           front = false;
         }
-        w = cosd / (dd * d);  // a6: Eq. 7 in fp64, added if the ray is clear
-        cosr = cosd - 1e-2 * d >= 0.0 ? 1.0 : 0.0;  // cos θ ≥ 1e-2 (no division)
+        const double ri = rsqrt(dd);  // 1/d (fp64, ~1 ulp): one square root instead of sqrt + division
+        w = cosd * (ri * ri * ri);    // a6: Eq. 7 in fp64, added if the ray is clear
+        cosr = cosd * ri >= 1e-2 ? 1.0 : 0.0;  // cos θ ≥ 1e-2
       }
       const float dx = cx - ox, dy = cy - oy, dz = cz - oz;
       if (front) {
@@ -501,7 +501,8 @@ __global__ void __launch_bounds__(kCscThreads) k_csc_fill(const AsmParams P, con
         const D3 D = d3((double)cx - (double)pl[0], (double)cy - (double)pl[1], (double)cz - (double)pl[2]);
         const double dd = ddot3(D, D);
         const double cosd = -(D.x * (double)nx + D.y * (double)ny + D.z * (double)nz);
-        acc += cosd / (dd * sqrt(dd));
+        const double ri = rsqrt(dd);  // Eq. 7 exactly as k_assemble_lane computes it
+        acc += cosd * (ri * ri * ri);
       }
       rowidx[o] = r;
       vals[o] = (float)(acc * P.scale);
@@ -590,6 +591,7 @@ __device__ void fixup_entry(const AsmParams& P, int64_t c, int r) {
     const D3 D = d3((double)cx - (double)ox, (double)cy - (double)oy, (double)cz - (double)oz);
     const double dd = ddot3(D, D);
     const double d = sqrt(dd);
+    const double ri = rsqrt(dd);  // Eq. 7 as in k_assemble_lane: cosd · (1/d)³
     const double cosd = -(D.x * (double)nx + D.y * (double)ny + D.z * (double)nz);
     bool vis;
     if (P.area_m >= 0) {  // NEXT-2: every sub-triangle re-traced exactly
@@ -612,8 +614,8 @@ __device__ void fixup_entry(const AsmParams& P, int64_t c, int r) {
         }
       }
     } else {
-      vis = cosd > 0.0 && d >= kMinDist && lane_clear_exact(P, ox, oy, oz, cx, cy, cz, r);
-      if (vis) acc += cosd / (dd * d);
+      vis = cosd > 0.0 && dd >= kMinDist * kMinDist && lane_clear_exact(P, ox, oy, oz, cx, cy, cz, r);
+      if (vis) acc += cosd * (ri * ri * ri);
     }
     if (P.vis_bits) {
       uint32_t* vw = P.vis_bits + (c * P.L + l) * P.words + word;

@@ -23,8 +23,14 @@ struct Ray32 {  // fp32 ray for slab tests: o + t*dir, t in [0, tmax]
   float ix, iy, iz;  // safe reciprocals of dir
 };
 
+// 1/d for slab tests: the hardware reciprocal (rcp.approx, relative error
+// <= 2^-23, one instruction instead of the ~8 of an IEEE division).  With the
+// FFMA's rounding a slab parameter is scaled by at most 1 + 1.5·2^-23, i.e. a
+// plane moves by <= 7 µm over a 40 m scene — inside the >= 10 µm box padding.
 __device__ __forceinline__ float safe_inv(float d) {
-  return fabsf(d) < 1e-30f ? copysignf(1e30f, d) : 1.0f / d;
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(d));
+  return fabsf(d) < 1e-30f ? copysignf(1e30f, d) : r;
 }
 
 __device__ __forceinline__ Ray32 make_ray32(float ox, float oy, float oz, float dx, float dy, float dz) {
