@@ -53,6 +53,9 @@ struct AsmParams {
   const float* __restrict__ lampc;  // [n_cols][L][3] lamps gathered per column (k_assemble_lane)
   const float* __restrict__ lamp_free;   // [n_cols][L] lamp radius r_L (free.cu), or nullptr
   const float* __restrict__ front_free;  // [N] front radius r_T (free.cu), or nullptr
+  const HNode* __restrict__ hnodes;      // 8 octant copies of the H nodes (hnodes.cu), or nullptr
+  int32_t n_h;
+  float hcx, hcy, hcz, hex, hey, hez;    // H coordinate origin and the scene's half extents
   int L;
   double scale;  // P / (4π L)
   const int64_t* __restrict__ cols;  // device, nullptr = identity
@@ -118,9 +121,51 @@ __device__ __forceinline__ int lane_walk32(const AsmParams& P, float ox, float o
                        ((__float_as_uint(iz) >> 31) << 2);
   // OCT = false: the scene has no octant copies (memory cap), one array, min/max per slab
   uint32_t ref = (!OCT || ref_is_leaf(P.root)) ? P.root : P.root + oct * (uint32_t)P.n_nodes;
+  // the top of the tree in fp16 (hnodes.cu) when this segment is in fp16 range:
+  // |1/d| <= 2048 per axis, the lamp inside the scene box; constants packed in
+  // half2 pairs (the HFMA2 operands select their halves)
+  __half2 hA = __float2half2_rn(0.f), hB = hA, hC = hA, hT = hA;
+  if (OCT && P.hnodes && fmaxf(fabsf(ix), fmaxf(fabsf(iy), fabsf(iz))) <= 2048.0f) {
+    const float orx = ox - P.hcx, ory = oy - P.hcy, orz = oz - P.hcz;
+    if (fabsf(orx) <= P.hex && fabsf(ory) <= P.hey && fabsf(orz) <= P.hez) {
+      const __half hix = __float2half_rn(ix), hiy = __float2half_rn(iy), hiz = __float2half_rn(iz);
+      hA = __halves2half2(hix, hiy);
+      hB = __halves2half2(hiz, __float2half_rn(-orx * __half2float(hix)));
+      hC = __halves2half2(__float2half_rn(-ory * __half2float(hiy)), __float2half_rn(-orz * __half2float(hiz)));
+      hT = __halves2half2(__float2half_rd(tmin), __float2half_ru(tmax));
+      ref = kHalfRef | (oct * (uint32_t)P.n_h);  // H root: H node 0 of this octant's copy
+    }
+  }
   for (;;) {
     // ---- inner nodes until this lane holds a leaf (or is done) ----
     while (!ref_is_leaf(ref)) {
+      if (OCT && (ref & kHalfRef)) {
+        // ---- H node: 32 bytes, both children per HFMA2 (hnodes.cu) ----
+        const uint4* hq = reinterpret_cast<const uint4*>(P.hnodes + (ref & ~kHalfRef));
+        const uint4 q0 = __ldg(hq), q1 = __ldg(hq + 1);
+        if (COUNT) { cnt[1] += 2; cnt[3] += 1; cnt[5] += 1; }
+        const __half2 tex = __hfma2(*reinterpret_cast<const __half2*>(&q0.x), __low2half2(hA), __high2half2(hB));
+        const __half2 txx = __hfma2(*reinterpret_cast<const __half2*>(&q0.y), __low2half2(hA), __high2half2(hB));
+        const __half2 tey = __hfma2(*reinterpret_cast<const __half2*>(&q0.z), __high2half2(hA), __low2half2(hC));
+        const __half2 txy = __hfma2(*reinterpret_cast<const __half2*>(&q0.w), __high2half2(hA), __low2half2(hC));
+        const __half2 tez = __hfma2(*reinterpret_cast<const __half2*>(&q1.x), __low2half2(hB), __high2half2(hC));
+        const __half2 txz = __hfma2(*reinterpret_cast<const __half2*>(&q1.y), __low2half2(hB), __high2half2(hC));
+        const __half2 en = __hmax2(__hmax2(tex, tey), __hmax2(tez, __low2half2(hT)));
+        const __half2 ex = __hmin2(__hmin2(txx, txy), __hmin2(txz, __high2half2(hT)));
+        const bool h0 = __hle(__low2half(en), __low2half(ex));
+        const bool h1 = __hle(__high2half(en), __high2half(ex));
+        if (h0 && h1) {
+          const bool swap = __hlt(__high2half(en), __low2half(en));  // near child first
+          ref = swap ? q1.w : q1.z;
+          if (sp < kLaneStack) stk[sp++] = swap ? q1.z : q1.w;
+          else atomicExch(P.err, 2);
+        } else if (h0 || h1) {
+          ref = h0 ? q1.z : q1.w;
+        } else {
+          ref = sp ? stk[--sp] : kDone;
+        }
+        continue;
+      }
       const Node* nd = (OCT ? P.onodes : P.nodes) + ref;
       const float4 na = __ldg(&nd->a), nb = __ldg(&nd->b), nc = __ldg(&nd->c);
       const uint2 ch = __ldg(reinterpret_cast<const uint2*>(&nd->d));
@@ -892,6 +937,12 @@ extern "C" int uvd_irradiance_matrix(const uvd_scene* s, const float* lamp_xyz, 
   P.vis_bits = out->vis_bits ? out->vis_bits : vis_scratch;
   P.lampc = nullptr;
   P.lamp_free = nullptr;
+  P.hnodes = s->hnodes;
+  P.n_h = s->n_h;
+  if (const char* e = getenv("UVD_HNODES")) if (atoi(e) == 0) P.hnodes = nullptr;  // dev A/B
+  P.hcx = s->hcenter[0]; P.hcy = s->hcenter[1]; P.hcz = s->hcenter[2];
+  P.hex = 0.5f * (s->bbox[3] - s->bbox[0]); P.hey = 0.5f * (s->bbox[4] - s->bbox[1]);
+  P.hez = 0.5f * (s->bbox[5] - s->bbox[2]);
   P.front_free = s->front_free;
   if (const char* e = getenv("UVD_FREE")) if (atoi(e) == 0) P.front_free = nullptr;  // dev A/B
   if (!area_model) {

@@ -1366,6 +1366,7 @@ int build_bvh(uvd_scene* s, float4* tri_in, uint32_t** order_out, cudaStream_t s
     s->root = 0;
   }
   UVD_TRY(build_octants(s, st));
+  UVD_TRY(build_hnodes(s, st));
   UVD_CUDA_TRY(cudaGetLastError());
   if (order_out) {
     sc.keep(vals);  // ownership passes to the caller

@@ -443,7 +443,7 @@ static void free_scene(uvd_scene* s) {
   Alloc& al = s->alloc;
   for (void* p : {(void*)s->centroid, (void*)s->normal, (void*)s->area, (void*)s->orig_id,
                   (void*)s->tri, (void*)s->nodes, (void*)s->walls, (void*)s->poly_xy,
-                  (void*)s->poly_off, (void*)s->err_flag, (void*)s->ptri, (void*)s->onodes, (void*)s->front_free})
+                  (void*)s->poly_off, (void*)s->err_flag, (void*)s->ptri, (void*)s->onodes, (void*)s->front_free, (void*)s->hnodes})
     al.put(p);
   for (auto& c : s->cov_part) al.put(c.p);
   cudaStreamSynchronize(al.stream);
@@ -750,6 +750,7 @@ extern "C" int uvd_scene_import(const void* buf, size_t bytes, int device, void*
     }
   }
   if (rc == UVD_OK) rc = build_octants(s, st);
+  if (rc == UVD_OK) rc = build_hnodes(s, st);
   if (rc == UVD_OK) {
     s->err_flag = (int*)s->alloc.get(sizeof(int));
     if (!s->err_flag || !host_stage()) { set_error("uvd_scene_import: out of memory"); rc = UVD_ERR_NOMEM; }

@@ -1,6 +1,7 @@
 // uvd_internal.cuh — shared internals of libuvd (CUDA path only; the oracle
 // under oracle/ shares nothing with this tree).
 #pragma once
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -71,6 +72,20 @@ struct __align__(16) Node {
   float4 c;  // child0 lo.z hi.z, child1 lo.z hi.z
   uint4 d;   // child0 ref, child1 ref, (unused), (unused)
 };
+
+// H node (hnodes.cu): the two child boxes of a top-level node as fp16 planes
+// relative to the scene centre, (child 0, child 1) pairs per plane in (entry,
+// exit) order for one ray octant — p[0..5] = entry x, exit x, entry y, exit y,
+// entry z, exit z — and the child refs (an H child carries kHalfRef)
+struct __align__(16) HNode {
+  __half2 p[6];
+  uint32_t ref[2];
+};
+constexpr uint32_t kHalfRef = 0x40000000u;  // internal ref into the H node copies
+#ifndef UVD_HDEPTH
+#define UVD_HDEPTH 6
+#endif
+constexpr int kHDepth = UVD_HDEPTH;          // H nodes: the nodes at depth <= kHDepth
 
 // ------------------------------------------------------------------ memory --
 struct Alloc {
@@ -159,6 +174,9 @@ struct uvd_scene {
   int64_t n_nodes = 0;
   uint32_t root = 0;          // root ref
   float* front_free = nullptr; // [N] front radius of every patch (free.cu)
+  uvd::HNode* hnodes = nullptr; // 8 octant copies of the H nodes (hnodes.cu), or nullptr
+  int32_t n_h = 0;              // H nodes per copy
+  float hcenter[3] = {0, 0, 0}; // origin of the H nodes' fp16 coordinates
   // 2.5D description (device + host copies) for the floorplan vantage test
   uvd::Wall* walls = nullptr;  // device
   int64_t n_walls = 0;
@@ -185,6 +203,7 @@ void* host_stage();
 // launchers implemented in the .cu files
 int build_bvh(uvd_scene* s, float4* tri_in, uint32_t** order_out, cudaStream_t st);
 int build_octants(uvd_scene* s, cudaStream_t st);
+int build_hnodes(uvd_scene* s, cudaStream_t st);
 int sort_pairs_u64(uint64_t* keys, uint32_t* vals, int64_t n, Alloc& al, cudaStream_t st);
 // free.cu: empty regions at the segment ends (front radius per patch, lamp radius per sample)
 int front_radius(uvd_scene* s, cudaStream_t st);
