@@ -331,19 +331,24 @@ __global__ void k_emit(const float4* __restrict__ tri, int64_t n, const int32_t*
 // Octant copies of the nodes: copy o (bit 0/1/2 = the ray's 1/d is negative in
 // x/y/z) stores every child box slab as (near plane, far plane) for rays of that
 // octant, so the traversal takes the slab entry and exit without a min/max per
-// axis.  Same boxes; internal child refs point into the same copy (+ o x nn).
+// axis, and pairs the two children's planes for the paired FMA (FFMA2):
+//   a = (x entry c0, x entry c1, x exit c0, x exit c1), b = the same for y,
+//   c = for z, d = child refs.
+// Same boxes; internal child refs point into the same copy (+ o x nn).
 __global__ void k_octant_nodes(const Node* __restrict__ nodes, int64_t nn, Node* __restrict__ onodes) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= 8 * nn) return;
   const int o = (int)(i / nn);
-  Node nd = nodes[i - o * nn];
-  float t;
-  if (o & 1) { t = nd.a.x; nd.a.x = nd.a.y; nd.a.y = t; t = nd.b.x; nd.b.x = nd.b.y; nd.b.y = t; }
-  if (o & 2) { t = nd.a.z; nd.a.z = nd.a.w; nd.a.w = t; t = nd.b.z; nd.b.z = nd.b.w; nd.b.w = t; }
-  if (o & 4) { t = nd.c.x; nd.c.x = nd.c.y; nd.c.y = t; t = nd.c.z; nd.c.z = nd.c.w; nd.c.w = t; }
-  if (!ref_is_leaf(nd.d.x)) nd.d.x += (uint32_t)(o * nn);
-  if (!ref_is_leaf(nd.d.y)) nd.d.y += (uint32_t)(o * nn);
-  onodes[i] = nd;
+  const Node nd = nodes[i - o * nn];
+  Node on;
+  const bool nx = o & 1, ny = o & 2, nz = o & 4;
+  on.a = nx ? make_float4(nd.a.y, nd.b.y, nd.a.x, nd.b.x) : make_float4(nd.a.x, nd.b.x, nd.a.y, nd.b.y);
+  on.b = ny ? make_float4(nd.a.w, nd.b.w, nd.a.z, nd.b.z) : make_float4(nd.a.z, nd.b.z, nd.a.w, nd.b.w);
+  on.c = nz ? make_float4(nd.c.y, nd.c.w, nd.c.x, nd.c.z) : make_float4(nd.c.x, nd.c.z, nd.c.y, nd.c.w);
+  on.d = nd.d;
+  if (!ref_is_leaf(on.d.x)) on.d.x += (uint32_t)(o * nn);
+  if (!ref_is_leaf(on.d.y)) on.d.y += (uint32_t)(o * nn);
+  onodes[i] = on;
 }
 
 // single-leaf scene (M <= kLeafMax): a root node with one leaf child and an

@@ -124,23 +124,29 @@ __device__ __forceinline__ int64_t cube_closest(const CubeParams& P, float ox, f
     const Node* nd = (OCT ? P.onodes : P.nodes) + ref;
     const float4 na = __ldg(&nd->a), nb = __ldg(&nd->b), nc = __ldg(&nd->c);
     const uint2 ch = __ldg(reinterpret_cast<const uint2*>(&nd->d));
-    const float ax0 = fmaf(na.x, ix, -oix), ax1 = fmaf(na.y, ix, -oix);
-    const float ay0 = fmaf(na.z, iy, -oiy), ay1 = fmaf(na.w, iy, -oiy);
-    const float az0 = fmaf(nc.x, iz, -oiz), az1 = fmaf(nc.y, iz, -oiz);
-    const float bx0 = fmaf(nb.x, ix, -oix), bx1 = fmaf(nb.y, ix, -oix);
-    const float by0 = fmaf(nb.z, iy, -oiy), by1 = fmaf(nb.w, iy, -oiy);
-    const float bz0 = fmaf(nc.z, iz, -oiz), bz1 = fmaf(nc.w, iz, -oiz);
     // no widening per node: fl(1/d), fl(d) and the FFMA's rounding move a plane by
     // <= 2^-22 |b - o| + 2^-24 |o| <= 1e-5 m for |coords| <= 20 m, inside the box
     // padding (k_assemble_lane's argument, plus the fp32 rounding of the direction);
     // tmax keeps its widening above ru(best) (ties go to the lower input index)
     float an, af, bn, bf;
-    if (OCT) {
-      an = fmaxf(fmaxf(ax0, ay0), fmaxf(az0, 0.0f));
-      af = fminf(fminf(ax1, ay1), fminf(az1, tmax));
-      bn = fmaxf(fmaxf(bx0, by0), fmaxf(bz0, 0.0f));
-      bf = fminf(fminf(bx1, by1), fminf(bz1, tmax));
+    if (OCT) {  // paired octant layout (bvh.cu k_octant_nodes): both children per FFMA2
+      const float2 ex = ffma2(make_float2(na.x, na.y), make_float2(ix, ix), make_float2(-oix, -oix));
+      const float2 xx = ffma2(make_float2(na.z, na.w), make_float2(ix, ix), make_float2(-oix, -oix));
+      const float2 ey = ffma2(make_float2(nb.x, nb.y), make_float2(iy, iy), make_float2(-oiy, -oiy));
+      const float2 xy = ffma2(make_float2(nb.z, nb.w), make_float2(iy, iy), make_float2(-oiy, -oiy));
+      const float2 ez = ffma2(make_float2(nc.x, nc.y), make_float2(iz, iz), make_float2(-oiz, -oiz));
+      const float2 xz = ffma2(make_float2(nc.z, nc.w), make_float2(iz, iz), make_float2(-oiz, -oiz));
+      an = fmaxf(fmaxf(ex.x, ey.x), fmaxf(ez.x, 0.0f));
+      af = fminf(fminf(xx.x, xy.x), fminf(xz.x, tmax));
+      bn = fmaxf(fmaxf(ex.y, ey.y), fmaxf(ez.y, 0.0f));
+      bf = fminf(fminf(xx.y, xy.y), fminf(xz.y, tmax));
     } else {
+      const float ax0 = fmaf(na.x, ix, -oix), ax1 = fmaf(na.y, ix, -oix);
+      const float ay0 = fmaf(na.z, iy, -oiy), ay1 = fmaf(na.w, iy, -oiy);
+      const float az0 = fmaf(nc.x, iz, -oiz), az1 = fmaf(nc.y, iz, -oiz);
+      const float bx0 = fmaf(nb.x, ix, -oix), bx1 = fmaf(nb.y, ix, -oix);
+      const float by0 = fmaf(nb.z, iy, -oiy), by1 = fmaf(nb.w, iy, -oiy);
+      const float bz0 = fmaf(nc.z, iz, -oiz), bz1 = fmaf(nc.w, iz, -oiz);
       an = fmaxf(fmaxf(fminf(ax0, ax1), fminf(ay0, ay1)), fmaxf(fminf(az0, az1), 0.0f));
       af = fminf(fminf(fmaxf(ax0, ax1), fmaxf(ay0, ay1)), fminf(fmaxf(az0, az1), tmax));
       bn = fmaxf(fmaxf(fminf(bx0, bx1), fminf(by0, by1)), fmaxf(fminf(bz0, bz1), 0.0f));

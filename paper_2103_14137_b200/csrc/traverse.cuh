@@ -33,6 +33,15 @@ __device__ __forceinline__ float safe_inv(float d) {
   return fabsf(d) < 1e-30f ? copysignf(1e30f, d) : r;
 }
 
+// Blackwell's paired FP32 FMA (FFMA2: one instruction, two IEEE fmas with the
+// same rounding as two FFMA); a scalar b / c is broadcast to both halves
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long ra = *reinterpret_cast<unsigned long long*>(&a), rb = *reinterpret_cast<unsigned long long*>(&b),
+                     rc = *reinterpret_cast<unsigned long long*>(&c), rd;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(rd) : "l"(ra), "l"(rb), "l"(rc));
+  return *reinterpret_cast<float2*>(&rd);
+}
+
 __device__ __forceinline__ Ray32 make_ray32(float ox, float oy, float oz, float dx, float dy, float dz) {
   Ray32 r;
   r.ox = ox; r.oy = oy; r.oz = oz;

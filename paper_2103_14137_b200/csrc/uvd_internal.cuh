@@ -71,7 +71,7 @@ struct __align__(16) Node {
   float4 b;  // child1 lo.x hi.x lo.y hi.y
   float4 c;  // child0 lo.z hi.z, child1 lo.z hi.z
   uint4 d;   // child0 ref, child1 ref, (unused), (unused)
-};
+};  // (the octant copies, bvh.cu k_octant_nodes, pair the children's planes instead)
 
 // H node (hnodes.cu): the two child boxes of a top-level node as fp16 planes
 // relative to the scene centre, (child 0, child 1) pairs per plane in (entry,
