@@ -450,6 +450,145 @@ static void packet_item(const Node* nodes, const float* tri, const float* cen, c
   }
 }
 
+
+/* ---- beam (frustum) replay: one conservative pyramid per work item (apex at
+ * the lamp, side planes bounding the 32 target directions, near/far caps from
+ * the trimmed segment ends); a DFS of the BVH against it collects candidate
+ * leaves; then every lane slab-tests its own segment against the candidate
+ * leaf boxes (near first) and tests the triangles of the leaves it enters. */
+typedef struct { double items, fallback, fr_nodes, cand_leaves, lane_box, lane_tri, lanes, cand_hist[8]; } Bm;
+static double lin_min(const double w[3], double c, const float lo[3], const float hi[3], V3 L) {
+  /* min over the box of w·(x − L) − c */
+  double m = -c;
+  const double l[3] = {lo[0] - L.x, lo[1] - L.y, lo[2] - L.z}, h[3] = {hi[0] - L.x, hi[1] - L.y, hi[2] - L.z};
+  for (int k = 0; k < 3; ++k) m += fmin(w[k] * l[k], w[k] * h[k]);
+  return m;
+}
+static void beam_item(const Node* nodes, const float* tri, const float* cen, const float* nrm, int64_t N, uint32_t root,
+                      float ox, float oy, float oz, double rL, int64_t tile, Bm* bm) {
+  double D[32][3], tmn[32], tmx[32];
+  int live[32], nl = 0;
+  V3 L = v3(ox, oy, oz);
+  double ax[3] = {0, 0, 0};
+  for (int l = 0; l < 32; ++l) {
+    live[l] = 0;
+    const int64_t r = tile * 32 + l;
+    if (r >= N) continue;
+    const double Dx = (double)cen[3 * r] - ox, Dy = (double)cen[3 * r + 1] - oy, Dz = (double)cen[3 * r + 2] - oz;
+    if (!(-(Dx * nrm[3 * r] + Dy * nrm[3 * r + 1] + Dz * nrm[3 * r + 2]) > 0.0)) continue;
+    const double len = sqrt(Dx * Dx + Dy * Dy + Dz * Dz);
+    const double rT = fmin(nearest(nodes, tri, root, v3(cen[3 * r], cen[3 * r + 1], cen[3 * r + 2]), nrm + 3 * r, (int)r), RT_CAP);
+    D[l][0] = Dx; D[l][1] = Dy; D[l][2] = Dz;
+    tmn[l] = fmin(rL, 2.0) / len * 0.999;
+    tmx[l] = fmin(1.0 - 1e-4 / len, 1.0 - rT / len * 0.999);
+    ax[0] += Dx / len; ax[1] += Dy / len; ax[2] += Dz / len;
+    live[l] = 1;
+    ++nl;
+  }
+  if (!nl) return;
+  bm->items += 1;
+  double an = sqrt(ax[0] * ax[0] + ax[1] * ax[1] + ax[2] * ax[2]);
+  for (int k = 0; k < 3; ++k) ax[k] /= an;
+  /* e1, e2 perpendicular to the axis */
+  double e1[3], e2[3];
+  { double t[3] = {fabs(ax[0]) < 0.9 ? 1.0 : 0.0, fabs(ax[0]) < 0.9 ? 0.0 : 1.0, 0.0};
+    double d = t[0] * ax[0] + t[1] * ax[1] + t[2] * ax[2];
+    for (int k = 0; k < 3; ++k) e1[k] = t[k] - d * ax[k];
+    double n1 = sqrt(e1[0] * e1[0] + e1[1] * e1[1] + e1[2] * e1[2]);
+    for (int k = 0; k < 3; ++k) e1[k] /= n1;
+    e2[0] = ax[1] * e1[2] - ax[2] * e1[1]; e2[1] = ax[2] * e1[0] - ax[0] * e1[2]; e2[2] = ax[0] * e1[1] - ax[1] * e1[0]; }
+  double s1lo = 1e300, s1hi = -1e300, s2lo = 1e300, s2hi = -1e300, hlo = 1e300, hhi = -1e300;
+  int bad = 0;
+  for (int l = 0; l < 32; ++l) {
+    if (!live[l]) continue;
+    const double h = D[l][0] * ax[0] + D[l][1] * ax[1] + D[l][2] * ax[2];
+    if (h <= 1e-3 * sqrt(D[l][0] * D[l][0] + D[l][1] * D[l][1] + D[l][2] * D[l][2])) { bad = 1; break; }
+    const double p1 = (D[l][0] * e1[0] + D[l][1] * e1[1] + D[l][2] * e1[2]) / h;
+    const double p2 = (D[l][0] * e2[0] + D[l][1] * e2[1] + D[l][2] * e2[2]) / h;
+    s1lo = fmin(s1lo, p1); s1hi = fmax(s1hi, p1); s2lo = fmin(s2lo, p2); s2hi = fmax(s2hi, p2);
+    hlo = fmin(hlo, h * tmn[l]); hhi = fmax(hhi, h * tmx[l]);
+  }
+  if (bad || s1hi - s1lo > 4.0 || s2hi - s2lo > 4.0) { bm->fallback += 1; return; }
+  bm->lanes += nl;
+  const double pad = 1e-4;
+  /* half-spaces w·y <= c (y = x − L): p1 − s1hi h <= 0, s1lo h − p1 <= 0, same for 2, h <= hhi, −h <= −hlo */
+  double W[6][3], C[6];
+  for (int k = 0; k < 3; ++k) {
+    W[0][k] = e1[k] - s1hi * ax[k]; W[1][k] = s1lo * ax[k] - e1[k];
+    W[2][k] = e2[k] - s2hi * ax[k]; W[3][k] = s2lo * ax[k] - e2[k];
+    W[4][k] = ax[k]; W[5][k] = -ax[k];
+  }
+  for (int q = 0; q < 4; ++q) { double n = sqrt(W[q][0] * W[q][0] + W[q][1] * W[q][1] + W[q][2] * W[q][2]); for (int k = 0; k < 3; ++k) W[q][k] /= n; C[q] = pad; }
+  C[4] = hhi + pad; C[5] = -hlo + pad;
+  /* DFS */
+  uint32_t stk[STK];
+  float cl[4096][6];
+  uint32_t cr[4096];
+  double ch[4096];
+  int nc = 0, sp = 0;
+  uint32_t ref = root;
+  for (;;) {
+    if (!is_leaf(ref)) {
+      const Node* n = nodes + ref;
+      bm->fr_nodes += 1;
+      for (int s = 0; s < 2; ++s) {
+        const float lo[3] = {s ? n->b[0] : n->a[0], s ? n->b[2] : n->a[2], n->c[2 * s]};
+        const float hi[3] = {s ? n->b[1] : n->a[1], s ? n->b[3] : n->a[3], n->c[2 * s + 1]};
+        if (lo[0] > hi[0]) continue;
+        int out = 0;
+        for (int q = 0; q < 6 && !out; ++q) out = lin_min(W[q], C[q], lo, hi, L) > 0;
+        if (out) continue;
+        const uint32_t c = n->d[s];
+        if (is_leaf(c)) {
+          if (nc < 4096) {
+            for (int k = 0; k < 3; ++k) { cl[nc][2 * k] = lo[k]; cl[nc][2 * k + 1] = hi[k]; }
+            cr[nc] = c;
+            ch[nc] = ((lo[0] + hi[0]) * 0.5 - ox) * ax[0] + ((lo[1] + hi[1]) * 0.5 - oy) * ax[1] + ((lo[2] + hi[2]) * 0.5 - oz) * ax[2];
+            ++nc;
+          }
+        } else {
+          stk[sp++] = c;
+        }
+      }
+    }
+    if (!sp) break;
+    ref = stk[--sp];
+  }
+  bm->cand_leaves += nc;
+  { int b = nc < 4 ? 0 : nc < 8 ? 1 : nc < 16 ? 2 : nc < 32 ? 3 : nc < 64 ? 4 : nc < 128 ? 5 : nc < 256 ? 6 : 7; bm->cand_hist[b] += 1; }
+  /* sort candidates near first (insertion sort) */
+  int ord[4096];
+  for (int i = 0; i < nc; ++i) ord[i] = i;
+  for (int i = 1; i < nc; ++i) { int v = ord[i], j = i - 1; while (j >= 0 && ch[ord[j]] > ch[v]) { ord[j + 1] = ord[j]; --j; } ord[j + 1] = v; }
+  for (int l = 0; l < 32; ++l) {
+    if (!live[l]) continue;
+    const int64_t r = tile * 32 + l;
+    const float dx = (float)D[l][0], dy = (float)D[l][1], dz = (float)D[l][2];
+    const float ix = sinv(dx), iy = sinv(dy), iz = sinv(dz), nD = fabsf(dx) + fabsf(dy) + fabsf(dz);
+    const float tlo = 1e-4f / sqrtf(dx * dx + dy * dy + dz * dz), thi = (float)tmx[l], tmin = (float)tmn[l];
+    for (int q = 0; q < nc; ++q) {
+      const float* b = cl[ord[q]];
+      bm->lane_box += 1;
+      float x0 = (b[0] - ox) * ix, x1 = (b[1] - ox) * ix, y0 = (b[2] - oy) * iy, y1 = (b[3] - oy) * iy;
+      float z0 = (b[4] - oz) * iz, z1 = (b[5] - oz) * iz;
+      float a0 = fmaxf(fmaxf(fminf(x0, x1), fminf(y0, y1)), fmaxf(fminf(z0, z1), tmin));
+      float a1 = fminf(fminf(fmaxf(x0, x1), fmaxf(y0, y1)), fminf(fmaxf(z0, z1), thi));
+      if (a0 > a1) continue;
+      const uint32_t c = cr[ord[q]], st = (c & 0x7fffffffu) >> 3, cnt = (c & 7u) + 1u;
+      int hit = 0;
+      for (uint32_t k = 0; k < cnt; ++k) {
+        const float* tv = tri + 12 * (int64_t)(st + k);
+        int own;
+        memcpy(&own, tv + 3, 4);
+        if (own == (int)r) continue;
+        bm->lane_tri += 1;
+        if (tri32(ox, oy, oz, dx, dy, dz, nD, tlo, 1.0f - tlo, tv, tv + 4, tv + 8) == 1) { hit = 1; break; }
+      }
+      if (hit) break;
+    }
+  }
+}
+
 int main(int argc, char** argv) {
   if (argc < 13) { fprintf(stderr, "usage\n"); return 1; }
   size_t sz;
@@ -479,6 +618,8 @@ int main(int argc, char** argv) {
   double rays[2] = {0, 0}, tri_tests[2] = {0, 0}, n_it = 0, und = 0;
   double maxlane_sum = 0, nv_res[2] = {0, 0}, leaf_lane = 0;
   Pk pk = {0, 0, 0, 0};
+  Bm bm;
+  memset(&bm, 0, sizeof(bm));
   double nv_free = 0, tri_free = 0, free_t_lo = 0, free_t_hi = 0, march_steps = 0, march_free = 0, march_free_clear = 0, nv_march = 0, tri_march = 0;
   double uni_leaf = 0;
   for (int64_t it = 0; it < n_items; ++it) {
@@ -491,6 +632,7 @@ int main(int argc, char** argv) {
     double item_vis[MAXD] = {0};
     int any = 0, maxlane = 0;
     packet_item(nodes, tri, cen, nrm, N, root, ox, oy, oz, tile, &pk);
+    beam_item(nodes, tri, cen, nrm, N, root, ox, oy, oz, rL, tile, &bm);
     for (int lane = 0; lane < 32; ++lane) {
       const int64_t r = tile * 32 + lane;
       if (r >= N) continue;
@@ -611,6 +753,10 @@ int main(int argc, char** argv) {
   printf(" \"packet\": {\"node_steps_per_item\": %.3f, \"leaf_steps_per_item\": %.3f, \"tri_steps_per_item\": %.3f, \"lane_tri_tests_per_ray\": %.3f},\n",
          pk.node_steps / n_it, pk.leaf_steps / n_it, pk.tri_steps / n_it, pk.lane_tri / R);
   printf(" \"lanes_per_item\": %.3f,\n", R / n_it);
+  printf(" \"beam\": {\"items\": %.0f, \"fallback_items\": %.0f, \"frustum_nodes_per_item\": %.2f, \"cand_leaves_per_item\": %.2f, \"lane_leaf_box_tests_per_ray\": %.2f, \"lane_tri_tests_per_ray\": %.3f, \"cand_hist_lt4_8_16_32_64_128_256_more\": [%.0f, %.0f, %.0f, %.0f, %.0f, %.0f, %.0f, %.0f]},\n",
+         bm.items, bm.fallback, bm.fr_nodes / (bm.items - bm.fallback), bm.cand_leaves / (bm.items - bm.fallback),
+         bm.lane_box / bm.lanes, bm.lane_tri / bm.lanes, bm.cand_hist[0], bm.cand_hist[1], bm.cand_hist[2], bm.cand_hist[3],
+         bm.cand_hist[4], bm.cand_hist[5], bm.cand_hist[6], bm.cand_hist[7]);
   printf(" \"order_visits\": {\"near_first\": [%.2f, %.2f], \"larger_subtree\": [%.2f, %.2f], \"larger_area\": [%.2f, %.2f], \"far_first\": [%.2f, %.2f]},\n",
          ord_v[0][0] / ord_n[0], ord_v[0][1] / ord_n[1], ord_v[1][0] / ord_n[0], ord_v[1][1] / ord_n[1],
          ord_v[2][0] / ord_n[0], ord_v[2][1] / ord_n[1], ord_v[3][0] / ord_n[0], ord_v[3][1] / ord_n[1]);
