@@ -50,10 +50,15 @@
  *   UVD_FREE=0                no empty end regions (free.cu) in the walk's box
  *                             tests (dev A/B); UVD_FREE_CAP=r caps the front
  *                             radius search at r m (default 0.1)
+ *   UVD_HNODES=0              the walk skips the fp16 copies of the top BVH
+ *                             levels (hnodes.cu; dev A/B); UVD_HDEPTH=d builds
+ *                             them for depth <= d (default 6, read by
+ *                             uvd_scene_create / uvd_scene_import)
  *   UVD_LP_*                  PDHG tuning knobs of uvd_lp_solve (lp.cu; they
  *                             change the iterates, not the optimum)
  * The others never change a result: every setting gives bit-identical A and
- * visibility bits (tests/test_gpu_order.py, tests/test_gpu_bvh.py).
+ * visibility bits (tests/test_gpu_order.py, tests/test_gpu_bvh.py,
+ * tests/test_gpu_hnodes.py).
  */
 #ifndef UVD_H_
 #define UVD_H_
