@@ -298,7 +298,9 @@ typedef struct {
  * lamp_xyz: DEVICE [k_total * L * 3] (configuration j -> samples j*L .. j*L+L-1).
  * cols: HOST [n_cols] global configuration ids of this call's columns (local
  * column c <-> cols[c]); NULL means all, n_cols = k_total.  Asynchronous;
- * call uvd_sync_status to collect in-kernel DOMAIN errors.
+ * call uvd_sync_status to collect in-kernel DOMAIN errors and the lamp-range
+ * check (every lamp coordinate finite and within the scene's largest
+ * |coordinate| + 50 m).
  * UVD_MODEL_AREA (NEXT-2): dense output only (CSC returns INVALID); vis_bits
  * bit = some sub-triangle of the patch seen from lamp sample l. */
 UVD_API int uvd_irradiance_matrix(const uvd_scene* scene, const float* lamp_xyz, int64_t k_total,
@@ -307,7 +309,10 @@ UVD_API int uvd_irradiance_matrix(const uvd_scene* scene, const float* lamp_xyz,
 
 /* Synchronise `stream` and report the scene's in-kernel error flag, read and
  * cleared in one device atomic: UVD_OK, UVD_ERR_DOMAIN (a lamp–centroid
- * distance < 1e-9 m), or UVD_ERR_CUDA for a traversal-stack overflow (cannot
+ * distance < 1e-9 m), UVD_ERR_INVALID (a lamp coordinate of uvd_irradiance_matrix
+ * non-finite or beyond the scene's largest |coordinate| + 50 m, the range the
+ * BVH's fp32 box padding covers; the matrix is then not trusted), or
+ * UVD_ERR_CUDA for a traversal-stack overflow (cannot
  * happen: scene creation refuses BVHs deeper than 62 levels with
  * UVD_ERR_INVALID).  The flag is per SCENE, not per stream: the call reports
  * errors raised by any assembly on this scene, on any stream, that completed

@@ -23,6 +23,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cmath>
 #include <cstdlib>
 
 #include "traverse.cuh"
@@ -810,6 +811,22 @@ __global__ void k_gather_lamps(const AsmParams P, float* __restrict__ out) {
   }
 }
 
+// The walk's conservativeness rests on the box padding (bvh.cu pad_lo/hi:
+// 1e-5 m + 1e-6|x| + 4·2^-24·max|scene coordinate|) covering the slab
+// rounding, which grows with |lamp| (plane shift <= 1.5·2^-23 |o| beyond the
+// scene's own terms): valid for lamp coordinates within the scene's largest
+// |coordinate| + 50 m.  Lamps outside that (or non-finite) raise flag 3, which
+// uvd_sync_status reports as UVD_ERR_INVALID — the matrix is not trusted then.
+__global__ void k_check_lamps(const float* __restrict__ lamps, const int64_t* __restrict__ cols, int64_t n_cols,
+                              int L, float bound, int* __restrict__ err) {
+  const int64_t per = 3 * (int64_t)L, n = n_cols * per;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t c = i / per, q = i - c * per;
+    const float v = lamps[(cols ? cols[c] : c) * per + q];
+    if (!(fabsf(v) <= bound)) atomicExch(err, 3);
+  }
+}
+
 // persistent grids (occupancy x SMs), cached per device and kernel
 template <typename K>
 static int persistent_grid(K kernel, int threads, int dev, int* cache) {
@@ -953,6 +970,14 @@ extern "C" int uvd_irradiance_matrix(const uvd_scene* s, const float* lamp_xyz, 
   P.hez = 0.5f * (s->bbox[5] - s->bbox[2]);
   P.front_free = s->front_free;
   if (const char* e = getenv("UVD_FREE")) if (atoi(e) == 0) P.front_free = nullptr;  // dev A/B
+  {  // lamps inside the range the box padding covers (k_check_lamps)
+    float maxc = 0.f;
+    for (int k = 0; k < 6; ++k) maxc = std::max(maxc, std::fabs(s->bbox[k]));
+    const int64_t n = n_cols * P.L * 3;
+    k_check_lamps<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 1024)), 256, 0, st>>>(
+        lamp_xyz, dcols, n_cols, P.L, maxc + 50.0f, s->err_flag);
+    note_launch();
+  }
   if (!area_model) {
     float* lampc = (float*)sc.get((size_t)n_cols * P.L * 3 * sizeof(float));
     if (!lampc) { set_error("uvd_irradiance_matrix: out of device memory"); return UVD_ERR_NOMEM; }

@@ -559,6 +559,11 @@ extern "C" int uvd_sync_status(const uvd_scene* s, void* stream) {
       set_error("traversal stack overflow (BVH deeper than 64)");
       return UVD_ERR_CUDA;
     }
+    if (flag == 3) {  // assemble.cu k_check_lamps
+      set_error("lamp sample outside the validated range (|coordinate| > the scene's largest + 50 m, or "
+                "non-finite): the box padding does not cover its rounding");
+      return UVD_ERR_INVALID;
+    }
     set_error("lamp–centroid distance below 1e-9 m (S:160)");
     return UVD_ERR_DOMAIN;
   }

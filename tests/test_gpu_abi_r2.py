@@ -174,3 +174,22 @@ def test_scene_export_import_roundtrip(uvd, which):
     assert e.value.code == uvd.UVD_ERR_INVALID
     with pytest.raises(uvd.UvdError):
         uvd.Scene.from_image(img[:200].contiguous())
+
+
+def test_lamp_outside_padding_range_is_reported(uvd):
+    """A lamp farther than the scene's largest coordinate + 50 m (beyond what
+    the fp32 box padding covers) or non-finite makes uvd_sync_status return
+    INVALID; lamps inside the range do not."""
+    c = configs.c2(2)
+    sc = uvd.Scene(c["scene"])
+    lamps, _ = sc.vantage(c["vantage"])
+    sc.irradiance(lamps)
+    sc.sync_status()
+    for bad in (1000.0, float("nan")):
+        far = lamps.clone()
+        far[3, 0, 2] = bad
+        sc.irradiance(far)
+        with pytest.raises(Exception, match="validated range"):
+            sc.sync_status()
+        sc.sync_status()  # the flag was cleared by the read
+    sc.close()
