@@ -589,6 +589,195 @@ static void beam_item(const Node* nodes, const float* tri, const float* cen, con
   }
 }
 
+/* ---- beam over the TOP of the tree only: the item's pyramid culls the BVH
+ * down to depth D (subtree roots at depth D and leaves above it become the
+ * item's candidate list, near first); each lane then slab-tests its own
+ * segment against the candidate boxes (a shared list: no dependent node
+ * fetches) and walks only the subtrees it enters. */
+typedef struct { double items, cands, beam_tests, lane_cand_tests, lane_visits, lane_tri, lanes, warp_steps, cur_steps, max_front, levels; } Bm2;
+static int walk_sub(const Node* nodes, const float* tri, uint32_t root, float ox, float oy, float oz, float dx, float dy,
+                    float dz, float tmin, float thi, float tlo, float thi_tri, int own, double* ntri, int* hit) {
+  const float ix = sinv(dx), iy = sinv(dy), iz = sinv(dz), nD = fabsf(dx) + fabsf(dy) + fabsf(dz);
+  uint32_t stk[STK];
+  int sp = 0, nv = 0;
+  uint32_t ref = root;
+  *hit = 0;
+  for (;;) {
+    while (!is_leaf(ref)) {
+      const Node* n = nodes + ref;
+      ++nv;
+      const float* bx[2] = {n->a, n->b};
+      float an[2], af[2];
+      for (int s = 0; s < 2; ++s) {
+        float x0 = (bx[s][0] - ox) * ix, x1 = (bx[s][1] - ox) * ix;
+        float y0 = (bx[s][2] - oy) * iy, y1 = (bx[s][3] - oy) * iy;
+        float z0 = (n->c[2 * s] - oz) * iz, z1 = (n->c[2 * s + 1] - oz) * iz;
+        an[s] = fmaxf(fmaxf(fminf(x0, x1), fminf(y0, y1)), fmaxf(fminf(z0, z1), tmin));
+        af[s] = fminf(fminf(fmaxf(x0, x1), fmaxf(y0, y1)), fminf(fmaxf(z0, z1), thi));
+      }
+      const int h0 = an[0] <= af[0], h1 = an[1] <= af[1];
+      if (h0 && h1) {
+        const int sw = an[1] < an[0];
+        ref = sw ? n->d[1] : n->d[0];
+        stk[sp++] = sw ? n->d[0] : n->d[1];
+      } else if (h0 || h1) {
+        ref = h0 ? n->d[0] : n->d[1];
+      } else {
+        ref = sp ? stk[--sp] : 0xffffffffu;
+      }
+    }
+    if (ref == 0xffffffffu) break;
+    const uint32_t st = (ref & 0x7fffffffu) >> 3, cnt = (ref & 7u) + 1u;
+    for (uint32_t k = 0; k < cnt; ++k) {
+      const float* tv = tri + 12 * (int64_t)(st + k);
+      int o;
+      memcpy(&o, tv + 3, 4);
+      if (o == own) continue;
+      *ntri += 1;
+      if (tri32(ox, oy, oz, dx, dy, dz, nD, tlo, thi_tri, tv, tv + 4, tv + 8) == 1) { *hit = 1; return nv; }
+    }
+    ref = sp ? stk[--sp] : 0xffffffffu;
+    if (ref == 0xffffffffu) break;
+  }
+  return nv;
+}
+
+static void beam2_item(const Node* nodes, const int* depth, const float* tri, const float* cen, const float* nrm,
+                       int64_t N, uint32_t root, float ox, float oy, float oz, double rL, int64_t tile, int D, Bm2* bm) {
+  double Dv[32][3], tmn[32], tmx[32];
+  int live[32], nl = 0;
+  V3 L = v3(ox, oy, oz);
+  double ax[3] = {0, 0, 0};
+  for (int l = 0; l < 32; ++l) {
+    live[l] = 0;
+    const int64_t r = tile * 32 + l;
+    if (r >= N) continue;
+    const double Dx = (double)cen[3 * r] - ox, Dy = (double)cen[3 * r + 1] - oy, Dz = (double)cen[3 * r + 2] - oz;
+    if (!(-(Dx * nrm[3 * r] + Dy * nrm[3 * r + 1] + Dz * nrm[3 * r + 2]) > 0.0)) continue;
+    const double len = sqrt(Dx * Dx + Dy * Dy + Dz * Dz);
+    const double rT = fmin(nearest(nodes, tri, root, v3(cen[3 * r], cen[3 * r + 1], cen[3 * r + 2]), nrm + 3 * r, (int)r), RT_CAP);
+    Dv[l][0] = Dx; Dv[l][1] = Dy; Dv[l][2] = Dz;
+    tmn[l] = fmin(rL, 2.0) / len * 0.999;
+    tmx[l] = fmin(1.0 - 1e-4 / len, 1.0 - rT / len * 0.999);
+    ax[0] += Dx / len; ax[1] += Dy / len; ax[2] += Dz / len;
+    live[l] = 1;
+    ++nl;
+  }
+  if (!nl) return;
+  double an = sqrt(ax[0] * ax[0] + ax[1] * ax[1] + ax[2] * ax[2]);
+  for (int k = 0; k < 3; ++k) ax[k] /= an;
+  double e1[3], e2[3];
+  { double t[3] = {fabs(ax[0]) < 0.9 ? 1.0 : 0.0, fabs(ax[0]) < 0.9 ? 0.0 : 1.0, 0.0};
+    double d = t[0] * ax[0] + t[1] * ax[1] + t[2] * ax[2];
+    for (int k = 0; k < 3; ++k) e1[k] = t[k] - d * ax[k];
+    double n1 = sqrt(e1[0] * e1[0] + e1[1] * e1[1] + e1[2] * e1[2]);
+    for (int k = 0; k < 3; ++k) e1[k] /= n1;
+    e2[0] = ax[1] * e1[2] - ax[2] * e1[1]; e2[1] = ax[2] * e1[0] - ax[0] * e1[2]; e2[2] = ax[0] * e1[1] - ax[1] * e1[0]; }
+  double s1lo = 1e300, s1hi = -1e300, s2lo = 1e300, s2hi = -1e300, hlo = 1e300, hhi = -1e300;
+  int bad = 0;
+  for (int l = 0; l < 32; ++l) {
+    if (!live[l]) continue;
+    const double h = Dv[l][0] * ax[0] + Dv[l][1] * ax[1] + Dv[l][2] * ax[2];
+    if (h <= 1e-3 * sqrt(Dv[l][0] * Dv[l][0] + Dv[l][1] * Dv[l][1] + Dv[l][2] * Dv[l][2])) { bad = 1; break; }
+    const double p1 = (Dv[l][0] * e1[0] + Dv[l][1] * e1[1] + Dv[l][2] * e1[2]) / h;
+    const double p2 = (Dv[l][0] * e2[0] + Dv[l][1] * e2[1] + Dv[l][2] * e2[2]) / h;
+    s1lo = fmin(s1lo, p1); s1hi = fmax(s1hi, p1); s2lo = fmin(s2lo, p2); s2hi = fmax(s2hi, p2);
+    hlo = fmin(hlo, h * tmn[l]); hhi = fmax(hhi, h * tmx[l]);
+  }
+  if (bad || s1hi - s1lo > 4.0 || s2hi - s2lo > 4.0) return;
+  bm->items += 1;
+  bm->lanes += nl;
+  const double pad = 1e-4;
+  double W[6][3], C[6];
+  for (int k = 0; k < 3; ++k) {
+    W[0][k] = e1[k] - s1hi * ax[k]; W[1][k] = s1lo * ax[k] - e1[k];
+    W[2][k] = e2[k] - s2hi * ax[k]; W[3][k] = s2lo * ax[k] - e2[k];
+    W[4][k] = ax[k]; W[5][k] = -ax[k];
+  }
+  for (int q = 0; q < 4; ++q) { double n = sqrt(W[q][0] * W[q][0] + W[q][1] * W[q][1] + W[q][2] * W[q][2]); for (int k = 0; k < 3; ++k) W[q][k] /= n; C[q] = pad; }
+  C[4] = hhi + pad; C[5] = -hlo + pad;
+  uint32_t stk[STK];
+  static float cl[8192][6];
+  static uint32_t cr[8192];
+  static double ch[8192];
+  int nc = 0, sp = 0;
+  uint32_t ref = root;
+  for (;;) {
+    if (!is_leaf(ref)) {
+      const Node* n = nodes + ref;
+      bm->beam_tests += 1;
+      for (int s = 0; s < 2; ++s) {
+        const float lo[3] = {s ? n->b[0] : n->a[0], s ? n->b[2] : n->a[2], n->c[2 * s]};
+        const float hi[3] = {s ? n->b[1] : n->a[1], s ? n->b[3] : n->a[3], n->c[2 * s + 1]};
+        if (lo[0] > hi[0]) continue;
+        int out = 0;
+        for (int q = 0; q < 6 && !out; ++q) out = lin_min(W[q], C[q], lo, hi, L) > 0;
+        if (out) continue;
+        const uint32_t c = n->d[s];
+        if (is_leaf(c) || depth[c] >= D) {
+          if (nc < 8192) {
+            for (int k = 0; k < 3; ++k) { cl[nc][2 * k] = lo[k]; cl[nc][2 * k + 1] = hi[k]; }
+            cr[nc] = c;
+            ch[nc] = ((lo[0] - ox) * ax[0] + (lo[1] - oy) * ax[1] + (lo[2] - oz) * ax[2]);  /* near corner along the axis, roughly */
+            ++nc;
+          }
+        } else {
+          stk[sp++] = c;
+        }
+      }
+    }
+    if (!sp) break;
+    ref = stk[--sp];
+  }
+  bm->cands += nc;
+  int ord[8192];
+  for (int i = 0; i < nc; ++i) ord[i] = i;
+  for (int i = 1; i < nc; ++i) { int v = ord[i], j = i - 1; while (j >= 0 && ch[ord[j]] > ch[v]) { ord[j + 1] = ord[j]; --j; } ord[j + 1] = v; }
+  int done[32] = {0};
+  float lix[32], liy[32], liz[32], ltlo[32], lthi[32], ltmin[32];
+  for (int l = 0; l < 32; ++l) {
+    if (!live[l]) continue;
+    const float dx = (float)Dv[l][0], dy = (float)Dv[l][1], dz = (float)Dv[l][2];
+    lix[l] = sinv(dx); liy[l] = sinv(dy); liz[l] = sinv(dz);
+    ltlo[l] = 1e-4f / sqrtf(dx * dx + dy * dy + dz * dz); lthi[l] = (float)tmx[l]; ltmin[l] = (float)tmn[l];
+  }
+  /* current design's warp cost for this item: max over lanes of the full walk's visits (free regions) */
+  { int mx = 0;
+    for (int l = 0; l < 32; ++l) {
+      if (!live[l]) continue;
+      double nt = 0;
+      const int v = replay(nodes, tri, root, ox, oy, oz, (float)Dv[l][0], (float)Dv[l][1], (float)Dv[l][2], ltmin[l], lthi[l], ltlo[l], (int)(tile * 32 + l), &nt);
+      if (v > mx) mx = v;
+    }
+    bm->cur_steps += mx; }
+  double wsteps = D;  /* BFS levels */
+  for (int q = 0; q < nc; ++q) {
+    int mx = 0, any = 0;
+    for (int l = 0; l < 32; ++l) {
+      if (!live[l] || done[l]) continue;
+      any = 1;
+      const int64_t r = tile * 32 + l;
+      const float dx = (float)Dv[l][0], dy = (float)Dv[l][1], dz = (float)Dv[l][2];
+      const float* b = cl[ord[q]];
+      bm->lane_cand_tests += 1;
+      float x0 = (b[0] - ox) * lix[l], x1 = (b[1] - ox) * lix[l], y0 = (b[2] - oy) * liy[l], y1 = (b[3] - oy) * liy[l];
+      float z0 = (b[4] - oz) * liz[l], z1 = (b[5] - oz) * liz[l];
+      float a0 = fmaxf(fmaxf(fminf(x0, x1), fminf(y0, y1)), fmaxf(fminf(z0, z1), ltmin[l]));
+      float a1 = fminf(fminf(fmaxf(x0, x1), fmaxf(y0, y1)), fminf(fmaxf(z0, z1), lthi[l]));
+      if (a0 > a1) continue;
+      int hit = 0;
+      const int v = walk_sub(nodes, tri, cr[ord[q]], ox, oy, oz, dx, dy, dz, ltmin[l], lthi[l], ltlo[l], 1.0f - ltlo[l], (int)r,
+                             &bm->lane_tri, &hit);
+      bm->lane_visits += v;
+      if (v > mx) mx = v;
+      if (hit) done[l] = 1;
+    }
+    if (!any) break;
+    wsteps += 1 + mx;
+  }
+  bm->warp_steps += wsteps;
+}
+
 int main(int argc, char** argv) {
   if (argc < 13) { fprintf(stderr, "usage\n"); return 1; }
   size_t sz;
@@ -620,6 +809,9 @@ int main(int argc, char** argv) {
   Pk pk = {0, 0, 0, 0};
   Bm bm;
   memset(&bm, 0, sizeof(bm));
+  static const int kDs[4] = {6, 9, 12, 15};
+  Bm2 bm2[4];
+  memset(bm2, 0, sizeof(bm2));
   double nv_free = 0, tri_free = 0, free_t_lo = 0, free_t_hi = 0, march_steps = 0, march_free = 0, march_free_clear = 0, nv_march = 0, tri_march = 0;
   double uni_leaf = 0;
   for (int64_t it = 0; it < n_items; ++it) {
@@ -633,6 +825,7 @@ int main(int argc, char** argv) {
     int any = 0, maxlane = 0;
     packet_item(nodes, tri, cen, nrm, N, root, ox, oy, oz, tile, &pk);
     beam_item(nodes, tri, cen, nrm, N, root, ox, oy, oz, rL, tile, &bm);
+    for (int q = 0; q < 4; ++q) beam2_item(nodes, depth, tri, cen, nrm, N, root, ox, oy, oz, rL, tile, kDs[q], &bm2[q]);
     for (int lane = 0; lane < 32; ++lane) {
       const int64_t r = tile * 32 + lane;
       if (r >= N) continue;
@@ -753,6 +946,10 @@ int main(int argc, char** argv) {
   printf(" \"packet\": {\"node_steps_per_item\": %.3f, \"leaf_steps_per_item\": %.3f, \"tri_steps_per_item\": %.3f, \"lane_tri_tests_per_ray\": %.3f},\n",
          pk.node_steps / n_it, pk.leaf_steps / n_it, pk.tri_steps / n_it, pk.lane_tri / R);
   printf(" \"lanes_per_item\": %.3f,\n", R / n_it);
+  for (int q = 0; q < 4; ++q)
+    printf(" \"beam_top_D%d\": {\"items\": %.0f, \"cands_per_item\": %.2f, \"beam_node_tests_per_item\": %.2f, \"lane_cand_tests_per_ray\": %.2f, \"lane_visits_per_ray\": %.2f, \"lane_tri_per_ray\": %.3f, \"warp_steps_per_item\": %.2f, \"current_max_lane_visits_per_item\": %.2f},\n",
+           kDs[q], bm2[q].items, bm2[q].cands / bm2[q].items, bm2[q].beam_tests / bm2[q].items, bm2[q].lane_cand_tests / bm2[q].lanes,
+           bm2[q].lane_visits / bm2[q].lanes, bm2[q].lane_tri / bm2[q].lanes, bm2[q].warp_steps / bm2[q].items, bm2[q].cur_steps / bm2[q].items);
   printf(" \"beam\": {\"items\": %.0f, \"fallback_items\": %.0f, \"frustum_nodes_per_item\": %.2f, \"cand_leaves_per_item\": %.2f, \"lane_leaf_box_tests_per_ray\": %.2f, \"lane_tri_tests_per_ray\": %.3f, \"cand_hist_lt4_8_16_32_64_128_256_more\": [%.0f, %.0f, %.0f, %.0f, %.0f, %.0f, %.0f, %.0f]},\n",
          bm.items, bm.fallback, bm.fr_nodes / (bm.items - bm.fallback), bm.cand_leaves / (bm.items - bm.fallback),
          bm.lane_box / bm.lanes, bm.lane_tri / bm.lanes, bm.cand_hist[0], bm.cand_hist[1], bm.cand_hist[2], bm.cand_hist[3],
