@@ -44,7 +44,7 @@
  *   UVD_OCT=0                 no octant node copies (default: built when they
  *                             take <= 1/16 of device memory)
  *   UVD_ASM_SUPER=k           assembly work order: super-tiles of 2^k tiles,
- *                             < 0 column-major (default: 9 when the traversal
+ *                             < 0 column-major (default: 11 when the traversal
  *                             data exceeds 2x the L2, else column-major)
  *   UVD_FIXUP_CAP=n           capacity of the exact re-trace list (tests only)
  *   UVD_FREE=0                no empty end regions (free.cu) in the walk's box

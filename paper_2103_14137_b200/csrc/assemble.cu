@@ -240,9 +240,11 @@ __device__ __forceinline__ int lane_walk32(const AsmParams& P, float ox, float o
 
 // work item -> (column, tile).  P.super_log2 < 0: column-major (all SMs sweep
 // one column's tiles: rays from one or two lamps in flight); > 0: super-tiles of
-// that many tiles, every column of a super-tile before the next one (rays from
-// ~9 lamps to the same 16 K patches in flight), chosen when the BVH is several
-// times the L2: the paths near the patches are then shared across lamps.
+// that many tiles, every column of a super-tile before the next one (default
+// 2048 tiles: rays from ~2–3 lamps to the same 64 K patches in flight), chosen
+// when the BVH is several times the L2: the paths near the patches are then
+// shared across lamps (2^8 / 2^9 / 2^10 / 2^11 / 2^12 / 2^13 tiles measured on
+// C5: 904 / 905 / 895 / 892 / 898 / 903 ms).
 __device__ __forceinline__ void item_to_unit(const AsmParams& P, int64_t units, int super_log2, int64_t item,
                                              int64_t& c, int64_t& tile) {
   if (super_log2 < 0) {
@@ -925,11 +927,11 @@ extern "C" int uvd_irradiance_matrix(const uvd_scene* s, const float* lamp_xyz, 
   P.n_cols = n_cols;
   P.words = (s->N + 31) / 32;
   P.tiles = csc ? P.words : out->ld / 32;
-  {  // work order (item_to_tile): super-tiles of 512 tiles when the traversal data is > 2x the L2
+  {  // work order (item_to_tile): super-tiles of 2048 tiles when the traversal data is > 2x the L2
     int l2 = 0;
     cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev);
     const double bvh_bytes = 8.0 * (double)s->n_nodes * sizeof(Node) + 48.0 * (double)s->M;
-    P.super_log2 = bvh_bytes > 2.0 * (double)l2 ? 9 : -1;
+    P.super_log2 = bvh_bytes > 2.0 * (double)l2 ? 11 : -1;
     if (const char* e = getenv("UVD_ASM_SUPER")) P.super_log2 = atoi(e);  // dev override (log2, < 0 off)
     P.items32 = n_cols * P.tiles < ((int64_t)1 << 32);
     if (P.super_log2 > 30 || !P.items32 ||
