@@ -1267,8 +1267,7 @@ int build_octants(uvd_scene* s, cudaStream_t st) {
   if (s->onodes) al.put(s->onodes);
   s->onodes = nullptr;
   s->n_nodes = nn;
-  size_t free_b = 0, total_b = 0;
-  cudaMemGetInfo(&free_b, &total_b);
+  const size_t total_b = device_total_mem(al.device);
   const char* e = getenv("UVD_OCT");
   const bool want = !(e && atoi(e) == 0) && 8 * nn < ((int64_t)1 << 31) &&
                     (double)(8 * nn * (int64_t)sizeof(Node)) <= (double)total_b / 16.0;
@@ -1307,7 +1306,9 @@ int build_bvh(uvd_scene* s, float4* tri_in, uint32_t** order_out, cudaStream_t s
   float3 inv = make_float3(ex > 0 ? 1.f / ex : 0.f, ey > 0 ? 1.f / ey : 0.f, ez > 0 ? 1.f / ez : 0.f);
   k_morton<<<grid_for(M, 256), 256, 0, st>>>(tri_in, M, lo, inv, keys, vals);
   note_launch();
+  HostTrace::mark("bvh: morton");
   UVD_TRY(sort_pairs_u64(keys, vals, M, al, st));
+  HostTrace::mark("bvh: sort");
   k_gather_tri<<<grid_for(M, 256), 256, 0, st>>>(tri_in, vals, M, s->tri);
   note_launch();
   if (s->kind == UVD_SCENE_TRIMESH) {  // row (patch) of the triangle at Morton position r is r
@@ -1348,6 +1349,7 @@ int build_bvh(uvd_scene* s, float4* tri_in, uint32_t** order_out, cudaStream_t s
     } else {  // PLOC (default): agglomerative clustering over the Morton order
       UVD_TRY(build_ploc(s, M, left, right, rf, rl, pint, pleaf, ibox, arrive, vals, st));
     }
+    HostTrace::mark("bvh: builder");
     {  // the traversal stacks hold 64 entries: refuse deeper trees loudly
       int* dd = (int*)sc.get(sizeof(int));
       if (!dd) { set_error("scene: out of device memory"); return UVD_ERR_NOMEM; }
@@ -1370,8 +1372,10 @@ int build_bvh(uvd_scene* s, float4* tri_in, uint32_t** order_out, cudaStream_t s
     note_launch();
     s->root = 0;
   }
+  HostTrace::mark("bvh: depth+emit");
   UVD_TRY(build_octants(s, st));
   UVD_TRY(build_hnodes(s, st));
+  HostTrace::mark("bvh: octants+hnodes");
   UVD_CUDA_TRY(cudaGetLastError());
   if (order_out) {
     sc.keep(vals);  // ownership passes to the caller

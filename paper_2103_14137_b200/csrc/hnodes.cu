@@ -61,11 +61,16 @@ __device__ __forceinline__ __half h_up(double v) { return __float2half_ru(__doub
 
 // one H node in one octant copy: planes padded outward and rounded outward to
 // fp16, swapped to (entry, exit) for the octant; refs into the same copy
-__global__ void k_h_build(const Node* __restrict__ nodes, const int32_t* __restrict__ hmap, int nh, int64_t nn,
-                          float3 ctr, float3 pad, HNode* __restrict__ hn) {
+// (copies are `cap` nodes apart; the count nh comes from k_h_collect on the
+// device, so the host never waits for it)
+__global__ void k_h_build(const Node* __restrict__ nodes, const int32_t* __restrict__ hmap,
+                          const int* __restrict__ n_h, int cap, int64_t nn, float3 ctr, float3 pad,
+                          HNode* __restrict__ hn) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= 8 * nh) return;
-  const int o = i / nh, h = i - o * nh;
+  if (i >= 8 * cap) return;
+  const int nh = *n_h;
+  const int o = i / cap, h = i - o * cap;
+  if (h >= nh) return;
   const Node nd = nodes[hmap[h]];
   // child k: lo/hi per axis (fp32 boxes of the base array)
   const float lo[2][3] = {{nd.a.x, nd.a.z, nd.c.x}, {nd.b.x, nd.b.z, nd.c.z}};
@@ -92,7 +97,7 @@ __global__ void k_h_build(const Node* __restrict__ nodes, const int32_t* __restr
       int hc = -1;
       for (int q = 0; q < nh; ++q)
         if ((uint32_t)hmap[q] == r) { hc = q; break; }
-      r = hc >= 0 ? kHalfRef | (uint32_t)(hc + o * nh) : r + (uint32_t)(o * nn);
+      r = hc >= 0 ? kHalfRef | (uint32_t)(hc + o * cap) : r + (uint32_t)(o * nn);
     }
     out.ref[k] = r;
   }
@@ -120,23 +125,17 @@ int build_hnodes(uvd_scene* s, cudaStream_t st) {
   int* dn = (int*)(hmap + cap);
   k_h_collect<<<1, 1, 0, st>>>(s->nodes, s->root, depth, cap, hmap, dn);
   note_launch();
-  int* h = (int*)host_stage();
-  if (!h) { set_error("scene: out of pinned host memory"); return UVD_ERR_NOMEM; }
-  UVD_CUDA_TRY(cudaMemcpyAsync(h, dn, sizeof(int), cudaMemcpyDeviceToHost, st));
-  UVD_CUDA_TRY(cudaStreamSynchronize(st));
-  const int nh = *h;
-  if (nh <= 0) return UVD_OK;
-  s->hnodes = (HNode*)al.get((size_t)8 * nh * sizeof(HNode));
+  s->hnodes = (HNode*)al.get((size_t)8 * cap * sizeof(HNode));
   if (!s->hnodes) { set_error("scene: out of device memory (H nodes)"); return UVD_ERR_NOMEM; }
   const float3 ctr = make_float3(0.5f * (s->bbox[0] + s->bbox[3]), 0.5f * (s->bbox[1] + s->bbox[4]),
                                  0.5f * (s->bbox[2] + s->bbox[5]));
   // 1.25·2^-10·L per axis (the fp16 slab error bound above) + 1e-4 m
   const double k = 1.25 / 1024.0;
   const float3 pad = make_float3((float)(k * 2 * hx + 1e-4), (float)(k * 2 * hy + 1e-4), (float)(k * 2 * hz + 1e-4));
-  k_h_build<<<(8 * nh + 127) / 128, 128, 0, st>>>(s->nodes, hmap, nh, nn, ctr, pad, s->hnodes);
+  k_h_build<<<(8 * cap + 127) / 128, 128, 0, st>>>(s->nodes, hmap, dn, cap, nn, ctr, pad, s->hnodes);
   note_launch();
   UVD_CUDA_TRY(cudaGetLastError());
-  s->n_h = nh;
+  s->n_h = cap;  // the stride between octant copies (the walk enters node 0 of its copy)
   s->hcenter[0] = ctr.x; s->hcenter[1] = ctr.y; s->hcenter[2] = ctr.z;
   return UVD_OK;
 }

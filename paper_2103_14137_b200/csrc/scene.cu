@@ -9,6 +9,8 @@
 // them).
 #include <cuda_runtime.h>
 
+#include <chrono>
+
 #include <algorithm>
 #include <atomic>
 #include <string>
@@ -52,6 +54,22 @@ int pointer_device(const void* p) {
   return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged ? a.device : -1;
 }
 
+// total device memory, queried once per device (cudaMemGetInfo took 0.1–20 ms
+// per call on the bench box: it sat in every scene build)
+size_t device_total_mem(int dev) {
+  static size_t cache[kMaxDevices] = {0};
+  if (dev < 0 || dev >= kMaxDevices) return 0;
+  if (!cache[dev]) {
+    cudaDeviceProp pr;
+    if (cudaGetDeviceProperties(&pr, dev) != cudaSuccess) {
+      cudaGetLastError();
+      return 0;
+    }
+    cache[dev] = pr.totalGlobalMem;
+  }
+  return cache[dev];
+}
+
 int sm_count(int dev) {
   static int cache[kMaxDevices] = {0};
   if (dev < 0 || dev >= kMaxDevices) return 148;
@@ -66,10 +84,34 @@ int sm_count(int dev) {
   return cache[dev];
 }
 
+bool HostTrace::on() {
+  static const bool v = [] { const char* e = getenv("UVD_TRACE_HOST"); return e && atoi(e) != 0; }();
+  return v;
+}
+static thread_local std::chrono::steady_clock::time_point g_trace_t = std::chrono::steady_clock::now();
+static thread_local double g_trace_alloc_us = 0.0;
+static thread_local int g_trace_allocs = 0;
+void HostTrace::alloc_time(double us) { g_trace_alloc_us += us; ++g_trace_allocs; }
+void HostTrace::mark(const char* what) {
+  if (!on()) return;
+  const auto t = std::chrono::steady_clock::now();
+  fprintf(stderr, "[uvd-host] %-28s %9.1f us  (allocator %d calls %8.1f us)\n", what,
+          std::chrono::duration<double, std::micro>(t - g_trace_t).count(), g_trace_allocs, g_trace_alloc_us);
+  g_trace_t = t;
+  g_trace_alloc_us = 0.0;
+  g_trace_allocs = 0;
+}
+
 void* Alloc::get(size_t bytes) {
   if (bytes == 0) bytes = 16;
   bytes = (bytes + 255) & ~(size_t)255;
-  if (has_user) return user.alloc(bytes, device, (void*)stream, user.ctx);
+  if (has_user) {
+    if (!HostTrace::on()) return user.alloc(bytes, device, (void*)stream, user.ctx);
+    const auto t = std::chrono::steady_clock::now();
+    void* p = user.alloc(bytes, device, (void*)stream, user.ctx);
+    HostTrace::alloc_time(std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t).count());
+    return p;
+  }
   void* p = nullptr;
   if (cudaMallocAsync(&p, bytes, stream) != cudaSuccess) {
     cudaGetLastError();
@@ -79,8 +121,14 @@ void* Alloc::get(size_t bytes) {
 }
 void Alloc::put(void* p) {
   if (!p) return;
-  if (has_user) user.free(p, device, (void*)stream, user.ctx);
-  else cudaFreeAsync(p, stream);
+  if (has_user) {
+    if (!HostTrace::on()) { user.free(p, device, (void*)stream, user.ctx); return; }
+    const auto t = std::chrono::steady_clock::now();
+    user.free(p, device, (void*)stream, user.ctx);
+    HostTrace::alloc_time(std::chrono::duration<double, std::micro>(std::chrono::steady_clock::now() - t).count());
+  } else {
+    cudaFreeAsync(p, stream);
+  }
 }
 
 // --------------------------------------------------------- fp64 helpers --
@@ -477,7 +525,9 @@ extern "C" int uvd_scene_create(const uvd_scene_desc* desc, int device, void* st
     s->alloc.has_user = true;
   }
   cudaStream_t st = (cudaStream_t)stream;
+  HostTrace::mark("scene_create: enter");
   int rc = desc->kind == UVD_SCENE_TRIMESH ? create_trimesh(s, desc, st) : create_extruded(s, desc, st);
+  HostTrace::mark("scene_create: trimesh+bvh");
   if (rc == UVD_OK) rc = front_radius(s, st);  // patches (row order) and BVH are final here
   if (rc == UVD_OK && !host_stage()) {
     set_error("scene: out of pinned host memory (staging)");
@@ -498,6 +548,7 @@ extern "C" int uvd_scene_create(const uvd_scene_desc* desc, int device, void* st
       s->alloc.put(dsum);
     }
   }
+  HostTrace::mark("scene_create: radii+area+sync");
   if (rc != UVD_OK) {
     std::string msg = uvd_last_error();
     free_scene(s);

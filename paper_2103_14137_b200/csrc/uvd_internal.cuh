@@ -97,6 +97,14 @@ struct Alloc {
   void put(void* p);
 };
 
+// Host-side trace (UVD_TRACE_HOST=1, development): wall-clock marks of the
+// stages of a call and the time spent in allocator callbacks, to stderr.
+struct HostTrace {
+  static bool on();
+  static void mark(const char* what);      // time since the previous mark
+  static void alloc_time(double us);        // accumulated into the next mark
+};
+
 // Call-scoped device buffers: every buffer taken through get() is returned
 // (stream-ordered on the call's stream) at every exit of the call, error
 // returns included; release(p) hands one back early, keep(p) moves ownership out.
@@ -143,6 +151,7 @@ struct NvtxRange {
 // per-device cached launch geometry (SM count; occupancy-derived grids)
 constexpr int kMaxDevices = 64;
 int sm_count(int dev);
+size_t device_total_mem(int dev);  // cached per device
 
 // ------------------------------------------------------------------- scene --
 struct Wall {  // 2.5D wall (host-prepared from the polygon description)
