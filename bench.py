@@ -7,7 +7,7 @@ workload, inputs resident in HBM when the timed region starts:
          attributes + LBVH build)
   a3     uvd_vantage_sample (Armbot grid, clearance, free space, reach)
   a4–a6  uvd_irradiance_matrix (this rank's block-cyclic column shard)
-  a7     uvd_fluence: μ = A·t (sparse LP-like plan), A·𝟙 (ever-visible rows),
+  a7     uvd_fluence_multi: μ = A·t (sparse LP-like plan), A·𝟙 (ever-visible rows),
          g = Aᵀ·y; NCCL all_reduce of μ and A·𝟙 when N > 1
   a8     uvd_coverage
 value = N_patches · K_configs / (step time, max over ranks)  [dense-equivalent
@@ -308,7 +308,6 @@ def main():
     A = torch.empty((n_loc, ld), dtype=torch.float32, device=dev)
     t_glob = vectors.sparse_plan(K, seed=0)
     t_loc = torch.from_numpy(t_glob[cols]).to(dev)
-    ones = torch.ones(n_loc, dtype=torch.float64, device=dev)
     y = torch.from_numpy(vectors.row_weights(N, 0)).to(dev)
     scene.close()
     del lamps
@@ -341,9 +340,8 @@ def main():
             ev_k1[i].record(stream)
             ev[3].record(stream)
         t = t_in if t_in.is_cuda else t_in.to(dev, non_blocking=True)
-        mu = uvd.fluence(A, N, t)                             # a7: μ = A·t
-        rowsum = uvd.fluence(A, N, ones)                      #     A·𝟙 (ever-visible rows)
-        g = uvd.fluence(A, N, y, transpose=True)              #     g = Aᵀ·y
+        # a7: μ = A·t, A·𝟙 (ever-visible rows) and g = Aᵀ·y in one pass over A
+        mu, rowsum, g = uvd.fluence_multi(A, N, x=t, y=y, rowsum=True)
         shard.reduce_partials(mu, rowsum)                     # NCCL all_reduce (N > 1)
         if ev:
             ev[4].record(stream)
@@ -425,12 +423,11 @@ def main():
                               f"FFMA microbenchmark ({FFMA_MEASURED_TFLOPS} TFLOP/s, profiles/peaks_r01.json); "
                               "flops per unit: DESIGN.md §6 (reading R1)")}
 
-    # a7 (HBM-bound GEMVs) against the measured HBM peak: algorithmic bytes of
-    # the step's three products = A's nonzero-t columns + A twice + vectors
-    nnz_t = int((t_loc != 0).sum().item())
-    a7_bytes = 4.0 * ld * (nnz_t + 2 * n_loc) + 8.0 * (4 * N + 2 * n_loc)
+    # a7 (HBM-bound, one pass) against the measured HBM peak: algorithmic bytes
+    # of the step's three products = A once + the vectors (t, y, μ, A·𝟙, g)
+    a7_bytes = 4.0 * ld * n_loc + 8.0 * (3 * N + 2 * n_loc)
     a7_ms = phases["fluence"]
-    a7 = {"kernels": "k_gemv_n (A·t, A·1), k_gemv_t (Aᵀ·y)", "bytes": a7_bytes, "ms": a7_ms,
+    a7 = {"kernels": "k_gemv_multi (A·t, A·𝟙, Aᵀ·y in one pass) + k_gemv_t_reduce", "bytes": a7_bytes, "ms": a7_ms,
           "achieved_gbs": a7_bytes / (a7_ms / 1e3) / 1e9, "peak_gbs": HBM_PEAK_GBS,
           "frac": a7_bytes / (a7_ms / 1e3) / 1e9 / HBM_PEAK_GBS,
           "note": "phase time includes the all_reduce for N > 1"}

@@ -334,6 +334,23 @@ UVD_API int uvd_sync_status(const uvd_scene* scene, void* stream);
 UVD_API int uvd_fluence(const uvd_matrix_out* A, int64_t n, int64_t k, int transpose, const double* x,
                 double* out, void* stream);
 
+/* The step's fluence products in ONE pass over a dense A (a7; SURVEY §8(a):
+ * μ = A·t, the ever-visible denominator A·𝟙, and g = Aᵀ·y of Eq. 5 / Eq. 9):
+ *   ax[n]  = A · x   (x[k] DEVICE fp64, e.g. dwell times; NULL ax: not computed)
+ *   a1[n]  = A · 𝟙   (row sums; NULL: not computed)
+ *   aty[k] = Aᵀ · y  (y[n] DEVICE fp64; NULL aty: not computed)
+ * At least one output; an output needs its input vector (ax needs x, aty needs
+ * y).  Dense A only (CSC: INVALID; use uvd_fluence).  A is read once instead of
+ * once per product.  Deterministic: ax and a1 sum over the columns in order
+ * (ax equals uvd_fluence's A·x whenever that call does not split its columns:
+ * zero x_k add exact zeros), aty sums fixed row blocks in order (it may differ
+ * from uvd_fluence's Aᵀ·y in the last fp64 bits).  Scratch (aty: one fp64 per
+ * 128 rows and column, ceil(n/128) × k doubles) through the allocator of A;
+ * above 4 GB of it (env UVD_MULTI_PART_MAX, tests) the call makes one pass per
+ * product instead (then equal to uvd_fluence's results).  Asynchronous. */
+UVD_API int uvd_fluence_multi(const uvd_matrix_out* A, int64_t n, int64_t k, const double* x, const double* y,
+                              double* ax, double* a1, double* aty, void* stream);
+
 /* ---------------------------------------------------------------------- a8 */
 /* Coverage (P:9 "fraction of the surface area"):
  *   out[0] = Σ_i |s_i| [μ_i >= μ_min]      (covered area, inclusive, Q16)

@@ -14,6 +14,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 #include <cmath>
 #include <mutex>
 #include <vector>
@@ -147,6 +148,121 @@ __global__ void __launch_bounds__(kGemvThreads) k_gemv_t(const float* __restrict
     double v = 0.0;
     for (int w = 0; w < kGemvThreads / 32; ++w) v += red[threadIdx.x][w];
     out[c0 + threadIdx.x] = v;
+  }
+}
+
+// The three products of one step in ONE pass over a dense A (uvd_fluence_multi):
+// μ = A·x, A·𝟙 and g = Aᵀ·y.  A thread owns 4 rows across all columns (one
+// float4 per column, 8 columns in flight): μ and A·𝟙 accumulate in registers in
+// column order — the same fp64 sums as k_gemv_n over all columns (x_j = 0 adds
+// an exact 0).  For Aᵀ·y each warp reduces its 128 rows' dots of the 8 columns
+// with a butterfly reduce-scatter (lanes trade half their columns at each of
+// the first three steps: 9 shuffles for 8 columns instead of 40) and writes the
+// 8 partials as one contiguous 64-byte row of part[warp][k]; k_gemv_t_reduce
+// sums the warps in order.  No block barrier; deterministic; HBM-bound: A is
+// read once instead of once per product.
+static __global__ void k_fill_value(double* __restrict__ p, int64_t n, double v) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
+}
+
+constexpr int kMultiThreads = 256;
+constexpr int kMultiCols = 8;  // columns in flight per thread
+
+__device__ __forceinline__ double shfl_x(double v, int m) { return __shfl_xor_sync(0xffffffffu, v, m); }
+
+template <bool X, bool ONE, bool Y>
+__global__ void __launch_bounds__(kMultiThreads) k_gemv_multi(const float* __restrict__ A, int64_t ld, int64_t n,
+                                                              int64_t k, const double* __restrict__ x,
+                                                              const double* __restrict__ y,
+                                                              double* __restrict__ ax, double* __restrict__ a1,
+                                                              double* __restrict__ part) {
+  const int lane = threadIdx.x & 31;
+  const int64_t q = (int64_t)blockIdx.x * kMultiThreads + threadIdx.x;  // row quad
+  const int64_t gw = q >> 5;                                           // global warp
+  const int64_t r0 = 4 * q;
+  const bool in = r0 < n;
+  const float4* __restrict__ A4 = reinterpret_cast<const float4*>(A) + q;
+  const int64_t ld4 = ld / 4;
+  double m0 = 0.0, m1 = 0.0, m2 = 0.0, m3 = 0.0, s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+  double y0 = 0.0, y1 = 0.0, y2 = 0.0, y3 = 0.0;
+  if (Y && in) {
+    y0 = y[r0];
+    y1 = r0 + 1 < n ? y[r0 + 1] : 0.0;
+    y2 = r0 + 2 < n ? y[r0 + 2] : 0.0;
+    y3 = r0 + 3 < n ? y[r0 + 3] : 0.0;
+  }
+  // after the reduce-scatter, lane l holds column c(l) = bits 4, 3, 2 of l (as
+  // 4·b4 + 2·b3 + b2) summed over lanes l ^ {0, 1, 2, 3}; lanes with l % 4 == 0 write
+  const int cl = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+  // software-pipelined: the next 8 columns are in flight while this group's
+  // sums and the shuffle chain of its reduce-scatter run
+  float4 v[kMultiCols], vn[kMultiCols];
+#pragma unroll
+  for (int u = 0; u < kMultiCols; ++u)
+    v[u] = (in && u < k) ? __ldcs(A4 + (int64_t)u * ld4) : make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int64_t c0 = 0; c0 < k; c0 += kMultiCols) {
+    const int nc = (int)(k - c0 < kMultiCols ? k - c0 : kMultiCols);
+    const int64_t c1 = c0 + kMultiCols;
+#pragma unroll
+    for (int u = 0; u < kMultiCols; ++u)
+      vn[u] = (in && c1 + u < k) ? __ldcs(A4 + (c1 + u) * ld4) : make_float4(0.f, 0.f, 0.f, 0.f);
+    double d[kMultiCols];
+#pragma unroll
+    for (int u = 0; u < kMultiCols; ++u) {
+      if (X && u < nc) {
+        const double t = x[c0 + u];
+        m0 += (double)v[u].x * t; m1 += (double)v[u].y * t; m2 += (double)v[u].z * t; m3 += (double)v[u].w * t;
+      }
+      if (ONE) { s0 += (double)v[u].x; s1 += (double)v[u].y; s2 += (double)v[u].z; s3 += (double)v[u].w; }
+      d[u] = Y ? (double)v[u].x * y0 + (double)v[u].y * y1 + (double)v[u].z * y2 + (double)v[u].w * y3 : 0.0;
+    }
+    if (Y) {
+      // step 1 (xor 16): keep columns 0-3 (bit 4 clear) or 4-7, send the other half
+      const bool h4 = lane & 16, h3 = lane & 8, h2 = lane & 4;
+      double e[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const double mine = h4 ? d[u + 4] : d[u], other = h4 ? d[u] : d[u + 4];
+        e[u] = mine + shfl_x(other, 16);
+      }
+      double f[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const double mine = h3 ? e[u + 2] : e[u], other = h3 ? e[u] : e[u + 2];
+        f[u] = mine + shfl_x(other, 8);
+      }
+      double g = (h2 ? f[1] : f[0]) + shfl_x(h2 ? f[0] : f[1], 4);
+      g += shfl_x(g, 2);
+      g += shfl_x(g, 1);
+      if ((lane & 3) == 0 && cl < nc) part[gw * k + c0 + cl] = g;
+    }
+#pragma unroll
+    for (int u = 0; u < kMultiCols; ++u) v[u] = vn[u];
+  }
+  if (!in) return;
+  if (X) {
+    ax[r0] = m0;
+    if (r0 + 1 < n) ax[r0 + 1] = m1;
+    if (r0 + 2 < n) ax[r0 + 2] = m2;
+    if (r0 + 3 < n) ax[r0 + 3] = m3;
+  }
+  if (ONE) {
+    a1[r0] = s0;
+    if (r0 + 1 < n) a1[r0 + 1] = s1;
+    if (r0 + 2 < n) a1[r0 + 2] = s2;
+    if (r0 + 3 < n) a1[r0 + 3] = s3;
+  }
+}
+
+// Σ over the warps' partials in a fixed order: gridDim.y chunks of warps
+// (chunk sums to part2[chunk][k]), then the chunks in order (deterministic)
+__global__ void k_gemv_t_reduce(const double* __restrict__ part, int64_t nw, int64_t k, double* __restrict__ out) {
+  const int64_t per = (nw + gridDim.y - 1) / gridDim.y, w0 = blockIdx.y * per;
+  const int64_t w1 = w0 + per < nw ? w0 + per : nw;
+  for (int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; j < k; j += (int64_t)gridDim.x * blockDim.x) {
+    double v = 0.0;
+    for (int64_t w = w0; w < w1; ++w) v += part[w * k + j];
+    out[(int64_t)blockIdx.y * k + j] = v;
   }
 }
 
@@ -418,6 +534,72 @@ extern "C" int uvd_fluence(const uvd_matrix_out* A, int64_t n, int64_t k, int tr
     if (!ws) { set_error("uvd_fluence: out of device memory"); return UVD_ERR_NOMEM; }
   }
   return fluence_run(A, n, k, transpose, x, out, st, ws);
+}
+
+extern "C" int uvd_fluence_multi(const uvd_matrix_out* A, int64_t n, int64_t k, const double* x,
+                                 const double* y, double* ax, double* a1, double* aty, void* stream) {
+  clear_error();
+  double* any = ax ? ax : a1 ? a1 : aty;
+  if (!A || n < 0 || k < 0 || !any || (ax && !x) || (aty && !y)) {
+    set_error("uvd_fluence_multi: bad argument (an output needs its input vector)");
+    return UVD_ERR_INVALID;
+  }
+  DeviceGuard dg(pointer_device(any));
+  NvtxRange nv("uvd_fluence_multi");
+  cudaStream_t st = (cudaStream_t)stream;
+  if (A->format != UVD_DENSE_COLMAJOR) { set_error("uvd_fluence_multi: dense A only"); return UVD_ERR_INVALID; }
+  if (n == 0 || k == 0) {  // empty: A·x = A·𝟙 = 0 (n rows), Aᵀ·y = 0 (k columns)
+    if (ax && n) UVD_CUDA_TRY(cudaMemsetAsync(ax, 0, n * sizeof(double), st));
+    if (a1 && n) UVD_CUDA_TRY(cudaMemsetAsync(a1, 0, n * sizeof(double), st));
+    if (aty && k) UVD_CUDA_TRY(cudaMemsetAsync(aty, 0, k * sizeof(double), st));
+    return UVD_OK;
+  }
+  UVD_TRY(fluence_check(A, n, k, x ? x : y ? y : any));
+  int dev = 0;
+  cudaGetDevice(&dev);
+  const int64_t quads = (n + 3) / 4, nw = (quads + 31) / 32;
+  const size_t part_bytes = aty ? (size_t)nw * k * sizeof(double) : 0;
+  Scratch sc(matrix_alloc(A, dev, st), st);
+  size_t part_max = (size_t)4 << 30;
+  if (const char* e = getenv("UVD_MULTI_PART_MAX")) part_max = (size_t)atoll(e);  // tests
+  if (part_bytes > part_max) {  // the warp partials would exceed 4 GB: one pass per product
+    void* ws = (ax || a1) ? sc.get(fluence_ws_bytes(n, k, false, dev)) : nullptr;
+    double* ones = a1 ? (double*)sc.get((size_t)k * sizeof(double)) : nullptr;
+    if (((ax || a1) && !ws) || (a1 && !ones)) { set_error("uvd_fluence_multi: out of device memory"); return UVD_ERR_NOMEM; }
+    if (ax) UVD_TRY(fluence_run(A, n, k, 0, x, ax, st, ws));
+    if (a1) {
+      k_fill_value<<<(unsigned)std::min<int64_t>((k + 255) / 256, 1024), 256, 0, st>>>(ones, k, 1.0);
+      note_launch();
+      UVD_TRY(fluence_run(A, n, k, 0, ones, a1, st, ws));
+    }
+    if (aty) UVD_TRY(fluence_run(A, n, k, 1, y, aty, st, nullptr));
+    return UVD_OK;
+  }
+  double* part = nullptr;
+  double* part2 = nullptr;
+  // the warp partials are summed in chunks: enough blocks to stream them at HBM speed
+  const int64_t chunks = std::max<int64_t>(1, std::min<int64_t>(64, (8 * sm_count(dev) * 256 + k - 1) / std::max<int64_t>(k, 1)));
+  if (aty) {
+    part = (double*)sc.get(part_bytes);
+    part2 = chunks > 1 ? (double*)sc.get((size_t)chunks * k * sizeof(double)) : nullptr;
+    if (!part || (chunks > 1 && !part2)) { set_error("uvd_fluence_multi: out of device memory"); return UVD_ERR_NOMEM; }
+  }
+  const int sel = (ax ? 4 : 0) | (a1 ? 2 : 0) | (aty ? 1 : 0);
+  auto kern = sel == 7 ? k_gemv_multi<true, true, true> : sel == 6 ? k_gemv_multi<true, true, false>
+            : sel == 5 ? k_gemv_multi<true, false, true> : sel == 4 ? k_gemv_multi<true, false, false>
+            : sel == 3 ? k_gemv_multi<false, true, true> : sel == 2 ? k_gemv_multi<false, true, false>
+                       : k_gemv_multi<false, false, true>;
+  kern<<<(unsigned)((quads + kMultiThreads - 1) / kMultiThreads), kMultiThreads, 0, st>>>(A->values, A->ld, n, k, x,
+                                                                                         y, ax, a1, part);
+  note_launch();
+  if (aty) {
+    const unsigned gx = (unsigned)std::min<int64_t>((k + 255) / 256, 8 * sm_count(dev));
+    k_gemv_t_reduce<<<dim3(gx, (unsigned)chunks), 256, 0, st>>>(part, nw, k, chunks > 1 ? part2 : aty);
+    if (chunks > 1) k_gemv_t_reduce<<<dim3(gx, 1), 256, 0, st>>>(part2, chunks, k, aty);
+    note_launch(chunks > 1 ? 2 : 1);
+  }
+  UVD_CUDA_TRY(cudaGetLastError());
+  return UVD_OK;
 }
 
 extern "C" int uvd_coverage(const uvd_scene* s, const double* mu, double mu_min,

@@ -117,6 +117,8 @@ def lib():
         L.uvd_sync_status.argtypes = [C.c_void_p, C.c_void_p]
         L.uvd_fluence.argtypes = [C.POINTER(_MatrixOut), C.c_int64, C.c_int64, C.c_int, C.c_void_p,
                                   C.c_void_p, C.c_void_p]
+        L.uvd_fluence_multi.argtypes = [C.POINTER(_MatrixOut), C.c_int64, C.c_int64, C.c_void_p, C.c_void_p,
+                                        C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
         L.uvd_coverage.argtypes = [C.c_void_p, C.c_void_p, C.c_double, C.c_void_p,
                                    C.POINTER(C.c_double), C.c_void_p]
         L.uvd_cubemap_matrix.argtypes = [C.c_void_p, C.c_void_p, C.c_int64, C.c_void_p, C.c_int64,
@@ -135,7 +137,7 @@ def lib():
 
 EXPORTS = ("uvd_scene_create", "uvd_scene_query", "uvd_scene_patches", "uvd_scene_bvh", "uvd_scene_destroy",
            "uvd_scene_export", "uvd_scene_import",
-           "uvd_vantage_sample", "uvd_irradiance_matrix", "uvd_sync_status", "uvd_fluence",
+           "uvd_vantage_sample", "uvd_irradiance_matrix", "uvd_sync_status", "uvd_fluence", "uvd_fluence_multi",
            "uvd_coverage", "uvd_cubemap_matrix", "uvd_static_columns", "uvd_lp_solve", "uvd_last_error", "uvd_version", "uvd_launch_count")
 
 
@@ -502,6 +504,22 @@ def fluence(A: torch.Tensor, n: int, x: torch.Tensor, transpose: bool = False,
     m = _dense_desc(A)
     _check(lib().uvd_fluence(C.byref(m), n, k, int(bool(transpose)), _ptr(x), _ptr(out), _stream(stream)))
     return out
+
+
+def fluence_multi(A: torch.Tensor, n: int, x: torch.Tensor | None = None, y: torch.Tensor | None = None,
+                  rowsum: bool = False, stream=None):
+    """uvd_fluence_multi on a dense (n_cols, ld) A, one pass over A: returns
+    (A·x or None, A·𝟙 or None, Aᵀ·y or None) for x (n_cols,) / y (n,) fp64."""
+    k = A.shape[0]
+    for v in (x, y):
+        assert v is None or (v.dtype == torch.float64 and v.is_cuda and v.is_contiguous())
+    ax = torch.empty(n, dtype=torch.float64, device=A.device) if x is not None else None
+    a1 = torch.empty(n, dtype=torch.float64, device=A.device) if rowsum else None
+    aty = torch.empty(k, dtype=torch.float64, device=A.device) if y is not None else None
+    m = _dense_desc(A)
+    _check(lib().uvd_fluence_multi(C.byref(m), n, k, _ptr(x), _ptr(y), _ptr(ax), _ptr(a1), _ptr(aty),
+                                   _stream(stream)))
+    return ax, a1, aty
 
 
 def fluence_csc(csc: dict, n: int, x: torch.Tensor, transpose: bool = False,
