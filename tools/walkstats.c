@@ -642,6 +642,7 @@ static int walk_sub(const Node* nodes, const float* tri, uint32_t root, float ox
   return nv;
 }
 
+static int g_ia = 0;  /* 1: interval-arithmetic bundle test instead of the pyramid */
 static void beam2_item(const Node* nodes, const int* depth, const float* tri, const float* cen, const float* nrm,
                        int64_t N, uint32_t root, float ox, float oy, float oz, double rL, int64_t tile, int D, Bm2* bm) {
   double Dv[32][3], tmn[32], tmx[32];
@@ -687,6 +688,15 @@ static void beam2_item(const Node* nodes, const int* depth, const float* tri, co
   if (bad || s1hi - s1lo > 4.0 || s2hi - s2lo > 4.0) return;
   bm->items += 1;
   bm->lanes += nl;
+  float ia_lo[3] = {1e30f, 1e30f, 1e30f}, ia_hi[3] = {-1e30f, -1e30f, -1e30f}, ia_tmin = 1e30f, ia_tmax = -1e30f;
+  for (int l = 0; l < 32; ++l) {
+    if (!live[l]) continue;
+    for (int a = 0; a < 3; ++a) {
+      const float iv = sinv((float)Dv[l][a]);
+      ia_lo[a] = fminf(ia_lo[a], iv); ia_hi[a] = fmaxf(ia_hi[a], iv);
+    }
+    ia_tmin = fminf(ia_tmin, (float)tmn[l]); ia_tmax = fmaxf(ia_tmax, (float)tmx[l]);
+  }
   const double pad = 1e-4;
   double W[6][3], C[6];
   for (int k = 0; k < 3; ++k) {
@@ -711,7 +721,25 @@ static void beam2_item(const Node* nodes, const int* depth, const float* tri, co
         const float hi[3] = {s ? n->b[1] : n->a[1], s ? n->b[3] : n->a[3], n->c[2 * s + 1]};
         if (lo[0] > hi[0]) continue;
         int out = 0;
-        for (int q = 0; q < 6 && !out; ++q) out = lin_min(W[q], C[q], lo, hi, L) > 0;
+        if (g_ia) {
+          /* interval slab test of the bundle: t = (b - L)·i, i in [imin, imax] per axis */
+          float ten = ia_tmin, tex = ia_tmax;
+          for (int a = 0; a < 3; ++a) {
+            const float bl = lo[a] - (a == 0 ? ox : a == 1 ? oy : oz), bh = hi[a] - (a == 0 ? ox : a == 1 ? oy : oz);
+            const float i0 = ia_lo[a], i1 = ia_hi[a];
+            if (i0 <= 0.f && i1 >= 0.f && !(i0 == 0.f && i1 == 0.f)) {
+              /* sign change: unbounded on this axis unless L is outside the slab */
+              continue;
+            }
+            const float p0 = bl * i0, p1 = bl * i1, p2 = bh * i0, p3 = bh * i1;
+            const float mn = fminf(fminf(p0, p1), fminf(p2, p3)), mx = fmaxf(fmaxf(p0, p1), fmaxf(p2, p3));
+            ten = fmaxf(ten, mn);
+            tex = fminf(tex, mx);
+          }
+          out = ten > tex * 1.00001f + 1e-6f;
+        } else {
+          for (int q = 0; q < 6 && !out; ++q) out = lin_min(W[q], C[q], lo, hi, L) > 0;
+        }
         if (out) continue;
         const uint32_t c = n->d[s];
         if (is_leaf(c) || depth[c] >= D) {
@@ -810,8 +838,9 @@ int main(int argc, char** argv) {
   Bm bm;
   memset(&bm, 0, sizeof(bm));
   static const int kDs[4] = {6, 9, 12, 15};
-  Bm2 bm2[4];
+  Bm2 bm2[4], bm3[4];
   memset(bm2, 0, sizeof(bm2));
+  memset(bm3, 0, sizeof(bm3));
   double nv_free = 0, tri_free = 0, free_t_lo = 0, free_t_hi = 0, march_steps = 0, march_free = 0, march_free_clear = 0, nv_march = 0, tri_march = 0;
   double uni_leaf = 0;
   for (int64_t it = 0; it < n_items; ++it) {
@@ -826,6 +855,9 @@ int main(int argc, char** argv) {
     packet_item(nodes, tri, cen, nrm, N, root, ox, oy, oz, tile, &pk);
     beam_item(nodes, tri, cen, nrm, N, root, ox, oy, oz, rL, tile, &bm);
     for (int q = 0; q < 4; ++q) beam2_item(nodes, depth, tri, cen, nrm, N, root, ox, oy, oz, rL, tile, kDs[q], &bm2[q]);
+    g_ia = 1;
+    for (int q = 0; q < 4; ++q) beam2_item(nodes, depth, tri, cen, nrm, N, root, ox, oy, oz, rL, tile, kDs[q], &bm3[q]);
+    g_ia = 0;
     for (int lane = 0; lane < 32; ++lane) {
       const int64_t r = tile * 32 + lane;
       if (r >= N) continue;
@@ -950,6 +982,10 @@ int main(int argc, char** argv) {
     printf(" \"beam_top_D%d\": {\"items\": %.0f, \"cands_per_item\": %.2f, \"beam_node_tests_per_item\": %.2f, \"lane_cand_tests_per_ray\": %.2f, \"lane_visits_per_ray\": %.2f, \"lane_tri_per_ray\": %.3f, \"warp_steps_per_item\": %.2f, \"current_max_lane_visits_per_item\": %.2f},\n",
            kDs[q], bm2[q].items, bm2[q].cands / bm2[q].items, bm2[q].beam_tests / bm2[q].items, bm2[q].lane_cand_tests / bm2[q].lanes,
            bm2[q].lane_visits / bm2[q].lanes, bm2[q].lane_tri / bm2[q].lanes, bm2[q].warp_steps / bm2[q].items, bm2[q].cur_steps / bm2[q].items);
+  for (int q = 0; q < 4; ++q)
+    printf(" \"beam_ia_D%d\": {\"items\": %.0f, \"cands_per_item\": %.2f, \"beam_node_tests_per_item\": %.2f, \"lane_cand_tests_per_ray\": %.2f, \"lane_visits_per_ray\": %.2f, \"lane_tri_per_ray\": %.3f, \"warp_steps_per_item\": %.2f, \"current_max_lane_visits_per_item\": %.2f},\n",
+           kDs[q], bm3[q].items, bm3[q].cands / bm3[q].items, bm3[q].beam_tests / bm3[q].items, bm3[q].lane_cand_tests / bm3[q].lanes,
+           bm3[q].lane_visits / bm3[q].lanes, bm3[q].lane_tri / bm3[q].lanes, bm3[q].warp_steps / bm3[q].items, bm3[q].cur_steps / bm3[q].items);
   printf(" \"beam\": {\"items\": %.0f, \"fallback_items\": %.0f, \"frustum_nodes_per_item\": %.2f, \"cand_leaves_per_item\": %.2f, \"lane_leaf_box_tests_per_ray\": %.2f, \"lane_tri_tests_per_ray\": %.3f, \"cand_hist_lt4_8_16_32_64_128_256_more\": [%.0f, %.0f, %.0f, %.0f, %.0f, %.0f, %.0f, %.0f]},\n",
          bm.items, bm.fallback, bm.fr_nodes / (bm.items - bm.fallback), bm.cand_leaves / (bm.items - bm.fallback),
          bm.lane_box / bm.lanes, bm.lane_tri / bm.lanes, bm.cand_hist[0], bm.cand_hist[1], bm.cand_hist[2], bm.cand_hist[3],
