@@ -540,10 +540,11 @@ extern "C" int uvd_fluence_multi(const uvd_matrix_out* A, int64_t n, int64_t k, 
                                  const double* y, double* ax, double* a1, double* aty, void* stream) {
   clear_error();
   double* any = ax ? ax : a1 ? a1 : aty;
-  if (!A || n < 0 || k < 0 || !any || (ax && !x) || (aty && !y)) {
+  if (!A || n < 0 || k < 0 || (!any && n > 0 && k > 0) || (ax && !x && k > 0) || (aty && !y && n > 0)) {
     set_error("uvd_fluence_multi: bad argument (an output needs its input vector)");
     return UVD_ERR_INVALID;
   }
+  if (!any) return UVD_OK;  // nothing to compute (an empty shard asked only for its empty Aᵀ·y)
   DeviceGuard dg(pointer_device(any));
   NvtxRange nv("uvd_fluence_multi");
   cudaStream_t st = (cudaStream_t)stream;

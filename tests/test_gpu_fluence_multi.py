@@ -110,3 +110,15 @@ def test_multi_fallback_matches(uvd, monkeypatch):
     assert torch.equal(ax, uvd.fluence(A, n, x))
     assert torch.equal(a1, uvd.fluence(A, n, torch.ones(k, dtype=torch.float64, device="cuda")))
     assert torch.equal(aty, uvd.fluence(A, n, y, transpose=True))
+
+
+def test_multi_empty_shapes(uvd):
+    """An empty column shard (k = 0): A·x = A·𝟙 = 0 and Aᵀ·y is empty; n = 0:
+    nothing to compute."""
+    n = 70
+    A = torch.zeros((0, 96), dtype=torch.float32, device="cuda")
+    x = torch.zeros(0, dtype=torch.float64, device="cuda")
+    y = torch.rand(n, dtype=torch.float64, device="cuda")
+    ax, a1, aty = uvd.fluence_multi(A, n, x=x, y=y, rowsum=True)
+    assert ax.shape == (n,) and a1.shape == (n,) and aty.shape == (0,)
+    assert not ax.any() and not a1.any()
