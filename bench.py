@@ -400,7 +400,7 @@ def main():
     pairs = float(N) * K * L
     flops = FLOP_PER_PAIR * pairs + FLOP_PER_RAY * cnt[0] + FLOP_PER_BOX * cnt[1] + FLOP_PER_TRI * cnt[2]
     achieved = flops / ws / (k_ms / 1e3) / 1e12
-    traffic, traffic_note = None, None
+    traffic, traffic_note, ncu_issue = None, None, None
     tfile = os.path.join(ROOT, "profiles", "ncu_traffic_r02.json")
     if not os.path.exists(tfile):
         tfile = os.path.join(ROOT, "profiles", "ncu_traffic_r01.json")
@@ -409,8 +409,11 @@ def main():
         traffic = tr["bytes_per_col"] * K  # per launch: all columns of the step
         traffic_note = (f"DRAM read+write of {tr['capture']} ({tr['cols']}-column launch), scaled per column "
                         f"to this {K}-column launch")
+        ncu_issue = tr.get("ncu_issue")
     roofline = {"bound": "alu", "achieved": achieved, "peak": FP32_PEAK_TFLOPS, "unit": "TFLOP/s",
                 "frac": achieved / FP32_PEAK_TFLOPS,
+                # what bounds it (ncu of the same kernel): issue slots and threads per warp
+                "ncu_issue": ncu_issue,
                 "frac_vs_measured_ffma": achieved / FFMA_MEASURED_TFLOPS if FFMA_MEASURED_TFLOPS else None,
                 "traffic": traffic, "traffic_note": traffic_note,
                 "kernel": "k_assemble", "kernel_ms": k_ms, "kernel_ms_median": k_med,
