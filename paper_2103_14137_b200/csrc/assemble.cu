@@ -574,15 +574,20 @@ __global__ void __launch_bounds__(kCscThreads) k_csc_fill(const AsmParams P, con
 // fp32 triangle filter as the hot kernel, with every undecided triangle
 // re-tested at once in fp64 (no register pressure concern in this kernel).
 __device__ bool lane_clear_exact(const AsmParams& P, float ox, float oy, float oz, float cx, float cy,
-                                 float cz, int owner) {
+                                 float cz, int owner, float rl = 0.0f, float rt = 0.0f) {
   uint32_t stk[kLaneStack];
   int sp = 0;
   const float dx = cx - ox, dy = cy - oy, dz = cz - oz;
   const float ix = safe_inv(dx), iy = safe_inv(dy), iz = safe_inv(dz);
   const float oix = ox * ix, oiy = oy * iy, oiz = oz * iz;
   const float nD = fabsf(dx) + fabsf(dy) + fabsf(dz);
-  const float tlo = (float)kSelfEps * rsqrtf(dx * dx + dy * dy + dz * dz);
+  const float inv_len = rsqrtf(dx * dx + dy * dy + dz * dz);
+  const float tlo = (float)kSelfEps * inv_len;
   const float thi = 1.0f - tlo;
+  // the box tests use the segment's part outside its empty end regions, exactly
+  // as k_assemble_lane (free.cu; the triangle tests keep the full range)
+  const float tmin = rl * inv_len * 0.99999f;
+  const float tmax = fminf(thi, 1.0f - fmaxf(rt * inv_len * 0.99999f - 2e-7f, 0.0f));
   const D3 O = d3(ox, oy, oz);
   const D3 D = d3((double)cx - O.x, (double)cy - O.y, (double)cz - O.z);
   const double dd = ddot3(D, D);
@@ -609,15 +614,16 @@ __device__ bool lane_clear_exact(const AsmParams& P, float ox, float oy, float o
       const float bx0 = fmaf(nd.b.x, ix, -oix), bx1 = fmaf(nd.b.y, ix, -oix);
       const float by0 = fmaf(nd.b.z, iy, -oiy), by1 = fmaf(nd.b.w, iy, -oiy);
       const float bz0 = fmaf(nd.c.z, iz, -oiz), bz1 = fmaf(nd.c.w, iz, -oiz);
-      const float an = fmaxf(fmaxf(fminf(ax0, ax1), fminf(ay0, ay1)), fmaxf(fminf(az0, az1), 0.0f));
-      const float af = fminf(fminf(fmaxf(ax0, ax1), fmaxf(ay0, ay1)), fminf(fmaxf(az0, az1), thi));
-      const float bn = fmaxf(fmaxf(fminf(bx0, bx1), fminf(by0, by1)), fmaxf(fminf(bz0, bz1), 0.0f));
-      const float bf = fminf(fminf(fmaxf(bx0, bx1), fmaxf(by0, by1)), fminf(fmaxf(bz0, bz1), thi));
+      const float an = fmaxf(fmaxf(fminf(ax0, ax1), fminf(ay0, ay1)), fmaxf(fminf(az0, az1), tmin));
+      const float af = fminf(fminf(fmaxf(ax0, ax1), fmaxf(ay0, ay1)), fminf(fmaxf(az0, az1), tmax));
+      const float bn = fmaxf(fmaxf(fminf(bx0, bx1), fminf(by0, by1)), fmaxf(fminf(bz0, bz1), tmin));
+      const float bf = fminf(fminf(fmaxf(bx0, bx1), fmaxf(by0, by1)), fminf(fmaxf(bz0, bz1), tmax));
       const bool h0 = an <= fmaf(af, 1.000002f, 1e-7f);
       const bool h1 = bn <= fmaf(bf, 1.000002f, 1e-7f);
       if (h0 && h1) {
-        ref = nd.d.x;
-        if (sp < kLaneStack) stk[sp++] = nd.d.y;
+        const bool swap = bn < an;  // near child first: an occluder ends the walk sooner
+        ref = swap ? nd.d.y : nd.d.x;
+        if (sp < kLaneStack) stk[sp++] = swap ? nd.d.x : nd.d.y;
         else atomicExch(P.err, 2);
       } else if (h0 || h1) {
         ref = h0 ? nd.d.x : nd.d.y;
@@ -670,7 +676,11 @@ __device__ void fixup_entry(const AsmParams& P, int64_t c, int r) {
         }
       }
     } else {
-      vis = cosd > 0.0 && dd >= kMinDist * kMinDist && lane_clear_exact(P, ox, oy, oz, cx, cy, cz, r);
+      // the empty end regions of k_assemble_lane (lamp radius of this call's column, front radius
+      // when cos θ >= 1e-2, the same expressions)
+      const float rl = P.lamp_free ? P.lamp_free[c * P.L + l] : 0.0f;
+      const float rt = P.front_free && cosd * ri >= 1e-2 ? P.front_free[r] : 0.0f;
+      vis = cosd > 0.0 && dd >= kMinDist * kMinDist && lane_clear_exact(P, ox, oy, oz, cx, cy, cz, r, rl, rt);
       if (vis) acc += cosd * (ri * ri * ri);
     }
     if (P.vis_bits) {
