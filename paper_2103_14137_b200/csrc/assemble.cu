@@ -775,7 +775,7 @@ __global__ void k_fixup_overflow(AsmParams P, int64_t cap, const unsigned long l
 }
 
 #ifndef UVD_FIX_MINB
-#define UVD_FIX_MINB 12  // 40 registers (spilling): 48 warps per SM beat 16 at 119 registers (-24 %)
+#define UVD_FIX_MINB 8  // 64 registers: 8.6 ms per C5 launch (12 blocks / 40 registers: 9.8, 6: 9.4, 4: 10.1, 16: 17.6)
 #endif
 __global__ void __launch_bounds__(128, UVD_FIX_MINB) k_fixup_run(AsmParams P, const uint64_t* __restrict__ list, int64_t cap,
                             const unsigned long long* __restrict__ count) {
