@@ -165,8 +165,11 @@ static __global__ void k_fill_value(double* __restrict__ p, int64_t n, double v)
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) p[i] = v;
 }
 
-constexpr int kMultiThreads = 256;
-constexpr int kMultiCols = 8;  // columns in flight per thread
+#ifndef UVD_MULTI_THREADS
+#define UVD_MULTI_THREADS 128  // 128 / 64 / 256 / 512: 8.4–8.5 / 8.5 / 9.2 / 9.4 ms per C5 pass
+#endif
+constexpr int kMultiThreads = UVD_MULTI_THREADS;
+constexpr int kMultiCols = 8;  // columns in flight per thread (the reduce-scatter is written for 8)
 
 __device__ __forceinline__ double shfl_x(double v, int m) { return __shfl_xor_sync(0xffffffffu, v, m); }
 
