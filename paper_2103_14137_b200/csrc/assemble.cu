@@ -6,11 +6,16 @@
 // irradiance units), vis = front-facing and no other scene triangle on the open
 // segment p_jl -> c_i (Q5–Q8, Q15).
 //
-//   k_assemble_lane  one warp per (column, 32 Morton-adjacent patches); every
-//                    lane walks its own shadow ray through the BVH2 (Aila &
-//                    Laine 2009 while-while, near child first, private stack),
-//                    box tests bounded by the segment's own t range, triangles
-//                    decided by an fp32 filter with forward error bounds
+//   k_assemble_lane  one warp per (column, 32 adjacent patches in the BVH's
+//                    leaf order); every lane walks its own shadow ray through the
+//                    BVH2 (Aila & Laine 2009 while-while, near child first,
+//                    private stack): the top six levels from fp16 H nodes
+//                    (hnodes.cu, HFMA2), below that the octant node copies in
+//                    the paired layout (one FFMA2 per plane pair), box tests
+//                    bounded by the segment's part outside its empty end
+//                    regions (free.cu), triangles decided by an fp32 filter with
+//                    forward error bounds; super-tiles of 2048 tiles per column
+//                    sweep when the BVH exceeds the L2
 //   k_fixup          exact fp64 re-trace of the rare entries the fp32 pass left
 //                    undecided (~1e-3 of entries), rewriting value and bits
 //   k_csc_count/fill compressed-sparse-column output from the visibility bits

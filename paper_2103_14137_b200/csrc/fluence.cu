@@ -8,6 +8,10 @@
 //   k_gemv_t    g = Aᵀ·y (the LP's adjoint product): one CTA per 4
 //               columns, float4 row chunks, y read once per 4 columns, fixed
 //               tree reduction in fp64; HBM-bound
+//   k_gemv_multi  μ = A·x, A·𝟙 and Aᵀ·y in ONE pass over A (uvd_fluence_multi,
+//               the bench step's three products): register row sums, a butterfly
+//               reduce-scatter of the column dots into per-warp partials,
+//               k_gemv_t_reduce in a fixed chunked order; HBM-bound, deterministic
 //   k_coverage  Σ|s_i|[μ_i ≥ μ_min], Σ|s_i|, Σ|s_i|[rowsum_i > 0] (P:9),
 //               fixed-shape two-level reduction
 #include <cuda_runtime.h>
