@@ -310,7 +310,7 @@ UVD_API int uvd_irradiance_matrix(const uvd_scene* scene, const float* lamp_xyz,
 /* Synchronise `stream` and report the scene's in-kernel error flag, read and
  * cleared in one device atomic: UVD_OK, UVD_ERR_DOMAIN (a lamp–centroid
  * distance < 1e-9 m), UVD_ERR_INVALID (a lamp coordinate of uvd_irradiance_matrix
- * non-finite or beyond the scene's largest |coordinate| + 50 m, the range the
+ * or uvd_cubemap_matrix non-finite or beyond the scene's largest |coordinate| + 50 m, the range the
  * BVH's fp32 box padding covers; the matrix is then not trusted), or
  * UVD_ERR_CUDA for a traversal-stack overflow (cannot
  * happen: scene creation refuses BVHs deeper than 62 levels with

@@ -844,6 +844,18 @@ __global__ void k_check_lamps(const float* __restrict__ lamps, const int64_t* __
   }
 }
 
+int check_lamps(const uvd_scene* s, const float* lamps, const int64_t* dcols, int64_t n_cols, int L, cudaStream_t st) {
+  float maxc = 0.f;
+  for (int k = 0; k < 6; ++k) maxc = std::max(maxc, std::fabs(s->bbox[k]));
+  const int64_t n = n_cols * L * 3;
+  if (n <= 0) return UVD_OK;
+  k_check_lamps<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 1024)), 256, 0, st>>>(
+      lamps, dcols, n_cols, L, maxc + 50.0f, s->err_flag);
+  note_launch();
+  UVD_CUDA_TRY(cudaGetLastError());
+  return UVD_OK;
+}
+
 // persistent grids (occupancy x SMs), cached per device and kernel
 template <typename K>
 static int persistent_grid(K kernel, int threads, int dev, int* cache) {
@@ -987,14 +999,7 @@ extern "C" int uvd_irradiance_matrix(const uvd_scene* s, const float* lamp_xyz, 
   P.hez = 0.5f * (s->bbox[5] - s->bbox[2]);
   P.front_free = s->front_free;
   if (const char* e = getenv("UVD_FREE")) if (atoi(e) == 0) P.front_free = nullptr;  // dev A/B
-  {  // lamps inside the range the box padding covers (k_check_lamps)
-    float maxc = 0.f;
-    for (int k = 0; k < 6; ++k) maxc = std::max(maxc, std::fabs(s->bbox[k]));
-    const int64_t n = n_cols * P.L * 3;
-    k_check_lamps<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 1024)), 256, 0, st>>>(
-        lamp_xyz, dcols, n_cols, P.L, maxc + 50.0f, s->err_flag);
-    note_launch();
-  }
+  UVD_TRY(check_lamps(s, lamp_xyz, dcols, n_cols, P.L, st));  // lamps inside the range the box padding covers
   if (!area_model) {
     float* lampc = (float*)sc.get((size_t)n_cols * P.L * 3 * sizeof(float));
     if (!lampc) { set_error("uvd_irradiance_matrix: out of device memory"); return UVD_ERR_NOMEM; }

@@ -289,6 +289,7 @@ extern "C" int uvd_cubemap_matrix(const uvd_scene* s, const float* lamp_xyz, int
   P.F = F;
   P.hits = hits;
   P.err = s->err_flag;
+  UVD_TRY(check_lamps(s, lamp_xyz, dcols, n_cols, P.L, st));  // the padding's lamp range (assemble.cu)
   for (int64_t c0 = 0; c0 < n_cols; c0 += chunk) {
     const int64_t nc = std::min(chunk, n_cols - c0);
     P.c0 = c0;

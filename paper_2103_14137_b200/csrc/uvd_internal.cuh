@@ -217,6 +217,8 @@ int sort_pairs_u64(uint64_t* keys, uint32_t* vals, int64_t n, Alloc& al, cudaStr
 // free.cu: empty regions at the segment ends (front radius per patch, lamp radius per sample)
 int front_radius(uvd_scene* s, cudaStream_t st);
 int lamp_radius(const uvd_scene* s, const float* lamps, int64_t n, float* out, cudaStream_t st);
+// assemble.cu: flag 3 on the scene when a lamp coordinate is outside the fp32 padding's range
+int check_lamps(const uvd_scene* s, const float* lamps, const int64_t* dcols, int64_t n_cols, int L, cudaStream_t st);
 // fluence.cu: the a7 products without allocation (uvd_lp_solve graphs them)
 Alloc matrix_alloc(const uvd_matrix_out* A, int dev, cudaStream_t st);
 size_t fluence_ws_bytes(int64_t n, int64_t k, bool csc, int dev);
