@@ -86,6 +86,9 @@ def parse():
                     help="weak scaling: every rank assembles a fixed 1/8 of the C5 configurations "
                          "(total K = N x K/8), instead of a share of the fixed full problem")
     ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--dump", default=None, metavar="PREFIX",
+                    help="after the timed region, every rank writes its A shard and visibility bits "
+                         "(uvd-shard/1: PREFIX.rank<r>.json/.bin) for tools/recheck_dump.py")
     ap.add_argument("--no-bcast", action="store_true",
                     help="N > 1: every rank builds the scene instead of rank 0 building and broadcasting it")
     return ap.parse_args()
@@ -434,6 +437,16 @@ def main():
           "achieved_gbs": a7_bytes / (a7_ms / 1e3) / 1e9, "peak_gbs": HBM_PEAK_GBS,
           "frac": a7_bytes / (a7_ms / 1e3) / 1e9 / HBM_PEAK_GBS,
           "note": "phase time includes the all_reduce for N > 1"}
+
+    if args.dump:  # per-rank shard dump for offline re-checks (outside the timed region)
+        rd = sc.irradiance(lam, cols=cols, out=A, vis_bits=True)
+        sc.sync_status()
+        hp = shard.dump_shard(args.dump, workload=args.workload, A=A, n_rows=N, cols=cols,
+                              raw=raw.cpu().numpy()[np.asarray(cols, np.int64)],
+                              lamps=lam[torch.as_tensor(cols, device=lam.device)], orig_id=sc.patches()["orig_id"],
+                              power_w=80.0, vis_bits=rd["vis_bits"], rank=rank, world=ws)
+        print(f"[bench] rank {rank}: shard dump {hp}", file=sys.stderr, flush=True)
+        del rd
 
     # parity material: the timed kernel (not the instrumented one) once more in
     # the same launch configuration, with visibility bits and the fix-up list

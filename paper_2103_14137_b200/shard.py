@@ -69,3 +69,70 @@ def broadcast_scene(desc, device=None, src: int = 0):
         img = torch.empty(int(n.item()), dtype=torch.uint8, device=dev)
     dist.broadcast(img, src)
     return sc if sc is not None else uvd.Scene.from_image(img, device=dev.index)
+
+
+# ------------------------------------------------------------- shard dumps --
+# SURVEY §5 "checkpoint / resume": every rank can write its A shard and
+# visibility bits so that parity can be re-checked offline (tools/recheck_dump.py)
+# without the GPU.  Format "uvd-shard/1" (after SPEC's binary + JSON-header
+# irradiance file): {prefix}.rank{r}.json describes the sections of the
+# raw little-endian {prefix}.rank{r}.bin; the header names the seeded workload
+# preset, so the checker regenerates the scene and the oracle's lamps itself.
+SHARD_FORMAT = "uvd-shard/1"
+
+
+def dump_shard(prefix: str, *, workload: str, A, n_rows: int, cols, raw, lamps, orig_id, power_w: float,
+               vis_bits=None, rank: int | None = None, world: int | None = None) -> str:
+    """Write this rank's shard: A (n_cols, ld) fp32 (the first n_rows of each
+    column are kept), vis_bits (n_cols, L, words) uint32 or None, the shard's
+    global column ids `cols`, their grid-candidate ids `raw`, lamp samples
+    `lamps` (n_cols, L, 3) and the row -> input-triangle map `orig_id`.
+    Tensors may be CUDA or host; returns the header path."""
+    import json
+    import numpy as np
+
+    def host(x, dt):
+        if x is None:
+            return None
+        if hasattr(x, "detach"):
+            x = x.detach().cpu().numpy()
+        return np.ascontiguousarray(np.asarray(x), dtype=dt)
+
+    if rank is None:
+        rank = dist.get_rank() if dist.is_available() and dist.is_initialized() else 0
+    if world is None:
+        world = dist.get_world_size() if dist.is_available() and dist.is_initialized() else 1
+    Ah = host(A, np.float32)[:, :n_rows]
+    secs = [("A", np.ascontiguousarray(Ah)), ("lamps", host(lamps, np.float32)), ("orig_id", host(orig_id, np.int64))]
+    if vis_bits is not None:
+        secs.append(("vis_bits", host(vis_bits, np.uint32)))
+    head = {"format": SHARD_FORMAT, "rank": int(rank), "world": int(world), "workload": workload,
+            "n_rows": int(n_rows), "n_cols": int(Ah.shape[0]), "L": int(host(lamps, np.float32).shape[1]),
+            "power_w": float(power_w), "cols": [int(c) for c in cols], "raw": [int(r) for r in host(raw, np.int64)],
+            "sections": []}
+    off = 0
+    binp = f"{prefix}.rank{rank}.bin"
+    with open(binp, "wb") as f:
+        for name, arr in secs:
+            f.write(arr.tobytes())
+            head["sections"].append({"name": name, "dtype": arr.dtype.str, "shape": list(arr.shape), "offset": off})
+            off += arr.nbytes
+    hp = f"{prefix}.rank{rank}.json"
+    with open(hp, "w") as f:
+        json.dump(head, f)
+    return hp
+
+
+def load_shard(prefix: str, rank: int = 0):
+    """(header, {section: read-only numpy memmap}) of a dump_shard file pair."""
+    import json
+    import numpy as np
+    with open(f"{prefix}.rank{rank}.json") as f:
+        head = json.load(f)
+    if head.get("format") != SHARD_FORMAT:
+        raise ValueError(f"not a {SHARD_FORMAT} header: {head.get('format')}")
+    out = {}
+    for s in head["sections"]:
+        out[s["name"]] = np.memmap(f"{prefix}.rank{rank}.bin", dtype=np.dtype(s["dtype"]), mode="r",
+                                   offset=s["offset"], shape=tuple(s["shape"]))
+    return head, out

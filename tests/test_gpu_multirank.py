@@ -103,15 +103,17 @@ def test_two_ranks_on_libuvd_match_single_process(uvd):
     assert np.array_equal(out[0]["mu"], out[1]["mu"])
 
 
-def test_bench_torchrun_gloo_dry_run(uvd):
+def test_bench_torchrun_gloo_dry_run(uvd, tmp_path):
     """bench.py's multi-rank path end to end under torchrun (2 ranks, gloo,
     one device): one JSON line from rank 0 with n_gpus = 2, max-over-ranks
-    timing and the per-rank column shard."""
+    timing and the per-rank column shard; each rank's shard dump (--dump)
+    re-checks clean against the oracle offline (tools/recheck_dump.py)."""
     env = dict(os.environ, BENCH_BACKEND="gloo")
+    prefix = str(tmp_path / "mr")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr=127.0.0.1", f"--master-port={_free_port()}", os.path.join(ROOT, "bench.py"),
            "--gpus", "2", "--steps", "2", "--warmup", "3", "--workload", "C2", "--no-cpu-baseline",
-           "--no-e2e", "--no-clocks"]
+           "--no-e2e", "--no-clocks", "--dump", prefix]
     p = subprocess.run(cmd, cwd=ROOT, env=env, capture_output=True, text=True, timeout=600)
     assert p.returncode == 0, p.stderr[-3000:]
     lines = [ln for ln in p.stdout.splitlines() if ln.startswith("{")]
@@ -119,3 +121,8 @@ def test_bench_torchrun_gloo_dry_run(uvd):
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["value"] > 0 and d["config"]["k_per_gpu"] < d["config"]["k_configs"]
     assert d["roofline"]["imbalance"] >= 1.0
+    q = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "recheck_dump.py"), prefix, "--pairs", "2000"],
+                       cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert q.returncode == 0, q.stdout[-2000:] + q.stderr[-2000:]
+    st = [json.loads(ln) for ln in q.stdout.splitlines() if ln.startswith("{")]
+    assert sorted(x["rank"] for x in st) == [0, 1] and all(x["mismatches"] == 0 for x in st)
