@@ -27,6 +27,8 @@
 // per-lane ray refill (-20 %), speculative leaf postponing (-10 %).
 #include <cuda_runtime.h>
 
+#include <cassert>
+
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
@@ -59,6 +61,7 @@ struct AsmParams {
   const float* __restrict__ lampc;  // [n_cols][L][3] lamps gathered per column (k_assemble_lane)
   const float* __restrict__ lamp_free;   // [n_cols][L] lamp radius r_L (free.cu), or nullptr
   const float* __restrict__ front_free;  // [N] front radius r_T (free.cu), or nullptr
+  int64_t n_tris;                        // leaf-ordered triangles (UVD_CHECKED bounds)
   const HNode* __restrict__ hnodes;      // 8 octant copies of the H nodes (hnodes.cu), or nullptr
   int32_t n_h;
   float hcx, hcy, hcz, hex, hey, hez;    // H coordinate origin and the scene's half extents
@@ -92,6 +95,16 @@ struct AsmParams {
 // patches, so the lanes fetch mostly the same nodes (L1 broadcast) and
 // diverge little.
 constexpr int kLaneStack = 64;
+// UVD_CHECKED=1 (test builds: the sanitizer is closed on the GPU pool): device
+// asserts on every node / triangle index, stack access and output index
+#ifndef UVD_CHECKED
+#define UVD_CHECKED 0
+#endif
+#if UVD_CHECKED
+#define UVD_CHECK(c) assert(c)
+#else
+#define UVD_CHECK(c) ((void)0)
+#endif
 constexpr uint32_t kDone = 0xffffffffu;
 
 enum { kClear = 0, kBlocked = 1, kUndecided = 2 };
@@ -147,6 +160,7 @@ __device__ __forceinline__ int lane_walk32(const AsmParams& P, float ox, float o
     while (!ref_is_leaf(ref)) {
       if (OCT && (ref & kHalfRef)) {
         // ---- H node: 32 bytes, both children per HFMA2 (hnodes.cu) ----
+        UVD_CHECK((ref & ~kHalfRef) < 8u * (uint32_t)P.n_h);
         const uint4* hq = reinterpret_cast<const uint4*>(P.hnodes + (ref & ~kHalfRef));
         const uint4 q0 = __ldg(hq), q1 = __ldg(hq + 1);
         if (COUNT) { cnt[1] += 2; cnt[3] += 1; cnt[5] += 1; }
@@ -172,6 +186,7 @@ __device__ __forceinline__ int lane_walk32(const AsmParams& P, float ox, float o
         }
         continue;
       }
+      UVD_CHECK((int64_t)ref < (OCT ? 8 : 1) * P.n_nodes);
       const Node* nd = (OCT ? P.onodes : P.nodes) + ref;
       const float4 na = __ldg(&nd->a), nb = __ldg(&nd->b), nc = __ldg(&nd->c);
       const uint2 ch = __ldg(reinterpret_cast<const uint2*>(&nd->d));
@@ -229,6 +244,7 @@ __device__ __forceinline__ int lane_walk32(const AsmParams& P, float ox, float o
     const float nD = fabsf(dx) + fabsf(dy) + fabsf(dz);
     const uint32_t st = ref_start(ref), nt = ref_count(ref);
     for (uint32_t k = 0; k < nt; ++k) {
+      UVD_CHECK((int64_t)(st + k) < P.n_tris);
       const float4* t = P.tri + 3 * (int64_t)(st + k);
       const float4 a = __ldg(t);
       if (__float_as_int(a.w) == owner) continue;  // the target's own triangles
@@ -339,6 +355,7 @@ __global__ void __launch_bounds__(kAsmThreads, kAsmMinBlocks) k_assemble_lane(As
     if (lane == 0 && tile < P.words) __stcs(P.pending + c * P.words + tile, pm);
     if (COUNT) cnt[4] += pend;
     const float a = (float)(acc * P.scale);
+    UVD_CHECK(c < P.n_cols && (int64_t)r < P.ld);
     if (P.values) __stcs(P.values + c * P.ld + r, a);  // streaming: keep the BVH in L2
   }
   if (COUNT)
@@ -602,6 +619,7 @@ __device__ bool lane_clear_exact(const AsmParams& P, float ox, float oy, float o
     if (ref_is_leaf(ref)) {
       const uint32_t st = ref_start(ref), nt = ref_count(ref);
       for (uint32_t k = 0; k < nt; ++k) {
+        UVD_CHECK((int64_t)(st + k) < P.n_tris);
         const float4* t = P.tri + 3 * (int64_t)(st + k);
         const float4 a = t[0], b = t[1], c = t[2];
         if (__float_as_int(a.w) == owner) continue;
@@ -612,6 +630,7 @@ __device__ bool lane_clear_exact(const AsmParams& P, float ox, float oy, float o
       if (!sp) return true;
       ref = stk[--sp];
     } else {
+      UVD_CHECK((int64_t)ref < P.n_nodes);
       const Node nd = P.nodes[ref];
       const float ax0 = fmaf(nd.a.x, ix, -oix), ax1 = fmaf(nd.a.y, ix, -oix);
       const float ay0 = fmaf(nd.a.z, iy, -oiy), ay1 = fmaf(nd.a.w, iy, -oiy);
@@ -993,6 +1012,7 @@ extern "C" int uvd_irradiance_matrix(const uvd_scene* s, const float* lamp_xyz, 
   P.lamp_free = nullptr;
   P.hnodes = s->hnodes;
   P.n_h = s->n_h;
+  P.n_tris = s->M;
   if (const char* e = getenv("UVD_HNODES")) if (atoi(e) == 0) P.hnodes = nullptr;  // dev A/B
   P.hcx = s->hcenter[0]; P.hcy = s->hcenter[1]; P.hcz = s->hcenter[2];
   P.hex = 0.5f * (s->bbox[3] - s->bbox[0]); P.hey = 0.5f * (s->bbox[4] - s->bbox[1]);
