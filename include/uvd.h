@@ -54,6 +54,10 @@
  *                             levels (hnodes.cu; dev A/B); UVD_HDEPTH=d builds
  *                             them for depth <= d (default 6, read by
  *                             uvd_scene_create / uvd_scene_import)
+ *   UVD_MULTI_PART_MAX=bytes  uvd_fluence_multi's scratch cap before it falls
+ *                             back to one pass per product (default 4 GB; tests)
+ *   UVD_TRACE_HOST=1          wall-clock marks of a scene build's host stages
+ *                             and allocator-callback time, to stderr (development)
  *   UVD_LP_*                  PDHG tuning knobs of uvd_lp_solve (lp.cu; they
  *                             change the iterates, not the optimum)
  * The others never change a result: every setting gives bit-identical A and
